@@ -1,0 +1,404 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 pipelined-chain broadcast (BASELINE.json metric:
+bcast latency & bus GB/s vs message size, vs ncclBroadcast).
+
+  python bench.py [--steps K] [--warmup W]                      N=1
+  torchrun --nproc-per-node N bench.py --gpus N [...]           N>1, one rank per GPU
+  python bench.py --impl reference [...]                        the reference CPU path
+
+Workloads
+  N=1  BASELINE config 1 (the reference's CPU case): 4 ranks, 64 MiB float32,
+       root 0, 512 KiB chunks, pipelined chain — the 4 ranks share cuda:0 and
+       run in one cooperative launch, so every hop is an HBM read+write.
+  N>1  the same 64 MiB / 512 KiB pipelined chain over N GPUs (one process
+       each, buffers in the CUDA-IPC symmetric heap, pulls over NVLink), plus
+       the 4 B - 1 GiB sweep with the tuned algorithm per size next to
+       torch.distributed.broadcast (NCCL) on the same buffers.
+
+Method (osu_bcast as bcastlab bench, proj/tools/bcastlab.cpp:147-206): per
+step non-root buffers are zeroed, L2 is flushed (256 MiB write), ranks meet
+at a device barrier, the broadcast is timed with CUDA events on its stream,
+every buffer is verified before the time is kept; per-step latency is the
+max over ranks. One JSON line on rank 0.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS = {}
+try:
+    PEAKS = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+except OSError:
+    pass
+HBM_PEAK = float(PEAKS.get("hbm_gbs", 6650.0))
+HBM_PEAK_SRC = "measured" if "hbm_gbs" in PEAKS else "fallback"
+LINK_BW = 900e9  # north_star chain roofline: NVLink-5 per direction per GPU
+METRIC = "bcast latency (us) & bus GB/s vs msg size 4B–1GB at 2/4/8 B200 vs ncclBroadcast"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------- CPU legs
+
+def reference_cpu(n, m, chunk, iters, warmup=1, seed=1):
+    """The reference's own CPU broadcast (oracle/_ref, unmodified bcastlab
+    sources) timed with the osu method on this host: n rank threads."""
+    harness = os.path.join(ROOT, "oracle", "_ref", "ref_harness")
+    if os.path.exists(harness):
+        out = subprocess.run([harness, "bench", "chain_pipelined", str(n), "0", str(m), str(chunk), "0",
+                              str(warmup), str(iters), "inproc", str(seed)],
+                             capture_output=True, text=True, check=True).stdout
+        r = json.loads(out)
+        return {"median_s": r["median_us"] * 1e-6, "min_s": r["min_us"] * 1e-6, "cores": n, "kind": "reference",
+                "ok": r["ok"], "iters": iters,
+                "sample": f"{iters} timed iterations (+{warmup} warm-up) of the full workload, inproc transport"}
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import _oracle as O  # the plain-C restatement (single thread)
+    payload = O.payload(seed, m)
+    times = []
+    for _ in range(iters):
+        bufs = [bytearray(m) for _ in range(n)]
+        bufs[0][:] = payload
+        t0 = time.perf_counter()
+        O.bcast("chain_pipelined", n, 0, bufs, chunk=chunk)
+        times.append(time.perf_counter() - t0)
+    return {"median_s": statistics.median(times), "min_s": min(times), "cores": 1, "kind": "port", "ok": True,
+            "iters": iters, "sample": f"{iters} iterations of the full workload through the C oracle port"}
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    n = 4 if world == 1 else world
+    m, chunk = args.bytes, args.chunk
+    iters = max(1, args.steps)
+    r = reference_cpu(n, m, chunk, iters, warmup=max(1, min(args.warmup, 2)))
+    v = m / r["median_s"] / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": world,
+            "steps": iters, "warmup": args.warmup, "ms_per_step": round(r["median_s"] * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": workload_config(n, m, chunk, world),
+            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": r["cores"], "kind": r["kind"],
+                             "sample": r["sample"]},
+            "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "correct": r["ok"]}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(n, m, chunk, world):
+    if world == 1:
+        wl = (f"BASELINE config 1: pipelined-chain bcast, {n} ranks sharing one B200 (one cooperative launch), "
+              f"{m >> 20} MiB float32 payload, root 0, {chunk >> 10} KiB chunks")
+    else:
+        wl = (f"pipelined-chain bcast over {world} B200 (one process per GPU, NVLink P2P pulls), "
+              f"{m >> 20} MiB float32, root 0, {chunk >> 10} KiB chunks; sweep 4 B-1 GiB vs NCCL")
+    return {"workload": wl, "ranks": n, "bytes": m, "chunk_bytes": chunk, "root": 0,
+            "algorithm": "chain_pipelined", "l2": "flushed between steps (256 MiB write)"}
+
+
+# ----------------------------------------------------------------- GPU legs
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--bytes", type=int, default=64 << 20)
+    ap.add_argument("--chunk", type=int, default=512 << 10)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--sweep-max", type=int, default=1 << 30)
+    ap.add_argument("--cpu-iters", type=int, default=12)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    import torch
+    if world == 1:
+        bench_single(args, torch)
+    else:
+        bench_multi(args, torch, rank, world)
+
+
+def time_steps(torch, steps, warmup, prepare, body, verify, stream):
+    """Runs warmup+steps iterations; returns the per-step body times (s)."""
+    times = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for it in range(warmup + steps):
+        prepare(it)
+        ev0.record(stream)
+        body(it)
+        ev1.record(stream)
+        ev1.synchronize()
+        if not verify(it):
+            raise RuntimeError(f"verification failed at iteration {it}")
+        if it >= warmup:
+            times.append(ev0.elapsed_time(ev1) * 1e-3)
+    return times
+
+
+def bench_single(args, torch):
+    import paper_1707_09414_b200 as B
+    n, m, chunk = 4, args.bytes, args.chunk
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    comms = B.Comm.local([0] * n, timeout_s=30)
+    cfg = B.AlgorithmConfig(B.Algorithm.chain_pipelined, 0, chunk)
+    stream = torch.cuda.Stream()
+    g = torch.Generator(device=dev).manual_seed(1)
+    bufs = [torch.zeros(m, dtype=torch.uint8, device=dev) for _ in range(n)]
+    bufs[0].copy_(torch.randint(0, 256, (m,), dtype=torch.uint8, device=dev, generator=g))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def prepare(it):
+        with torch.cuda.stream(stream):
+            for r in range(1, n):
+                bufs[r].zero_()
+            flush.fill_(it & 0xFF)
+
+    def body(it):
+        B.bcast_all(comms, bufs, m, "uint8", 0, cfg, streams=[stream] * n)
+
+    def verify(it):
+        return all(torch.equal(bufs[r], bufs[0]) for r in range(1, n))
+
+    launches0 = comms[0].launches
+    torch.cuda.synchronize()
+    with ClockSampler(0) as clk:
+        times = time_steps(torch, args.steps, args.warmup, prepare, body, verify, stream)
+    torch.cuda.synchronize()
+    launches = comms[0].launches - launches0 - args.warmup
+
+    t = statistics.mean(times)
+    busbw = m / t / 1e9
+    # Roofline of the dominant (only) kernel: every hop reads M and writes M
+    # in HBM of the one GPU: 2 (P-1) M algorithmic bytes per launch.
+    alg_bytes = 2 * (n - 1) * m
+    achieved = alg_bytes / t / 1e9
+
+    # e2e through the C-ABI with pinned host buffers (run_bcast_host).
+    hosts = [torch.empty(m, dtype=torch.uint8, pin_memory=True) for _ in range(n)]
+    hosts[0].copy_(bufs[0].cpu())
+    e2e = []
+    for it in range(args.warmup + max(3, args.steps // 2)):
+        for r in range(1, n):
+            hosts[r].zero_()
+        w = B.run_bcast_host(comms, 0, hosts, m, cfg)
+        if it >= args.warmup:
+            e2e.append(w)
+    for r in range(1, n):
+        if not torch.equal(hosts[r], hosts[0]):
+            raise RuntimeError("e2e verification failed")
+    e2e_t = statistics.mean(e2e)
+
+    cpu = reference_cpu(n, m, chunk, args.cpu_iters)
+    line = {
+        "metric": METRIC, "value": round(busbw, 2), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(t * 1e3, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (torch.randint bytes, float32-sized payload)",
+        "config": workload_config(n, m, chunk, 1),
+        "latency_us": {"mean": round(t * 1e6, 2), "min": round(min(times) * 1e6, 2),
+                       "median": round(statistics.median(times) * 1e6, 2), "max": round(max(times) * 1e6, 2)},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": HBM_PEAK, "unit": "GB/s",
+                     "frac": round(achieved / HBM_PEAK, 4), "traffic": None,
+                     "note": f"kernel bcast_kernel<16>; algorithmic bytes 2*(P-1)*M per launch; peak {HBM_PEAK_SRC}"},
+        "cpu_baseline": {"value": round(m / cpu["median_s"] / 1e9, 4), "unit": "GB/s", "cores": cpu["cores"],
+                         "kind": cpu["kind"], "sample": cpu["sample"]},
+        "e2e": {"value": round(m / e2e_t / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": m,
+                "d2h_bytes_per_step": (n - 1) * m, "latency_ms": round(e2e_t * 1e3, 3),
+                "path": "bcl_run_bcast_host (C-ABI), pinned host buffers"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def bench_multi(args, torch, rank, world):
+    import torch.distributed as dist
+    import paper_1707_09414_b200 as B
+    from paper_1707_09414_b200.comm import DevicePtr
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    m, chunk = args.bytes, args.chunk
+    sweep_max = args.sweep_max if not args.no_sweep else 0
+    heap = max(m, sweep_max) + m + (16 << 20)
+    comm = B.Comm.connect_torch(world, rank, local, heap_bytes=heap, timeout_s=30)
+    stream = torch.cuda.Stream(device=dev)
+    cap = max(m, sweep_max)
+    raw = comm.alloc(cap)
+    buf_all = torch.as_tensor(DevicePtr(raw, cap), device=dev)
+    ref_all = torch.empty(cap, dtype=torch.uint8, device=dev)
+    g = torch.Generator(device=dev).manual_seed(1)
+    ref_all.copy_(torch.randint(0, 256, (cap,), dtype=torch.uint8, device=dev, generator=g))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def run(size, steps, warmup, ours, cfg=None, flush_l2=True):
+        buf = buf_all[:size]
+        ref = ref_all[:size]
+
+        def prepare(it):
+            with torch.cuda.stream(stream):
+                if rank == 0:
+                    buf.copy_(ref)
+                else:
+                    buf.zero_()
+                if flush_l2:
+                    flush.fill_(it & 0xFF)
+                if ours:
+                    comm.barrier(stream)
+            if not ours:
+                torch.cuda.current_stream().wait_stream(stream)
+                dist.barrier(device_ids=[local])
+
+        def body(it):
+            if ours:
+                comm.bcast(buf, size, "uint8", 0, cfg, stream=stream)
+            else:
+                with torch.cuda.stream(stream):
+                    dist.broadcast(buf, src=0)
+
+        def verify(it):
+            return torch.equal(buf, ref)
+
+        times = time_steps(torch, steps, warmup, prepare, body, verify, stream)
+        t = torch.tensor(times, dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ok = torch.tensor([1.0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        return t.cpu().tolist()
+
+    cfg = B.AlgorithmConfig(B.Algorithm.chain_pipelined, 0, chunk)
+    dist.barrier(device_ids=[local])
+    launches0 = comm.launches
+    with ClockSampler(local) as clk:
+        times = run(m, args.steps, args.warmup, True, cfg)
+    launches = comm.launches - launches0 - args.warmup
+    nccl = run(m, args.steps, args.warmup, False)
+
+    # e2e through the C-ABI with pinned host buffers (bcl_bcast_host)
+    host = torch.empty(m, dtype=torch.uint8, pin_memory=True)
+    ref_host = ref_all[:m].cpu()
+    e2e = []
+    for it in range(args.warmup + max(3, args.steps // 2)):
+        if rank == 0:
+            host.copy_(ref_host)
+        else:
+            host.zero_()
+        dist.barrier(device_ids=[local])
+        t0 = time.perf_counter()
+        comm.bcast_host(host, m, "uint8", 0, cfg, stream=stream)
+        stream.synchronize()
+        w = time.perf_counter() - t0
+        if not torch.equal(host, ref_host):
+            raise RuntimeError("e2e verification failed")
+        wt = torch.tensor([w], dtype=torch.float64, device=dev)
+        dist.all_reduce(wt, op=dist.ReduceOp.MAX)
+        if it >= args.warmup:
+            e2e.append(float(wt.item()))
+    comm.reset_heap()
+    raw = comm.alloc(cap)  # same region; the e2e scratch lived above it
+
+    sweep = []
+    if sweep_max:
+        size = 4
+        while size <= sweep_max:
+            steps = 20 if size <= (16 << 20) else 8
+            c = comm.choose(size)
+            ours = run(size, steps, 3, True, None, flush_l2=False)
+            theirs = run(size, steps, 3, False, None, flush_l2=False)
+            to, tn = statistics.median(ours), statistics.median(theirs)
+            sweep.append({"bytes": size, "algorithm": c.algorithm.name, "chunk": c.chunk_bytes,
+                          "ours_us": round(to * 1e6, 2), "nccl_us": round(tn * 1e6, 2),
+                          "ours_busbw": round(size / to / 1e9, 2), "nccl_busbw": round(size / tn / 1e9, 2)})
+            size *= 2
+
+    if rank == 0:
+        t = statistics.mean(times)
+        t_nccl = statistics.mean(nccl)
+        busbw = m / t / 1e9
+        t_roof = m / LINK_BW + (world - 1) * chunk / LINK_BW
+        line = {
+            "metric": METRIC, "value": round(busbw, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t * 1e3, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic (torch.randint bytes)",
+            "config": workload_config(world, m, chunk, world),
+            "latency_us": {"mean": round(t * 1e6, 2), "min": round(min(times) * 1e6, 2),
+                           "median": round(statistics.median(times) * 1e6, 2)},
+            "nccl": {"busbw": round(m / t_nccl / 1e9, 2), "latency_us": round(t_nccl * 1e6, 2),
+                     "impl": "torch.distributed.broadcast (NCCL %s)" % ".".join(map(str, torch.cuda.nccl.version()))},
+            "roofline": {"bound": "nvlink", "achieved": round(busbw, 1), "peak": LINK_BW / 1e9, "unit": "GB/s",
+                         "frac": round(busbw / (LINK_BW / 1e9), 4), "traffic": None,
+                         "chain_roofline_us": round(t_roof * 1e6, 2), "frac_of_chain_roofline": round(t_roof / t, 4),
+                         "note": "per-GPU ingress M/t vs NVLink-5 900 GB/s per direction (north_star)"},
+            "e2e": {"value": round(m / statistics.mean(e2e) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": m,
+                    "d2h_bytes_per_step": (world - 1) * m, "latency_ms": round(statistics.mean(e2e) * 1e3, 3),
+                    "path": "bcl_bcast_host (C-ABI) per rank, pinned host buffers"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "sweep": sweep,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier(device_ids=[local])
+    comm.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,689 @@
+// bcl_comm.cpp — see bcl_comm.hpp.
+#include "bcl_comm.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cstdlib>
+#include <cstring>
+#include <sstream>
+#include <unistd.h>
+
+namespace bcl {
+
+namespace {
+
+constexpr std::uint32_t kInfoMagic = 0xB200BC57u;
+
+struct ExportInfo {
+  std::uint32_t magic;
+  std::int32_t n;
+  std::int32_t rank;
+  std::int32_t lanes;
+  std::int32_t device;
+  std::int32_t pid;
+  std::uint64_t region_bytes;
+  std::uint64_t heap_bytes;
+  cudaIpcMemHandle_t region;
+  cudaIpcMemHandle_t heap;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(e, what);
+}
+
+// Restores the caller's current device on scope exit.
+class DeviceScope {
+ public:
+  explicit DeviceScope(int dev) {
+    cudaGetDevice(&saved_);
+    if (dev != saved_) ck(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceScope() { cudaSetDevice(saved_); }
+
+ private:
+  int saved_{0};
+};
+
+std::string describe(const dev::ErrorRecord& e) {
+  std::ostringstream s;
+  if (e.code == 1) {
+    s << "device wait timed out on rank " << e.rank << " (lane " << e.lane << ", peer " << e.peer
+      << ", chunk " << e.chunk << ", observed 0x" << std::hex << e.observed << ", expected 0x"
+      << e.expected << std::dec << ")";
+  } else {
+    s << "device error code " << e.code << " on rank " << e.rank;
+  }
+  return s.str();
+}
+
+std::string format_failures(const std::vector<RankFailure>& f) {
+  std::ostringstream out;
+  out << f.size() << " rank(s) failed:";
+  for (const RankFailure& x : f) out << " [rank " << x.rank << ": " << x.message << "]";
+  return out.str();
+}
+
+}  // namespace
+
+GroupOptions GroupOptions::from_env() {
+  GroupOptions o;
+  if (const char* v = std::getenv("BCL_POLL_NS")) o.poll_ns = static_cast<std::uint32_t>(std::strtoul(v, nullptr, 10));
+  if (const char* v = std::getenv("BCL_SLICE_BYTES")) o.slice_target = std::max<std::uint64_t>(16, std::strtoull(v, nullptr, 10));
+  if (const char* v = std::getenv("BCL_MAX_CTAS")) o.max_ctas_per_rank = std::atoi(v);
+  return o;
+}
+
+std::size_t dtype_size(DataType t) {
+  switch (t) {
+    case DataType::Int8: case DataType::Uint8: return 1;
+    case DataType::Float16: case DataType::Bfloat16: return 2;
+    case DataType::Int32: case DataType::Uint32: case DataType::Float32: return 4;
+    case DataType::Int64: case DataType::Uint64: case DataType::Float64: return 8;
+  }
+  throw std::invalid_argument("unknown datatype");
+}
+
+CudaError::CudaError(cudaError_t e, const std::string& where)
+    : std::runtime_error(where + ": " + cudaGetErrorString(e)), code_(e) {}
+
+AggregateRankError::AggregateRankError(std::vector<RankFailure> failures)
+    : std::runtime_error(format_failures(failures)), failures_(std::move(failures)) {}
+
+// ----------------------------------------------------------------- creation
+
+void Group::alloc_rank(LocalRank& r, std::size_t heap_bytes) {
+  DeviceScope ds(r.device);
+  r.region_bytes = (3 * static_cast<std::size_t>(n_) * lanes_alloc_ + static_cast<std::size_t>(n_) + 1) *
+                   sizeof(std::uint64_t);
+  ck(cudaMalloc(&r.region, r.region_bytes), "cudaMalloc(region)");
+  ck(cudaMemset(r.region, 0, r.region_bytes), "cudaMemset(region)");
+  ck(cudaMalloc(&r.d_peers, sizeof(dev::PeerTable)), "cudaMalloc(peers)");
+  ck(cudaHostAlloc(&r.err_host, sizeof(dev::ErrorRecord), cudaHostAllocMapped | cudaHostAllocPortable),
+     "cudaHostAlloc(err)");
+  std::memset(r.err_host, 0, sizeof(dev::ErrorRecord));
+  ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&r.err_dev), r.err_host, 0),
+     "cudaHostGetDevicePointer");
+  // Blocking stream: ordered after work on the legacy default stream (e.g. torch
+  // fills of the buffers), as the synchronous run_bcast contract expects.
+  ck(cudaStreamCreateWithFlags(&r.stream, cudaStreamDefault), "cudaStreamCreate");
+  if (heap_bytes > 0) {
+    ck(cudaMalloc(&r.heap, heap_bytes), "cudaMalloc(heap)");
+    r.heap_bytes = heap_bytes;
+  }
+  ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+}
+
+void Group::upload_peers(LocalRank& r) {
+  DeviceScope ds(r.device);
+  ck(cudaMemcpy(r.d_peers, &r.h_peers, sizeof(dev::PeerTable), cudaMemcpyHostToDevice),
+     "cudaMemcpy(peers)");
+}
+
+namespace {
+
+int lanes_for(int device, int ranks_per_device, int cap) {
+  DeviceScope ds(device);
+  int sms = 0;
+  ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
+  int occ = 0;
+  ck(static_cast<cudaError_t>(bcast_kernel_occupancy(&occ)), "occupancy");
+  int ctas = std::min(sms, std::max(1, sms * std::max(occ, 1) / std::max(ranks_per_device, 1)));
+  if (cap > 0) ctas = std::min(ctas, cap);
+  return ctas * dev::kWarpsPerCta;
+}
+
+}  // namespace
+
+std::shared_ptr<Group> Group::create_local(const std::vector<int>& devices, const GroupOptions& opt) {
+  const int n = static_cast<int>(devices.size());
+  if (n < 1) throw std::invalid_argument("rank count must be >= 1");
+  if (n > dev::kMaxRanks) throw std::invalid_argument("at most 64 ranks");
+  std::shared_ptr<Group> g(new Group());
+  g->n_ = n;
+  g->opt_ = opt;
+  int ndev = 0;
+  ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  for (int r = 0; r < n; ++r) {
+    if (devices[static_cast<std::size_t>(r)] < 0 || devices[static_cast<std::size_t>(r)] >= ndev) {
+      throw std::invalid_argument("device id out of range");
+    }
+    g->by_device_[devices[static_cast<std::size_t>(r)]].push_back(r);
+  }
+  int rpd = 0;
+  for (const auto& kv : g->by_device_) rpd = std::max(rpd, static_cast<int>(kv.second.size()));
+  if (rpd > dev::kMaxLocal) throw std::invalid_argument("at most 16 ranks may share one GPU");
+  for (const auto& a : g->by_device_) {
+    for (const auto& b : g->by_device_) {
+      if (a.first == b.first) continue;
+      int can = 0;
+      ck(cudaDeviceCanAccessPeer(&can, a.first, b.first), "cudaDeviceCanAccessPeer");
+      if (!can) throw std::runtime_error("no peer access between devices");
+      DeviceScope ds(a.first);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(b.first, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+      } else {
+        ck(e, "cudaDeviceEnablePeerAccess");
+      }
+    }
+  }
+  g->lanes_ = lanes_for(devices[0], rpd, opt.max_ctas_per_rank);
+  g->lanes_alloc_ = g->lanes_;
+  g->single_device_ = g->by_device_.size() == 1;
+  g->local_.resize(static_cast<std::size_t>(n));
+  for (int r = 0; r < n; ++r) {
+    LocalRank& lr = g->local_[static_cast<std::size_t>(r)];
+    lr.rank = r;
+    lr.device = devices[static_cast<std::size_t>(r)];
+    g->alloc_rank(lr, 0);
+  }
+  const std::size_t S = g->region_stride();
+  for (LocalRank& lr : g->local_) {
+    for (int p = 0; p < n; ++p) {
+      std::uint64_t* base = g->local_[static_cast<std::size_t>(p)].region;
+      lr.h_peers.flags[p] = base;
+      lr.h_peers.acks[p] = base + S;
+      lr.h_peers.mbox[p] = base + 2 * S;
+      lr.h_peers.bar[p] = base + 3 * S;
+      lr.h_peers.addr_base[p] = 0;
+    }
+    g->upload_peers(lr);
+  }
+  g->connected_ = true;
+  return g;
+}
+
+std::shared_ptr<Group> Group::create_rank(int n, int rank, int device, std::size_t heap_bytes,
+                                          const GroupOptions& opt) {
+  if (n < 1 || n > dev::kMaxRanks) throw std::invalid_argument("rank count must be in [1, 64]");
+  if (rank < 0 || rank >= n) throw std::invalid_argument("rank out of range");
+  std::shared_ptr<Group> g(new Group());
+  g->n_ = n;
+  g->opt_ = opt;
+  g->ipc_ = true;
+  g->lanes_ = lanes_for(device, 1, opt.max_ctas_per_rank);
+  g->lanes_alloc_ = g->lanes_;
+  g->local_.resize(1);
+  g->local_[0].rank = rank;
+  g->local_[0].device = device;
+  g->by_device_[device].push_back(0);
+  g->alloc_rank(g->local_[0], heap_bytes);
+  return g;
+}
+
+std::vector<std::uint8_t> Group::export_info() const {
+  if (!ipc_) throw std::invalid_argument("export_info is for per-process ranks");
+  const LocalRank& r = local_[0];
+  DeviceScope ds(r.device);
+  ExportInfo info{};
+  info.magic = kInfoMagic;
+  info.n = n_;
+  info.rank = r.rank;
+  info.lanes = lanes_alloc_;
+  info.device = r.device;
+  info.pid = static_cast<std::int32_t>(getpid());
+  info.region_bytes = r.region_bytes;
+  info.heap_bytes = r.heap_bytes;
+  ck(cudaIpcGetMemHandle(&info.region, r.region), "cudaIpcGetMemHandle(region)");
+  if (r.heap) ck(cudaIpcGetMemHandle(&info.heap, r.heap), "cudaIpcGetMemHandle(heap)");
+  std::vector<std::uint8_t> out(sizeof info);
+  std::memcpy(out.data(), &info, sizeof info);
+  return out;
+}
+
+void Group::connect(const std::vector<std::vector<std::uint8_t>>& infos) {
+  if (!ipc_) throw std::invalid_argument("connect is for per-process ranks");
+  if (connected_) throw std::invalid_argument("already connected");
+  if (static_cast<int>(infos.size()) != n_) throw std::invalid_argument("one info blob per rank required");
+  std::vector<ExportInfo> all(infos.size());
+  int lanes = lanes_alloc_;
+  for (std::size_t i = 0; i < infos.size(); ++i) {
+    if (infos[i].size() < sizeof(ExportInfo)) throw std::invalid_argument("truncated info blob");
+    std::memcpy(&all[i], infos[i].data(), sizeof(ExportInfo));
+    if (all[i].magic != kInfoMagic || all[i].n != n_ || all[i].rank != static_cast<int>(i)) {
+      throw std::invalid_argument("info blobs must be ordered by rank and belong to this group");
+    }
+    lanes = std::min(lanes, static_cast<int>(all[i].lanes));
+  }
+  lanes_ = lanes;
+  LocalRank& me = local_[0];
+  DeviceScope ds(me.device);
+  const std::size_t S = region_stride();
+  for (int p = 0; p < n_; ++p) {
+    std::uint64_t* base = nullptr;
+    std::uint64_t heap_base = 0;
+    if (p == me.rank) {
+      base = me.region;
+      heap_base = reinterpret_cast<std::uint64_t>(me.heap);
+    } else {
+      void* ptr = nullptr;
+      ck(cudaIpcOpenMemHandle(&ptr, all[static_cast<std::size_t>(p)].region,
+                              cudaIpcMemLazyEnablePeerAccess),
+         "cudaIpcOpenMemHandle(region)");
+      me.opened.push_back(ptr);
+      base = static_cast<std::uint64_t*>(ptr);
+      if (all[static_cast<std::size_t>(p)].heap_bytes > 0) {
+        void* h = nullptr;
+        ck(cudaIpcOpenMemHandle(&h, all[static_cast<std::size_t>(p)].heap,
+                                cudaIpcMemLazyEnablePeerAccess),
+           "cudaIpcOpenMemHandle(heap)");
+        me.opened.push_back(h);
+        heap_base = reinterpret_cast<std::uint64_t>(h);
+      }
+    }
+    me.h_peers.flags[p] = base;
+    me.h_peers.acks[p] = base + S;
+    me.h_peers.mbox[p] = base + 2 * S;
+    me.h_peers.bar[p] = base + 3 * S;
+    me.h_peers.addr_base[p] = heap_base;
+  }
+  upload_peers(me);
+  connected_ = true;
+}
+
+Group::~Group() {
+  for (LocalRank& r : local_) {
+    cudaSetDevice(r.device);
+    cudaDeviceSynchronize();
+    for (void* p : r.opened) cudaIpcCloseMemHandle(p);
+    if (r.region) cudaFree(r.region);
+    if (r.d_peers) cudaFree(r.d_peers);
+    if (r.heap) cudaFree(r.heap);
+    if (r.scratch && !ipc_) cudaFree(r.scratch);
+    if (r.err_host) cudaFreeHost(r.err_host);
+    if (r.stream) cudaStreamDestroy(r.stream);
+  }
+}
+
+int Group::local_index_of(int rank) const {
+  for (std::size_t i = 0; i < local_.size(); ++i) {
+    if (local_[i].rank == rank) return static_cast<int>(i);
+  }
+  return -1;
+}
+
+// ------------------------------------------------------------------ tables
+
+void Group::set_table(const TuningTable& t) {
+  if (t.entries.empty()) throw std::invalid_argument("tuning table is empty");
+  table_ = t;
+  have_table_ = true;
+}
+void Group::clear_table() { have_table_ = false; }
+const TuningTable& Group::table() const { return have_table_ ? table_ : builtin_table(); }
+
+// `bcast --algo auto` semantics: select per size, clamp the chunk to the
+// message (bcastlab.cpp:258-266).
+AlgorithmConfig Group::choose(std::uint64_t bytes, const AlgorithmConfig* cfg) const {
+  if (cfg) return *cfg;
+  AlgorithmConfig c = select(table(), n_, bytes);
+  if (c.algorithm == Algorithm::ChainPipelined) {
+    c.chunk_bytes = std::clamp<std::uint64_t>(c.chunk_bytes, 1, std::max<std::uint64_t>(bytes, 1));
+  }
+  return c;
+}
+
+// ------------------------------------------------------------------ plans
+
+CallPlan Group::plan(const AlgorithmConfig& cfg, int root, std::uint64_t bytes) {
+  const auto key = std::make_tuple(static_cast<int>(cfg.algorithm), cfg.radix_k, cfg.chunk_bytes, root, bytes);
+  {
+    std::lock_guard<std::mutex> lock(plan_mu_);
+    auto it = plans_.find(key);
+    if (it != plans_.end()) return *it->second;
+  }
+  cfg.validate();
+  auto p = std::make_shared<CallPlan>();
+  p->config = cfg;
+  const std::uint64_t nn = static_cast<std::uint64_t>(n_);
+  std::uint64_t max_len = bytes;
+  Schedule sched;
+  if (cfg.algorithm == Algorithm::ChainPipelined) {
+    if (root < 0 || root >= n_) throw std::invalid_argument("root out of range");
+    if (n_ < 2) throw std::invalid_argument("pipelined chain needs at least 2 ranks");
+    const std::uint64_t k = bytes == 0 ? 1 : (bytes + cfg.chunk_bytes - 1) / cfg.chunk_bytes;
+    if (k > 0xFFFFFFFFull) throw std::invalid_argument("too many chunks");
+    p->implicit_chain = true;
+    p->chunk_mode = dev::kFixedChunks;
+    p->n_chunks = static_cast<std::uint32_t>(k);
+    p->chunk_bytes = cfg.chunk_bytes;
+    max_len = std::min(cfg.chunk_bytes, bytes);
+  } else {
+    sched = make_schedule(cfg, n_, root, bytes);
+    p->n_chunks = static_cast<std::uint32_t>(sched.chunks.size());
+    if (cfg.algorithm == Algorithm::ScatterRingAllgather) {
+      p->chunk_mode = dev::kPartitions;
+      max_len = (bytes + nn - 1) / nn;
+    } else {
+      p->chunk_mode = dev::kWholeMessage;
+    }
+    p->chunk_bytes = max_len;
+  }
+  // Slices per chunk: the smallest divisor of L giving <= slice_target bytes.
+  const std::uint64_t want = std::max<std::uint64_t>(1, (max_len + opt_.slice_target - 1) / opt_.slice_target);
+  int q = lanes_;
+  for (int d = 1; d <= lanes_; ++d) {
+    if (lanes_ % d == 0 && static_cast<std::uint64_t>(d) >= want) { q = d; break; }
+  }
+  p->slices = q;
+  const std::uint64_t per = (max_len + static_cast<std::uint64_t>(q) - 1) / static_cast<std::uint64_t>(q);
+  p->slice_bytes = std::max<std::uint64_t>(16, (per + 15) / 16 * 16);
+  const int ns = lanes_ / q;
+  const std::uint64_t active = std::min<std::uint64_t>(static_cast<std::uint64_t>(ns), p->n_chunks) *
+                               static_cast<std::uint64_t>(q);
+  p->ctas = static_cast<int>((active + dev::kWarpsPerCta - 1) / dev::kWarpsPerCta);
+  if (!p->implicit_chain) {
+    p->events.resize(static_cast<std::size_t>(n_));
+    for (int r = 0; r < n_; ++r) {
+      const auto& ops = sched.per_rank_ops[static_cast<std::size_t>(r)];
+      if (ops.size() > static_cast<std::size_t>(dev::kMaxEvents)) {
+        throw std::invalid_argument("schedule has more events per rank than the device executor holds");
+      }
+      std::map<std::tuple<int, int, std::uint32_t>, std::uint32_t> seen;  // (kind, peer, class)
+      for (const Event& e : ops) {
+        const bool rv = e.kind == Event::Kind::Recv;
+        const std::uint32_t cls = e.chunk % static_cast<std::uint32_t>(ns);
+        const std::uint32_t idx = seen[{rv ? 1 : 0, e.peer, cls}]++;
+        p->events[static_cast<std::size_t>(r)].push_back(dev::pack_event(rv, e.peer, e.chunk, idx));
+      }
+    }
+  }
+  std::lock_guard<std::mutex> lock(plan_mu_);
+  if (plans_.size() > 256) plans_.clear();
+  plans_[key] = p;
+  return *p;
+}
+
+// ---------------------------------------------------------------- launches
+
+void Group::fill_rank_work(dev::RankWork& w, LocalRank& r, const CallPlan& p, void* buf) {
+  const std::size_t S = region_stride();
+  w.rank = r.rank;
+  w.n_events = p.implicit_chain ? -1 : static_cast<int>(p.events[static_cast<std::size_t>(r.rank)].size());
+  w.buf = static_cast<std::uint8_t*>(buf);
+  w.pub = ipc_ ? static_cast<std::uint64_t>(static_cast<std::uint8_t*>(buf) - r.heap)
+               : reinterpret_cast<std::uint64_t>(buf);
+  w.flags = r.region;
+  w.acks = r.region + S;
+  w.mbox = r.region + 2 * S;
+  w.peers = r.d_peers;
+  w.err = r.err_dev;
+  w.abort = reinterpret_cast<int*>(r.region + 3 * S + static_cast<std::size_t>(n_));
+  w.prov = r.prov;
+  w.trace = r.trace;
+  w.trace_cap = r.trace_cap;
+  if (!p.implicit_chain) {
+    const auto& ev = p.events[static_cast<std::size_t>(r.rank)];
+    std::copy(ev.begin(), ev.end(), w.events);
+  }
+}
+
+void Group::launch_group(const std::vector<int>& locals, const std::vector<void*>& bufs,
+                         std::uint64_t bytes, int root, const CallPlan& p, cudaStream_t stream) {
+  dev::LaunchParams P{};
+  P.n_ranks = n_;
+  P.root = root;
+  P.n_local = static_cast<int>(locals.size());
+  P.lanes = lanes_;
+  P.slices = p.slices;
+  P.ctas_per_rank = p.ctas;
+  P.chunk_mode = p.chunk_mode;
+  P.n_chunks = p.n_chunks;
+  P.bytes = bytes;
+  P.chunk_bytes = p.chunk_bytes;
+  P.slice_bytes = p.slice_bytes;
+  P.timeout_ns = opt_.timeout_ns;
+  P.poll_ns = opt_.poll_ns;
+  P.sys_scope = single_device_ ? 0 : 1;
+  std::uint64_t epoch = 0;
+  for (std::size_t i = 0; i < locals.size(); ++i) {
+    LocalRank& r = local_[static_cast<std::size_t>(locals[i])];
+    const std::uint64_t e = ++r.epoch;
+    if (i == 0) epoch = e;
+    if (e != epoch) throw std::runtime_error("ranks sharing a GPU drifted apart in call count");
+    fill_rank_work(P.ranks[i], r, p, bufs[i]);
+    ++r.launches;
+  }
+  P.epoch = epoch;
+  DeviceScope ds(local_[static_cast<std::size_t>(locals[0])].device);
+  ck(static_cast<cudaError_t>(launch_bcast(P, P.n_local > 1 ? 1 : 0, stream)), "launch(bcast)");
+}
+
+void Group::bcast(int li, void* buf, std::uint64_t bytes, int root, const AlgorithmConfig* cfg,
+                  cudaStream_t stream) {
+  if (broken_) throw std::runtime_error("communicator is unusable after a device failure");
+  if (!connected_) throw std::invalid_argument("communicator is not connected");
+  if (root < 0 || root >= n_) throw std::invalid_argument("root out of range");
+  LocalRank& r = local_.at(static_cast<std::size_t>(li));
+  if (by_device_.at(r.device).size() > 1) {
+    throw std::invalid_argument("ranks sharing a GPU must be driven together (bcast_all)");
+  }
+  if (bytes > 0 && buf == nullptr) throw std::invalid_argument("null buffer");
+  if (ipc_ && bytes > 0) {
+    const auto* b = static_cast<std::uint8_t*>(buf);
+    if (b < r.heap || b + bytes > r.heap + r.heap_bytes) {
+      throw std::invalid_argument("per-process ranks need buffers from bcl_mem_alloc");
+    }
+  }
+  const AlgorithmConfig c = choose(bytes, cfg);
+  const CallPlan p = plan(c, root, bytes);
+  if (n_ == 1) return;  // nothing moves (reference: n = 1 leaves the buffer untouched)
+  launch_group({li}, {buf}, bytes, root, p, stream);
+}
+
+void Group::bcast_all(const std::vector<void*>& bufs, std::uint64_t bytes, int root,
+                      const AlgorithmConfig* cfg, const std::vector<cudaStream_t>& streams) {
+  if (broken_) throw std::runtime_error("communicator is unusable after a device failure");
+  if (bufs.size() != local_.size()) throw std::invalid_argument("one buffer per rank required");
+  if (!streams.empty() && streams.size() != local_.size()) {
+    throw std::invalid_argument("one stream per rank (or none)");
+  }
+  if (root < 0 || root >= n_) throw std::invalid_argument("root out of range");
+  for (void* b : bufs) {
+    if (bytes > 0 && b == nullptr) throw std::invalid_argument("null buffer");
+  }
+  const AlgorithmConfig c = choose(bytes, cfg);
+  const CallPlan p = plan(c, root, bytes);
+  if (n_ == 1) return;
+  for (const auto& kv : by_device_) {
+    std::vector<void*> b;
+    for (int li : kv.second) b.push_back(bufs[static_cast<std::size_t>(li)]);
+    const int first = kv.second.front();
+    cudaStream_t s = streams.empty() ? local_[static_cast<std::size_t>(first)].stream
+                                     : streams[static_cast<std::size_t>(first)];
+    launch_group(kv.second, b, bytes, root, p, s);
+  }
+}
+
+void Group::bcast_host(int li, void* host_buf, std::uint64_t bytes, int root,
+                       const AlgorithmConfig* cfg, cudaStream_t stream) {
+  LocalRank& r = local_.at(static_cast<std::size_t>(li));
+  DeviceScope ds(r.device);
+  if (bytes > r.scratch_bytes) {
+    if (ipc_) {
+      r.scratch = static_cast<std::uint8_t*>(mem_alloc(li, bytes));
+    } else {
+      if (r.scratch) ck(cudaFree(r.scratch), "cudaFree(scratch)");
+      ck(cudaMalloc(&r.scratch, bytes), "cudaMalloc(scratch)");
+    }
+    r.scratch_bytes = bytes;
+  }
+  if (r.rank == root && bytes > 0) {
+    ck(cudaMemcpyAsync(r.scratch, host_buf, bytes, cudaMemcpyHostToDevice, stream), "H2D");
+  }
+  bcast(li, r.scratch, bytes, root, cfg, stream);
+  if (r.rank != root && bytes > 0) {
+    ck(cudaMemcpyAsync(host_buf, r.scratch, bytes, cudaMemcpyDeviceToHost, stream), "D2H");
+  }
+}
+
+void Group::raise_errors(const std::vector<int>& locals) {
+  std::vector<RankFailure> f;
+  for (int li : locals) {
+    const dev::ErrorRecord& e = *local_[static_cast<std::size_t>(li)].err_host;
+    if (e.code != 0) f.push_back(RankFailure{local_[static_cast<std::size_t>(li)].rank, describe(e)});
+  }
+  if (f.empty()) return;
+  broken_ = true;
+  if (f.size() == 1) throw DeviceTimeout(f.front().message);
+  throw AggregateRankError(std::move(f));
+}
+
+void Group::check(int li, cudaStream_t stream) {
+  LocalRank& r = local_.at(static_cast<std::size_t>(li));
+  DeviceScope ds(r.device);
+  ck(stream ? cudaStreamSynchronize(stream) : cudaDeviceSynchronize(), "synchronize");
+  raise_errors({li});
+}
+
+double Group::run_bcast(const std::vector<void*>& bufs, std::uint64_t bytes, int root,
+                        const AlgorithmConfig* cfg) {
+  if (static_cast<int>(bufs.size()) != n_ || local_count() != n_) {
+    throw std::invalid_argument("one buffer per rank required");
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  bcast_all(bufs, bytes, root, cfg, {});
+  std::vector<int> all;
+  for (const auto& kv : by_device_) {
+    DeviceScope ds(kv.first);
+    ck(cudaStreamSynchronize(local_[static_cast<std::size_t>(kv.second.front())].stream), "synchronize");
+    all.insert(all.end(), kv.second.begin(), kv.second.end());
+  }
+  const auto t1 = std::chrono::steady_clock::now();
+  std::vector<RankFailure> f;
+  for (int li : all) {
+    const dev::ErrorRecord& e = *local_[static_cast<std::size_t>(li)].err_host;
+    if (e.code != 0) f.push_back(RankFailure{local_[static_cast<std::size_t>(li)].rank, describe(e)});
+  }
+  if (!f.empty()) {
+    broken_ = true;
+    throw AggregateRankError(std::move(f));
+  }
+  return std::chrono::duration<double>(t1 - t0).count();
+}
+
+double Group::run_bcast_host(const std::vector<void*>& host_bufs, std::uint64_t bytes, int root,
+                             const AlgorithmConfig* cfg) {
+  if (static_cast<int>(host_bufs.size()) != n_ || local_count() != n_) {
+    throw std::invalid_argument("one buffer per rank required");
+  }
+  for (LocalRank& r : local_) {
+    if (bytes > r.scratch_bytes) {
+      DeviceScope ds(r.device);
+      if (r.scratch) ck(cudaFree(r.scratch), "cudaFree(scratch)");
+      ck(cudaMalloc(&r.scratch, bytes), "cudaMalloc(scratch)");
+      r.scratch_bytes = bytes;
+    }
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  const int root_li = local_index_of(root);
+  if (root_li < 0) throw std::invalid_argument("root out of range");
+  const int root_dev = local_[static_cast<std::size_t>(root_li)].device;
+  cudaStream_t root_stream = local_[static_cast<std::size_t>(by_device_.at(root_dev).front())].stream;
+  if (bytes > 0) {
+    DeviceScope ds(root_dev);
+    ck(cudaMemcpyAsync(local_[static_cast<std::size_t>(root_li)].scratch, host_bufs[static_cast<std::size_t>(root)],
+                       bytes, cudaMemcpyHostToDevice, root_stream), "H2D");
+  }
+  std::vector<void*> dbufs;
+  for (LocalRank& r : local_) dbufs.push_back(r.scratch);
+  bcast_all(dbufs, bytes, root, cfg, {});
+  for (const auto& kv : by_device_) {
+    DeviceScope ds(kv.first);
+    cudaStream_t s = local_[static_cast<std::size_t>(kv.second.front())].stream;
+    for (int li : kv.second) {
+      LocalRank& r = local_[static_cast<std::size_t>(li)];
+      if (r.rank != root && bytes > 0) {
+        ck(cudaMemcpyAsync(host_bufs[static_cast<std::size_t>(r.rank)], r.scratch, bytes,
+                           cudaMemcpyDeviceToHost, s), "D2H");
+      }
+    }
+  }
+  std::vector<int> all;
+  for (const auto& kv : by_device_) {
+    DeviceScope ds(kv.first);
+    ck(cudaStreamSynchronize(local_[static_cast<std::size_t>(kv.second.front())].stream), "synchronize");
+    all.insert(all.end(), kv.second.begin(), kv.second.end());
+  }
+  const auto t1 = std::chrono::steady_clock::now();
+  std::vector<RankFailure> f;
+  for (int li : all) {
+    const dev::ErrorRecord& e = *local_[static_cast<std::size_t>(li)].err_host;
+    if (e.code != 0) f.push_back(RankFailure{local_[static_cast<std::size_t>(li)].rank, describe(e)});
+  }
+  if (!f.empty()) {
+    broken_ = true;
+    throw AggregateRankError(std::move(f));
+  }
+  return std::chrono::duration<double>(t1 - t0).count();
+}
+
+void Group::barrier(int li, cudaStream_t stream) {
+  LocalRank& r = local_.at(static_cast<std::size_t>(li));
+  if (by_device_.at(r.device).size() > 1) {
+    throw std::invalid_argument("ranks sharing a GPU must use barrier_all");
+  }
+  dev::BarrierParams B{};
+  B.n_ranks = n_;
+  B.n_local = 1;
+  B.epoch = ++r.bar_epoch;
+  B.timeout_ns = opt_.timeout_ns;
+  B.rank[0] = r.rank;
+  B.bar[0] = r.region + 3 * region_stride();
+  B.peers[0] = r.d_peers;
+  B.err[0] = r.err_dev;
+  DeviceScope ds(r.device);
+  ck(static_cast<cudaError_t>(launch_barrier(B, stream)), "launch(barrier)");
+}
+
+void Group::barrier_all(const std::vector<cudaStream_t>& streams) {
+  for (const auto& kv : by_device_) {
+    dev::BarrierParams B{};
+    B.n_ranks = n_;
+    B.n_local = static_cast<int>(kv.second.size());
+    B.timeout_ns = opt_.timeout_ns;
+    for (std::size_t i = 0; i < kv.second.size(); ++i) {
+      LocalRank& r = local_[static_cast<std::size_t>(kv.second[i])];
+      B.epoch = ++r.bar_epoch;
+      B.rank[i] = r.rank;
+      B.bar[i] = r.region + 3 * region_stride();
+      B.peers[i] = r.d_peers;
+      B.err[i] = r.err_dev;
+    }
+    const int first = kv.second.front();
+    cudaStream_t s = streams.empty() ? local_[static_cast<std::size_t>(first)].stream
+                                     : streams[static_cast<std::size_t>(first)];
+    DeviceScope ds(kv.first);
+    ck(static_cast<cudaError_t>(launch_barrier(B, s)), "launch(barrier)");
+  }
+}
+
+void* Group::mem_alloc(int li, std::size_t bytes) {
+  LocalRank& r = local_.at(static_cast<std::size_t>(li));
+  if (!r.heap) throw std::invalid_argument("this communicator has no symmetric heap");
+  const std::size_t at = (r.heap_used + 255) / 256 * 256;
+  if (at + bytes > r.heap_bytes) throw std::invalid_argument("symmetric heap exhausted");
+  r.heap_used = at + bytes;
+  return r.heap + at;
+}
+
+void Group::mem_reset(int li) {
+  LocalRank& r = local_.at(static_cast<std::size_t>(li));
+  r.heap_used = 0;
+  r.scratch = nullptr;
+  r.scratch_bytes = 0;
+}
+
+void Group::set_provenance(int li, unsigned long long* counters) {
+  local_.at(static_cast<std::size_t>(li)).prov = counters;
+}
+
+void Group::set_trace(int li, unsigned long long* records, std::uint32_t per_lane) {
+  LocalRank& r = local_.at(static_cast<std::size_t>(li));
+  r.trace = records;
+  r.trace_cap = records ? per_lane : 0;
+}
+
+std::uint64_t Group::launches(int li) const { return local_.at(static_cast<std::size_t>(li)).launches; }
+
+}  // namespace bcl

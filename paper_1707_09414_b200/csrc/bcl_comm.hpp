@@ -1,0 +1,190 @@
+// bcl_comm: the B200 replacement of the reference's TransportFabric /
+// run_bcast / execute_rank boundary (proj/include/bcastlab/runtime.hpp:20-143).
+//
+//   Group         owns the device state of the ranks this process drives:
+//                 per-rank flag/ack/mailbox region, the peer table, the call
+//                 epoch and host-mapped error records. Two ways to build one:
+//                 * create_local(devices): one process drives every rank, one
+//                   rank per entry of `devices` (UVA + peer access; several
+//                   ranks may share a GPU — they then run in one launch);
+//                 * create_rank(n, rank, device, heap): one process per GPU;
+//                   export_info()/connect() swap CUDA IPC handles (the caller
+//                   moves the bytes, e.g. with torch.distributed).
+//   bcast()       per-rank MPI_Bcast-shaped call, enqueued on a stream.
+//   bcast_all()   every local rank, one launch per GPU (required when ranks
+//                 share a GPU: waiting kernels must be co-resident).
+//   run_bcast()   synchronous all-ranks call with wall time, the mirror of
+//                 run_bcast (runtime.cpp:66-103); run_bcast_host() takes host
+//                 buffers (H2D at the root, D2H at the others).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "bcl_core.hpp"
+#include "bcl_device.cuh"
+#include "bcl_tuner.hpp"
+
+namespace bcl {
+
+enum class DataType : int {
+  Int8 = 0, Uint8, Int32, Uint32, Int64, Uint64, Float16, Float32, Float64, Bfloat16,
+};
+std::size_t dtype_size(DataType t);
+
+class CudaError : public std::runtime_error {
+ public:
+  CudaError(cudaError_t e, const std::string& where);
+  cudaError_t code() const { return code_; }
+
+ private:
+  cudaError_t code_;
+};
+
+class DeviceTimeout : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+struct RankFailure {
+  int rank{};
+  std::string message;
+};
+
+// Mirrors AggregateRankError (runtime.hpp:51-63).
+class AggregateRankError : public std::runtime_error {
+ public:
+  explicit AggregateRankError(std::vector<RankFailure> failures);
+  const std::vector<RankFailure>& failures() const { return failures_; }
+
+ private:
+  std::vector<RankFailure> failures_;
+};
+
+struct GroupOptions {
+  std::uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;  // device spin bound
+  std::uint64_t slice_target = 16384;                       // bytes per lane per chunk
+  int max_ctas_per_rank = 0;                                // 0 = SM count
+  std::uint32_t poll_ns = 64;                               // back-off between flag polls (ns)
+  static GroupOptions from_env();                           // BCL_* overrides (tuning runs)
+};
+
+// What one call does on the device, derived identically on every rank.
+struct CallPlan {
+  AlgorithmConfig config;
+  std::uint32_t chunk_mode{};
+  std::uint32_t n_chunks{};
+  std::uint64_t chunk_bytes{};
+  int slices{};                 // Q
+  std::uint64_t slice_bytes{};
+  int ctas{};                   // CTAs per rank actually launched
+  bool implicit_chain{};
+  std::vector<std::vector<std::uint64_t>> events;  // [rank] packed (explicit only)
+};
+
+struct LocalRank {
+  int rank{-1};
+  int device{-1};
+  std::uint64_t* region{};      // flags | acks | mbox | bar
+  std::size_t region_bytes{};
+  dev::PeerTable* d_peers{};
+  dev::PeerTable h_peers{};
+  dev::ErrorRecord* err_host{};
+  dev::ErrorRecord* err_dev{};
+  std::uint64_t epoch{0};
+  std::uint64_t bar_epoch{0};
+  std::uint8_t* heap{};
+  std::size_t heap_bytes{};
+  std::size_t heap_used{};
+  std::uint8_t* scratch{};      // device staging for host-buffer calls
+  std::size_t scratch_bytes{};
+  cudaStream_t stream{};        // internal stream for run_bcast
+  unsigned long long* prov{};   // optional provenance counters
+  unsigned long long* trace{};  // optional per-lane event timestamps
+  std::uint32_t trace_cap{0};
+  std::uint64_t launches{0};
+  std::vector<void*> opened;    // IPC mappings to close
+};
+
+class Group {
+ public:
+  static std::shared_ptr<Group> create_local(const std::vector<int>& devices,
+                                             const GroupOptions& opt = {});
+  static std::shared_ptr<Group> create_rank(int n, int rank, int device,
+                                            std::size_t heap_bytes,
+                                            const GroupOptions& opt = {});
+  ~Group();
+
+  // Multi-process wiring (create_rank only).
+  std::vector<std::uint8_t> export_info() const;
+  void connect(const std::vector<std::vector<std::uint8_t>>& infos);
+
+  int n_ranks() const { return n_; }
+  int lanes() const { return lanes_; }
+  bool ipc() const { return ipc_; }
+  int local_count() const { return static_cast<int>(local_.size()); }
+  LocalRank& local(int i) { return local_.at(static_cast<std::size_t>(i)); }
+  int local_index_of(int rank) const;
+
+  void set_table(const TuningTable& t);
+  void clear_table();
+  const TuningTable& table() const;
+  AlgorithmConfig choose(std::uint64_t bytes, const AlgorithmConfig* cfg) const;
+  CallPlan plan(const AlgorithmConfig& cfg, int root, std::uint64_t bytes);
+
+  void* mem_alloc(int local_index, std::size_t bytes);
+  void mem_reset(int local_index);
+
+  void bcast(int local_index, void* buf, std::uint64_t bytes, int root,
+             const AlgorithmConfig* cfg, cudaStream_t stream);
+  void bcast_all(const std::vector<void*>& bufs, std::uint64_t bytes, int root,
+                 const AlgorithmConfig* cfg, const std::vector<cudaStream_t>& streams);
+  void bcast_host(int local_index, void* host_buf, std::uint64_t bytes, int root,
+                  const AlgorithmConfig* cfg, cudaStream_t stream);
+  double run_bcast(const std::vector<void*>& bufs, std::uint64_t bytes, int root,
+                   const AlgorithmConfig* cfg);
+  double run_bcast_host(const std::vector<void*>& host_bufs, std::uint64_t bytes,
+                        int root, const AlgorithmConfig* cfg);
+  void barrier(int local_index, cudaStream_t stream);
+  void barrier_all(const std::vector<cudaStream_t>& streams);
+  // Synchronizes `stream` (or the device) and raises the first device error.
+  void check(int local_index, cudaStream_t stream);
+  void set_provenance(int local_index, unsigned long long* counters);
+  void set_trace(int local_index, unsigned long long* records, std::uint32_t per_lane);
+  std::uint64_t launches(int local_index) const;
+
+ private:
+  Group() = default;
+  void alloc_rank(LocalRank& r, std::size_t heap_bytes);
+  void upload_peers(LocalRank& r);
+  void fill_rank_work(dev::RankWork& w, LocalRank& r, const CallPlan& p, void* buf);
+  void launch_group(const std::vector<int>& locals, const std::vector<void*>& bufs,
+                    std::uint64_t bytes, int root, const CallPlan& p, cudaStream_t stream);
+  void raise_errors(const std::vector<int>& locals);
+  std::size_t region_stride() const { return static_cast<std::size_t>(n_) * lanes_; }
+
+  int n_{0};
+  int lanes_{0};
+  int lanes_alloc_{0};
+  bool ipc_{false};
+  bool single_device_{false};  // every rank on one GPU: gpu-scope ordering suffices
+  bool connected_{false};
+  bool broken_{false};
+  GroupOptions opt_;
+  std::vector<LocalRank> local_;
+  std::map<int, std::vector<int>> by_device_;
+  TuningTable table_;
+  bool have_table_{false};
+  std::mutex plan_mu_;
+  std::map<std::tuple<int, int, std::uint64_t, int, std::uint64_t>, std::shared_ptr<CallPlan>> plans_;
+};
+
+}  // namespace bcl

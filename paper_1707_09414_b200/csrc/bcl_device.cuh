@@ -1,0 +1,126 @@
+// bcl_device.cuh — the host/device contract of the broadcast executor.
+//
+// The per-rank copy/forward loop of the reference (execute_rank,
+// proj/src/runtime.cpp:32-64) runs on the GPU as a set of independent
+// *lanes* (one warp each). A chunk is cut into Q slices; lane l serves slice
+// (l % Q) of every chunk c with c % (L/Q) == l / Q, walking the rank's event
+// list in order. A Recv(peer, c) waits for the peer's per-lane ready counter
+// to reach this pull's index, then copies the slice straight out of the
+// peer's buffer (NVLink P2P load, or a local load when ranks share a GPU); a
+// Send(peer, c) release-stores this lane's counter into the peer's flag
+// array. Because sender and receiver filter the same per-pair ordered event
+// sequence with the same lane predicate, the i-th send of lane l to d is the
+// i-th receive of lane l at d from the sender: one monotone 64-bit counter per
+// (src, lane) suffices, tagged with the call epoch in its upper 32 bits so
+// flags never need resetting. Consumers ack after their last pull so the
+// producer's kernel cannot finish (and its buffer cannot be reused) while a
+// downstream lane still reads it.
+#pragma once
+
+#include <cstdint>
+
+namespace bcl {
+namespace dev {
+
+constexpr int kMaxLocal = 16;    // ranks served by one launch (ranks sharing a GPU)
+constexpr int kMaxEvents = 64;   // explicit per-rank event list (trees, SRA)
+constexpr int kMaxRanks = 64;    // communicator size limit
+constexpr int kWarpsPerCta = 8;  // lanes per CTA
+constexpr int kThreads = kWarpsPerCta * 32;
+
+// Explicit event word: chunk (bits 0-23) | peer (24-30) | recv (31) |
+// pair index within the lane class (32-55).
+__host__ __device__ inline std::uint64_t pack_event(bool recv, int peer, std::uint32_t chunk,
+                                                    std::uint32_t pidx) {
+  return static_cast<std::uint64_t>(chunk & 0xFFFFFFu) |
+         (static_cast<std::uint64_t>(peer & 0x7F) << 24) |
+         (static_cast<std::uint64_t>(recv ? 1u : 0u) << 31) |
+         (static_cast<std::uint64_t>(pidx & 0xFFFFFFu) << 32);
+}
+
+enum ChunkMode : std::uint32_t {
+  kWholeMessage = 0,  // one chunk = the message (direct, chain, knomial)
+  kFixedChunks = 1,   // make_chunks(M, C) (chain_pipelined)
+  kPartitions = 2,    // partition_chunks(n, M) (scatter_ring_allgather)
+};
+
+// Addresses of every peer's state as mapped in *this* rank's address space.
+// Region layout of a rank: flags[n][L] | acks[n][L] | mbox[n][L] | bar[n] | abort.
+struct PeerTable {
+  std::uint64_t* flags[kMaxRanks];  // peer's flags array (index [my_rank][lane])
+  std::uint64_t* acks[kMaxRanks];   // peer's acks array  (index [my_rank][lane])
+  std::uint64_t* mbox[kMaxRanks];   // peer's mailbox     (index [my_rank][lane])
+  std::uint64_t* bar[kMaxRanks];    // peer's barrier slots (index [my_rank])
+  std::uint64_t addr_base[kMaxRanks];  // added to a mailbox value from that peer
+};
+
+struct ErrorRecord {  // host-mapped, written by the first failing lane
+  int code;           // 0 ok, 1 timeout, 2 aborted
+  int rank;
+  int peer;
+  int lane;
+  unsigned long long chunk;
+  unsigned long long observed;
+  unsigned long long expected;
+};
+
+struct RankWork {
+  int rank;                      // global rank id
+  int n_events;                  // explicit list length; -1 = implicit pipelined chain
+  std::uint8_t* buf;             // this rank's buffer (device)
+  std::uint64_t pub;             // mailbox value naming buf to consumers
+  std::uint64_t* flags;          // local flags[n][L]
+  std::uint64_t* acks;           // local acks[n][L]
+  std::uint64_t* mbox;           // local mbox[n][L]
+  const PeerTable* peers;        // device-resident
+  ErrorRecord* err;              // host-mapped error record of this rank (written once, on failure)
+  int* abort;                    // device-memory abort word polled by waiting lanes
+  unsigned long long* prov;      // optional provenance: bytes pulled per [src][chunk]
+  unsigned long long* trace;     // optional timeline: [lane][trace_cap][4] globaltimer stamps
+  std::uint32_t trace_cap;
+  std::uint64_t events[kMaxEvents];
+};
+
+// Launch parameters for a launch serving NL ranks. NL = 1 (one rank per GPU,
+// the production shape) keeps the parameter block small for launch latency;
+// NL = kMaxLocal serves ranks that share a GPU (emulation, tests).
+template <int NL>
+struct LaunchParamsT {
+  int n_ranks;
+  int root;
+  int n_local;
+  int lanes;          // L: lanes per rank (identical on every rank of the comm)
+  int slices;         // Q: slices per chunk, divides L
+  int ctas_per_rank;  // CTAs launched per local rank (active lanes only)
+  std::uint32_t chunk_mode;
+  std::uint32_t n_chunks;
+  std::uint64_t bytes;
+  std::uint64_t chunk_bytes;
+  std::uint64_t slice_bytes;  // multiple of 16
+  std::uint64_t epoch;        // >= 1, per call
+  std::uint64_t timeout_ns;
+  std::uint32_t poll_ns;      // __nanosleep between polls (0 = spin)
+  std::uint32_t sys_scope;    // 1: peers on other GPUs (fence.sys); 0: one GPU (fence.gpu)
+  RankWork ranks[NL];
+};
+using LaunchParams = LaunchParamsT<kMaxLocal>;
+
+struct BarrierParams {
+  int n_ranks;
+  int n_local;
+  std::uint64_t epoch;
+  std::uint64_t timeout_ns;
+  int rank[kMaxLocal];
+  std::uint64_t* bar[kMaxLocal];        // local barrier slots
+  const PeerTable* peers[kMaxLocal];
+  ErrorRecord* err[kMaxLocal];
+};
+
+}  // namespace dev
+
+// Launchers (bcl_kernels.cu). Return cudaError_t as int.
+int launch_bcast(const dev::LaunchParams& p, int cooperative, void* stream);
+int launch_barrier(const dev::BarrierParams& p, void* stream);
+int bcast_kernel_occupancy(int* blocks_per_sm);
+
+}  // namespace bcl

@@ -1,0 +1,401 @@
+// bcl_kernels.cu — sm_100a broadcast executor (see bcl_device.cuh).
+//
+// One launch per GPU serves every rank that GPU hosts (normally one). Each
+// warp is a lane: it owns slice q = lane % Q of the chunks c with
+// c % (L/Q) == lane / Q and walks the rank's schedule, pulling those slices
+// from its upstream peer's buffer with 16-byte vector loads as soon as the
+// peer's per-lane counter says they are ready, then publishing its own counter
+// to its downstream peers (release at system scope). Data never leaves HBM /
+// NVLink: no staging buffers, no cudaMemcpy, no NCCL.
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <cstring>
+
+#include "bcl_device.cuh"
+
+namespace bcl {
+namespace dev {
+namespace {
+
+__device__ __forceinline__ std::uint64_t ld_relaxed_sys(const std::uint64_t* p) {
+  std::uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ std::uint64_t ld_acquire_sys(const std::uint64_t* p) {
+  std::uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys(std::uint64_t* p, std::uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_sys() {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+__device__ __forceinline__ std::uint64_t globaltimer() {
+  std::uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ std::uint8_t ld_u8(const std::uint8_t* p) {
+  unsigned short v;
+  asm volatile("ld.global.L1::no_allocate.u8 %0, [%1];" : "=h"(v) : "l"(p));
+  return static_cast<std::uint8_t>(v);
+}
+__device__ __forceinline__ uint4 ld_v4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_v4(uint4* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+// Header fields shared by every LaunchParamsT<NL> (the ranks[] tail differs).
+struct Ctx {
+  const LaunchParamsT<1>* P;
+  const RankWork* W;
+  int lane_id;   // 0..31
+  int ell;       // lane (warp) index within the rank
+};
+
+// Record the first failure of this rank; every lane then drains out.
+__device__ void fail(const Ctx& c, int code, int peer, std::uint64_t chunk, std::uint64_t seen,
+                     std::uint64_t want) {
+  ErrorRecord* e = c.W->err;
+  atomicExch(c.W->abort, 1);
+  if (atomicCAS(&e->code, 0, code) == 0) {
+    e->rank = c.W->rank;
+    e->peer = peer;
+    e->lane = c.ell;
+    e->chunk = chunk;
+    e->observed = seen;
+    e->expected = want;
+    __threadfence_system();
+  }
+}
+
+// Warp-wide wait until *p >= target. Lane 0 polls (relaxed), then every
+// thread performs its own acquire so its later loads observe the producer's
+// data. Returns false on timeout/abort.
+__device__ bool wait_geq(const Ctx& c, const std::uint64_t* p, std::uint64_t target, int peer,
+                         std::uint64_t chunk) {
+  int ok = 1;
+  if (c.lane_id == 0) {
+    std::uint64_t v = ld_relaxed_sys(p);
+    if (v < target) {
+      const std::uint64_t t0 = globaltimer();
+      unsigned spins = 0;
+      while ((v = ld_relaxed_sys(p)) < target) {
+        if (c.P->poll_ns) __nanosleep(c.P->poll_ns);
+        if ((++spins & 255u) == 0) {
+          if (*(volatile int*)c.W->abort != 0) { ok = 0; break; }
+          if (globaltimer() - t0 > c.P->timeout_ns) {
+            fail(c, 1, peer, chunk, v, target);
+            ok = 0;
+            break;
+          }
+        }
+      }
+    }
+  }
+  ok = __shfl_sync(0xffffffffu, ok, 0);
+  if (ok) (void)ld_acquire_sys(p);
+  __syncwarp();
+  return ok != 0;
+}
+
+// Publish a counter / ack after this warp's preceding stores: warp barrier,
+// then lane 0 issues a system-scope release store.
+__device__ __forceinline__ void publish(const Ctx& c, std::uint64_t* p, std::uint64_t v) {
+  __syncwarp();
+  if (c.lane_id == 0) {
+    if (c.P->sys_scope) fence_acq_rel_sys(); else fence_acq_rel_gpu();
+    st_relaxed_sys(p, v);
+  }
+  __syncwarp();
+}
+
+// Warp copy of bytes [lo, hi) from src to dst (same offsets in both buffers).
+__device__ void warp_copy(const Ctx& c, const std::uint8_t* src, std::uint8_t* dst,
+                          std::uint64_t lo, std::uint64_t hi) {
+  if (hi <= lo) return;
+  const int t = c.lane_id;
+  const std::uintptr_t s0 = reinterpret_cast<std::uintptr_t>(src + lo);
+  const std::uintptr_t d0 = reinterpret_cast<std::uintptr_t>(dst + lo);
+  if (((s0 ^ d0) & 15u) != 0) {
+    for (std::uint64_t i = lo + t; i < hi; i += 32) dst[i] = ld_u8(src + i);
+    return;
+  }
+  // head up to the first 16-byte boundary, vector body, byte tail
+  const std::uint64_t head = ((16u - (d0 & 15u)) & 15u);
+  const std::uint64_t body_lo = lo + (head < hi - lo ? head : hi - lo);
+  if (t < static_cast<int>(body_lo - lo)) dst[lo + t] = ld_u8(src + lo + t);
+  const std::uint64_t nvec = (hi - body_lo) / 16;
+  const uint4* vs = reinterpret_cast<const uint4*>(src + body_lo);
+  uint4* vd = reinterpret_cast<uint4*>(dst + body_lo);
+  constexpr int U = 8;
+  std::uint64_t i = t;
+  for (; i + (U - 1) * 32 < nvec; i += U * 32) {
+    uint4 r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) r[u] = ld_v4(vs + i + u * 32);
+#pragma unroll
+    for (int u = 0; u < U; ++u) st_v4(vd + i + u * 32, r[u]);
+  }
+  for (; i < nvec; i += 32) st_v4(vd + i, ld_v4(vs + i));
+  const std::uint64_t tail_lo = body_lo + nvec * 16;
+  if (tail_lo + t < hi) dst[tail_lo + t] = ld_u8(src + tail_lo + t);
+}
+
+__device__ __forceinline__ void chunk_range(const LaunchParamsT<1>& P, std::uint32_t ch,
+                                            std::uint64_t* off, std::uint64_t* len) {
+  if (P.chunk_mode == kFixedChunks) {
+    *off = static_cast<std::uint64_t>(ch) * P.chunk_bytes;
+    *len = P.bytes - *off < P.chunk_bytes ? P.bytes - *off : P.chunk_bytes;
+  } else if (P.chunk_mode == kPartitions) {
+    const std::uint64_t n = static_cast<std::uint64_t>(P.n_ranks);
+    const std::uint64_t base = P.bytes / n, rem = P.bytes % n;
+    *off = ch * base + (ch < rem ? ch : rem);
+    *len = base + (ch < rem ? 1 : 0);
+  } else {
+    *off = 0;
+    *len = P.bytes;
+  }
+}
+
+__device__ __forceinline__ void pull_slice(const Ctx& c, std::uint32_t ch, int q,
+                                           const std::uint8_t* src, int src_rank) {
+  std::uint64_t off, len;
+  chunk_range(*c.P, ch, &off, &len);
+  const std::uint64_t lo = static_cast<std::uint64_t>(q) * c.P->slice_bytes;
+  if (lo >= len) return;
+  const std::uint64_t hi = lo + c.P->slice_bytes < len ? lo + c.P->slice_bytes : len;
+  warp_copy(c, src, c.W->buf, off + lo, off + hi);
+  if (c.W->prov != nullptr && c.lane_id == 0) {
+    atomicAdd(&c.W->prov[static_cast<std::uint64_t>(src_rank) * c.P->n_chunks + ch],
+              static_cast<unsigned long long>(hi - lo));
+  }
+}
+
+// Implicit pipelined chain (schedule_chain_pipelined, schedules.cpp:161-187):
+// logical rank l pulls from l-1 and serves l+1.
+__device__ void run_chain(const Ctx& c, int pipe, int q, int ns) {
+  const LaunchParamsT<1>& P = *c.P;
+  const RankWork& W = *c.W;
+  const int n = P.n_ranks;
+  const int L = P.lanes;
+  const int me = W.rank;
+  const int logical = (me - P.root + n) % n;
+  const int prev = (me + n - 1) % n;
+  const int next = (me + 1) % n;
+  const bool has_prev = logical > 0;
+  const bool has_next = logical + 1 < n;
+  const std::uint32_t K = P.n_chunks;
+  if (static_cast<std::uint32_t>(pipe) >= K) return;
+  const std::uint32_t mine = (K - 1 - pipe) / ns + 1;
+  const std::uint64_t tag = P.epoch << 32;
+  const std::size_t slot = static_cast<std::size_t>(me) * L + c.ell;
+
+  if (has_next && c.lane_id == 0) st_relaxed_sys(W.peers->mbox[next] + slot, W.pub);
+  if (!has_prev) {
+    publish(c, W.peers->flags[next] + slot, tag | mine);  // the head owns every chunk
+  } else {
+    const std::uint64_t* ready = W.flags + static_cast<std::size_t>(prev) * L + c.ell;
+    const std::uint8_t* src = nullptr;
+    std::uint32_t published = 0;
+    for (std::uint32_t k = 0; k < mine; ++k) {
+      // Forward what we hold before blocking on the next chunk.
+      if (has_next && published < k) {
+        publish(c, W.peers->flags[next] + slot, tag | k);
+        published = k;
+      }
+      const std::uint64_t t_wait = W.trace ? globaltimer() : 0;
+      if (!wait_geq(c, ready, tag | (k + 1), prev, pipe + static_cast<std::uint64_t>(k) * ns)) return;
+      const std::uint64_t t_ready = W.trace ? globaltimer() : 0;
+      if (k == 0) {
+        src = reinterpret_cast<const std::uint8_t*>(
+            W.peers->addr_base[prev] + ld_relaxed_sys(W.mbox + static_cast<std::size_t>(prev) * L + c.ell));
+      }
+      pull_slice(c, pipe + k * ns, q, src, prev);
+      if (W.trace && c.lane_id == 0 && k + 1 < W.trace_cap) {
+        unsigned long long* rec = W.trace + (static_cast<std::size_t>(c.ell) * W.trace_cap + k) * 4;
+        rec[0] = t_wait;
+        rec[1] = t_ready;
+        rec[2] = globaltimer();
+        rec[3] = 0;
+      }
+    }
+    if (has_next) publish(c, W.peers->flags[next] + slot, tag | mine);
+    publish(c, W.peers->acks[prev] + slot, P.epoch);  // done reading prev's buffer
+  }
+  if (W.trace && c.lane_id == 0 && W.trace_cap > 0) {
+    W.trace[(static_cast<std::size_t>(c.ell) * W.trace_cap + W.trace_cap - 1) * 4 + 1] = globaltimer();
+  }
+  if (has_next) {
+    (void)wait_geq(c, W.acks + static_cast<std::size_t>(next) * L + c.ell, P.epoch, next, K);
+  }
+}
+
+// Explicit schedule (direct, chain, knomial, scatter_ring_allgather): walk
+// the rank's event list, keeping the events of this lane's chunk class.
+__device__ void run_events(const Ctx& c, int pipe, int q, int ns) {
+  const LaunchParamsT<1>& P = *c.P;
+  const RankWork& W = *c.W;
+  const int L = P.lanes;
+  const std::size_t slot = static_cast<std::size_t>(W.rank) * L + c.ell;
+  const std::uint64_t tag = P.epoch << 32;
+  std::uint64_t sent_mask = 0, recv_mask = 0;
+  // Announce our buffer to every peer this lane will serve.
+  for (int i = 0; i < W.n_events; ++i) {
+    const std::uint64_t ev = W.events[i];
+    const std::uint32_t ch = static_cast<std::uint32_t>(ev & 0xFFFFFFu);
+    if ((ev >> 31) & 1u) continue;
+    if (static_cast<int>(ch % ns) != pipe) continue;
+    const int peer = static_cast<int>((ev >> 24) & 0x7F);
+    if (!((sent_mask >> peer) & 1u)) {
+      sent_mask |= 1ull << peer;
+      if (c.lane_id == 0) st_relaxed_sys(W.peers->mbox[peer] + slot, W.pub);
+    }
+  }
+  const std::uint8_t* src_of[kMaxRanks];
+  for (int i = 0; i < W.n_events; ++i) {
+    const std::uint64_t ev = W.events[i];
+    const std::uint32_t ch = static_cast<std::uint32_t>(ev & 0xFFFFFFu);
+    if (static_cast<int>(ch % ns) != pipe) continue;
+    const int peer = static_cast<int>((ev >> 24) & 0x7F);
+    const bool is_recv = (ev >> 31) & 1u;
+    const std::uint64_t idx = ((ev >> 32) & 0xFFFFFFu) + 1;
+    if (is_recv) {
+      const std::uint64_t* ready = W.flags + static_cast<std::size_t>(peer) * L + c.ell;
+      if (!wait_geq(c, ready, tag | idx, peer, ch)) return;
+      if (!((recv_mask >> peer) & 1u)) {
+        recv_mask |= 1ull << peer;
+        src_of[peer] = reinterpret_cast<const std::uint8_t*>(
+            W.peers->addr_base[peer] + ld_relaxed_sys(W.mbox + static_cast<std::size_t>(peer) * L + c.ell));
+      }
+      pull_slice(c, ch, q, src_of[peer], peer);
+    } else {
+      publish(c, W.peers->flags[peer] + slot, tag | idx);
+    }
+  }
+  for (std::uint64_t m = recv_mask; m; m &= m - 1) {
+    publish(c, W.peers->acks[__ffsll(static_cast<long long>(m)) - 1] + slot, P.epoch);
+  }
+  for (std::uint64_t m = sent_mask; m; m &= m - 1) {
+    const int peer = __ffsll(static_cast<long long>(m)) - 1;
+    if (!wait_geq(c, W.acks + static_cast<std::size_t>(peer) * L + c.ell, P.epoch, peer, 0)) return;
+  }
+}
+
+template <int NL>
+__global__ void __launch_bounds__(kThreads) bcast_kernel(const __grid_constant__ LaunchParamsT<NL> P) {
+  const int local = NL == 1 ? 0 : static_cast<int>(blockIdx.x) / P.ctas_per_rank;
+  const int cta = NL == 1 ? static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x) % P.ctas_per_rank;
+  Ctx c;
+  c.P = reinterpret_cast<const LaunchParamsT<1>*>(&P);
+  c.W = &P.ranks[local];
+  c.lane_id = threadIdx.x & 31;
+  c.ell = cta * kWarpsPerCta + (threadIdx.x >> 5);
+  if (c.ell >= P.lanes) return;
+  const int ns = P.lanes / P.slices;
+  const int pipe = c.ell / P.slices;
+  const int q = c.ell % P.slices;
+  const std::uint64_t t_enter = c.W->trace ? globaltimer() : 0;
+  if (c.W->n_events < 0) {
+    run_chain(c, pipe, q, ns);
+  } else {
+    run_events(c, pipe, q, ns);
+  }
+  if (c.W->trace && c.lane_id == 0 && c.W->trace_cap > 0) {
+    unsigned long long* rec = c.W->trace + (static_cast<std::size_t>(c.ell) * c.W->trace_cap + c.W->trace_cap - 1) * 4;
+    rec[0] = t_enter;
+    rec[3] = globaltimer();
+  }
+}
+
+// All-ranks barrier: rank r bumps slot [r] in every peer, then waits for
+// every peer's bump in its own slots.
+__global__ void barrier_kernel(const __grid_constant__ BarrierParams B) {
+  const int local = blockIdx.x;
+  const int t = threadIdx.x;
+  const int me = B.rank[local];
+  const PeerTable* peers = B.peers[local];
+  if (t < B.n_ranks && t != me) {
+    fence_acq_rel_sys();
+    st_relaxed_sys(peers->bar[t] + me, B.epoch);
+  }
+  __syncthreads();
+  if (t < B.n_ranks && t != me) {
+    const std::uint64_t* slot = B.bar[local] + t;
+    const std::uint64_t t0 = globaltimer();
+    while (ld_relaxed_sys(slot) < B.epoch) {
+      if (globaltimer() - t0 > B.timeout_ns) {
+        ErrorRecord* e = B.err[local];
+        if (atomicCAS(&e->code, 0, 1) == 0) {
+          e->rank = me;
+          e->peer = t;
+          e->lane = -1;
+          e->expected = B.epoch;
+          __threadfence_system();
+        }
+        break;
+      }
+    }
+    (void)ld_acquire_sys(slot);
+  }
+  __syncthreads();
+}
+
+}  // namespace
+}  // namespace dev
+
+int launch_bcast(const dev::LaunchParams& p, int cooperative, void* stream) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(p.n_local * p.ctas_per_rank));
+  cfg.blockDim = dim3(dev::kThreads);
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = cooperative ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (p.n_local == 1) {
+    // Same header layout; copy the header and the single rank into the small block.
+    dev::LaunchParamsT<1> one;
+    std::memcpy(&one, &p, offsetof(dev::LaunchParams, ranks));
+    one.ranks[0] = p.ranks[0];
+    return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::bcast_kernel<1>, one));
+  }
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::bcast_kernel<dev::kMaxLocal>, p));
+}
+
+int launch_barrier(const dev::BarrierParams& p, void* stream) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(p.n_local));
+  cfg.blockDim = dim3(dev::kMaxRanks);
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = p.n_local > 1 ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::barrier_kernel, p));
+}
+
+int bcast_kernel_occupancy(int* blocks_per_sm) {
+  return static_cast<int>(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      blocks_per_sm, dev::bcast_kernel<dev::kMaxLocal>, dev::kThreads, 0));
+}
+
+}  // namespace bcl

@@ -1,0 +1,239 @@
+"""GPU parity: the device broadcast vs the CPU oracle, bit-exact.
+
+All ranks share cuda:0 here (one cooperative launch serves them), so the same
+flag protocol, lane plan and copy code as the multi-GPU path run on one B200;
+tests/test_multigpu.py repeats the key cases across real GPUs. Cases follow
+the reference's own tests: acceptance criterion 4's random trials
+(proj/tests/acceptance.cpp:190-233) via the committed golden list, the
+runtime tests (proj/tests/test_runtime.cpp:99-254) and edge cases (empty,
+ragged, misaligned, C not dividing M, every root).
+"""
+import json
+import os
+import random
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import _oracle as O  # noqa: E402
+import paper_1707_09414_b200 as B  # noqa: E402
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_golden.json")))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    yield
+    torch.cuda.synchronize()
+
+
+_GROUPS = {}
+
+
+def comms_for(n):
+    """One emulated group per rank count, reused across tests (epochs advance)."""
+    if n not in _GROUPS:
+        _GROUPS[n] = B.Comm.local([0] * n, timeout_s=10)
+    return _GROUPS[n]
+
+
+def cfg_of(algo, chunk=0, radix=0):
+    a = B.Algorithm[algo]
+    return B.AlgorithmConfig(a, radix if a in (B.Algorithm.knomial, B.Algorithm.knomial_staged) else 0,
+                             chunk if a == B.Algorithm.chain_pipelined else 0)
+
+
+def make_bufs(n, m, root, payload, offsets=None):
+    """Device buffers (optionally at byte offsets into larger allocations)."""
+    offsets = offsets or [0] * n
+    store = [torch.zeros(m + 64, dtype=torch.uint8, device="cuda:0") for _ in range(n)]
+    views = [store[r][offsets[r]:offsets[r] + m] for r in range(n)]
+    if m:
+        views[root].copy_(torch.frombuffer(bytearray(payload), dtype=torch.uint8))
+    return store, views
+
+
+def run_case(algo, n, root, m, chunk=0, radix=0, seed=1, offsets=None):
+    payload = O.payload(seed, m)
+    expect = [bytearray(m) for _ in range(n)]
+    expect[root][:] = payload
+    O.bcast(algo, n, root, expect, chunk=chunk, radix=radix)
+    _, views = make_bufs(n, m, root, payload, offsets)
+    B.run_bcast(comms_for(n), root, views, m, cfg_of(algo, chunk, radix))
+    for r in range(n):
+        got = views[r].cpu().numpy().tobytes()
+        assert got == bytes(expect[r]), f"{algo} n={n} root={root} M={m} C={chunk}: rank {r} differs"
+
+
+@pytest.mark.parametrize("idx", range(len(GOLD["bcasts"])))
+def test_reference_trials_bit_exact(idx):
+    """Every golden trial: device result == reference result (FNV per rank)."""
+    algo, n, root, m, chunk, radix, seed = GOLD["bcasts"][idx]["case"]
+    if algo == "chain_pipelined" and n < 2:
+        pytest.skip("n < 2")
+    payload = O.payload(seed, m)
+    _, views = make_bufs(n, m, root, payload)
+    B.run_bcast(comms_for(n), root, views, m, cfg_of(algo, chunk, radix))
+    got = ["%016x" % O.fnv(views[r].cpu().numpy().tobytes()) for r in range(n)]
+    assert got == GOLD["bcasts"][idx]["rank_fnv"]
+
+
+@pytest.mark.parametrize("algo", ["direct", "chain", "knomial", "scatter_ring_allgather",
+                                  "chain_pipelined", "knomial_staged"])
+@pytest.mark.parametrize("m", [0, 1, 4, 15, 16, 17, 1000, 4096, 65537])
+def test_every_root_small_sizes(algo, m):
+    for n in (2, 3, 5, 8):
+        for root in range(n):
+            run_case(algo, n, root, m, chunk=max(1, m // 3 + 1) if m else 7, radix=2 + root % 3,
+                     seed=m * 31 + root)
+
+
+def test_chunk_not_dividing_message_and_tiny_chunks():
+    # C in [1, M+1] as acceptance.cpp:203-205 draws it.
+    rng = random.Random(5)
+    for _ in range(20):
+        n = rng.randrange(2, 9)
+        m = rng.randrange(0, 300000)
+        chunk = 1 + rng.randrange(m + 1)
+        if (m + chunk - 1) // max(chunk, 1) > 200000:
+            chunk = m // 200000 + 1
+        run_case("chain_pipelined", n, rng.randrange(n), m, chunk=chunk, seed=rng.randrange(1 << 30))
+
+
+def test_misaligned_buffers():
+    """Different byte misalignments per rank (vector and byte paths)."""
+    for offs in ([0, 1, 2, 3], [5, 5, 5, 5], [16, 3, 0, 9]):
+        for algo in ("chain_pipelined", "knomial", "scatter_ring_allgather"):
+            run_case(algo, 4, 1, 100003, chunk=8191, radix=2, seed=11, offsets=offs)
+
+
+def test_sixteen_ranks_one_megabyte():
+    # proj/tests/test_runtime.cpp:224-236 shape.
+    run_case("chain_pipelined", 16, 0, 1 << 20, chunk=65536, seed=99)
+    run_case("scatter_ring_allgather", 16, 5, 1 << 20, seed=98)
+
+
+def test_config1_full_size_all_ranks_equal_root():
+    """BASELINE config 1 at full size: 4 ranks, 64 MiB, 512 KiB chunks."""
+    n, m, chunk = 4, 64 << 20, 512 << 10
+    g = torch.Generator(device="cuda:0").manual_seed(1)
+    bufs = [torch.zeros(m, dtype=torch.uint8, device="cuda:0") for _ in range(n)]
+    bufs[0].copy_(torch.randint(0, 256, (m,), dtype=torch.uint8, device="cuda:0", generator=g))
+    B.run_bcast(comms_for(n), 0, bufs, m, cfg_of("chain_pipelined", chunk))
+    for r in range(1, n):
+        assert torch.equal(bufs[r], bufs[0])
+
+
+def test_back_to_back_calls_change_payload_and_root():
+    """Epoch stress: buffers reused immediately, roots and payloads vary."""
+    n, m = 4, 3 << 20
+    comms = comms_for(n)
+    bufs = [torch.zeros(m, dtype=torch.uint8, device="cuda:0") for _ in range(n)]
+    for it in range(40):
+        root = it % n
+        bufs[root].fill_(it + 1)
+        algo = ["chain_pipelined", "knomial", "scatter_ring_allgather", "direct"][it % 4]
+        B.bcast_all(comms, bufs, m, "uint8", root, cfg_of(algo, 262144 + it, 2))
+        if it % 7 == 6:
+            torch.cuda.synchronize()
+            for r in range(n):
+                assert int(bufs[r].min()) == it + 1 == int(bufs[r].max()), (it, r)
+    torch.cuda.synchronize()
+    for c in comms:
+        c.check()
+
+
+def test_provenance_matches_schedule_sends():
+    """Schedule fidelity (test_runtime.cpp:121-161): every (src, dst, chunk)
+    pull happened once and moved exactly the chunk's bytes."""
+    n, m = 6, 50000
+    for algo, chunk in (("scatter_ring_allgather", 0), ("chain_pipelined", 7000), ("knomial", 0)):
+        cfg = cfg_of(algo, chunk, 2)
+        sched = B.make_schedule(cfg, n, 2, m)
+        k = len(sched.chunks)
+        comms = comms_for(n)
+        prov = [torch.zeros(n * k, dtype=torch.int64, device="cuda:0") for _ in range(n)]
+        for r in range(n):
+            comms[r].set_provenance(prov[r])
+        payload = O.payload(3, m)
+        _, views = make_bufs(n, m, 2, payload)
+        B.run_bcast(comms, 2, views, m, cfg)
+        for r in range(n):
+            comms[r].set_provenance(None)
+        expected = {}
+        for src, ops in enumerate(sched.per_rank_ops):
+            for e in ops:
+                if e.kind == "send":
+                    expected[(src, e.peer, e.chunk)] = sched.chunks[e.chunk].length_bytes
+        got = {}
+        for dst in range(n):
+            cnt = prov[dst].view(n, k).cpu()
+            for src in range(n):
+                for c in range(k):
+                    if int(cnt[src, c]):
+                        got[(src, dst, c)] = int(cnt[src, c])
+        expected = {key: v for key, v in expected.items() if v}
+        assert got == expected, algo
+
+
+def test_auto_config_uses_table_select():
+    n = 4
+    comms = comms_for(n)
+    for m in (4, 4096, 1 << 20, 8 << 20):
+        want = B.select(B.builtin_table(), n, m)
+        got = comms[0].choose(m)
+        assert got.algorithm == want.algorithm
+        if want.algorithm == B.Algorithm.chain_pipelined:
+            assert got.chunk_bytes == max(1, min(want.chunk_bytes, max(m, 1)))
+        payload = O.payload(m, m)
+        _, views = make_bufs(n, m, 3, payload)
+        B.bcast_all(comms, views, m, "uint8", 3, None)
+        torch.cuda.synchronize()
+        for r in range(n):
+            assert views[r].cpu().numpy().tobytes() == payload
+
+
+def test_dtype_count_and_nan_payloads_are_bit_exact():
+    """float32 payloads holding NaN / denormal bit patterns move untouched."""
+    n, count = 4, 1 << 18
+    comms = comms_for(n)
+    bits = torch.randint(-(1 << 31), (1 << 31) - 1, (count,), dtype=torch.int32, device="cuda:0")
+    bits[::7] = 0x7FC00001  # NaN with payload
+    bits[1::11] = 0x00000001  # denormal
+    bufs = [torch.zeros(count, dtype=torch.float32, device="cuda:0") for _ in range(n)]
+    bufs[2].copy_(bits.view(torch.float32))
+    B.bcast_all(comms, bufs, count, "float32", 2, cfg_of("chain_pipelined", 65536))
+    torch.cuda.synchronize()
+    for r in range(n):
+        assert torch.equal(bufs[r].view(torch.int32), bits)
+
+
+def test_host_buffer_run_bcast():
+    n, m = 4, 777777
+    comms = B.Comm.local([0] * n, timeout_s=10)
+    payload = O.payload(4, m)
+    hosts = [bytearray(m) for _ in range(n)]
+    hosts[1][:] = payload
+    wall = B.run_bcast_host(comms, 1, hosts, m, cfg_of("chain_pipelined", 131072))
+    assert wall > 0
+    for r in range(n):
+        assert bytes(hosts[r]) == payload
+
+
+def test_contract_errors():
+    comms = comms_for(2)
+    buf = torch.zeros(16, dtype=torch.uint8, device="cuda:0")
+    with pytest.raises(ValueError):
+        B.bcast_all(comms, [buf, buf], 16, "uint8", 2, cfg_of("chain"))  # root out of range
+    with pytest.raises(ValueError):
+        B.bcast_all(comms, [buf, buf], 16, "uint8", 0, B.AlgorithmConfig(B.Algorithm.chain_pipelined, 0, 0))
+    with pytest.raises(ValueError):
+        comms[0].bcast(buf, 16, "uint8", 0, cfg_of("chain"))  # ranks share a GPU: per-rank call refused
+    one = B.Comm.local([0])
+    with pytest.raises(ValueError):  # schedules.cpp:164-166
+        B.run_bcast(one, 0, [buf], 16, cfg_of("chain_pipelined", 4))
+    B.run_bcast(one, 0, [buf], 16, cfg_of("chain"))  # n = 1: untouched, no error

@@ -1,0 +1,134 @@
+"""Multi-GPU parity (needs >= 2 visible B200s; skipped otherwise).
+
+* one process driving every GPU (UVA + peer access): all algorithms, roots;
+* 2 ranks per GPU on the available GPUs (8 ranks on 4 GPUs);
+* one process per GPU over CUDA IPC (the bench.py shape), spawned here with
+  a gloo rendezvous for the handle exchange;
+* a rank that never joins makes its peers time out with a named error.
+"""
+import os
+import random
+import socket
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import _oracle as O  # noqa: E402
+import paper_1707_09414_b200 as B  # noqa: E402
+
+
+def ngpu():
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+needs2 = pytest.mark.skipif(ngpu() < 2, reason="needs >= 2 GPUs")
+
+
+def cfg_of(algo, chunk=0, radix=0):
+    a = B.Algorithm[algo]
+    return B.AlgorithmConfig(a, radix if a in (B.Algorithm.knomial, B.Algorithm.knomial_staged) else 0,
+                             chunk if a == B.Algorithm.chain_pipelined else 0)
+
+
+def run_group(comms, devices, algo, root, m, chunk=0, radix=2, seed=1):
+    n = len(devices)
+    payload = O.payload(seed, m)
+    expect = [bytearray(m) for _ in range(n)]
+    expect[root][:] = payload
+    O.bcast(algo, n, root, expect, chunk=chunk, radix=radix)
+    bufs = [torch.zeros(m, dtype=torch.uint8, device=f"cuda:{d}") for d in devices]
+    if m:
+        bufs[root].copy_(torch.frombuffer(bytearray(payload), dtype=torch.uint8))
+    B.run_bcast(comms, root, bufs, m, cfg_of(algo, chunk, radix))
+    for r in range(n):
+        assert bufs[r].cpu().numpy().tobytes() == bytes(expect[r]), (algo, n, root, m, chunk, r)
+
+
+@needs2
+def test_one_process_all_gpus_every_algorithm_and_root():
+    devices = list(range(min(ngpu(), 8)))
+    comms = B.Comm.local(devices, timeout_s=10)
+    rng = random.Random(17)
+    for algo in ("chain_pipelined", "knomial", "scatter_ring_allgather", "direct", "chain"):
+        for root in range(len(devices)):
+            for m in (0, 4, 4097, 1 << 20, rng.randrange(1, 5 << 20)):
+                run_group(comms, devices, algo, root, m, chunk=max(1, m // 5 + 3), seed=m + root)
+    run_group(comms, devices, "chain_pipelined", 0, 64 << 20, chunk=512 << 10, seed=5)
+
+
+@needs2
+def test_two_ranks_per_gpu():
+    devices = [d for d in range(min(ngpu(), 4)) for _ in range(2)]
+    comms = B.Comm.local(devices, timeout_s=10)
+    for algo in ("chain_pipelined", "scatter_ring_allgather", "knomial"):
+        for root in (0, len(devices) - 1, len(devices) // 2):
+            run_group(comms, devices, algo, root, (3 << 20) + 5, chunk=262147, seed=root)
+
+
+@needs2
+def test_missing_rank_times_out_with_named_error():
+    comms = B.Comm.local([0, 1], timeout_s=1.0)
+    buf = torch.zeros(4096, dtype=torch.uint8, device="cuda:0")
+    comms[0].bcast(buf, 4096, "uint8", 1, cfg_of("chain_pipelined", 1024))  # rank 1 never calls
+    with pytest.raises(B.DeviceTimeout) as e:
+        comms[0].check()
+    assert "rank 0" in str(e.value) and "peer 1" in str(e.value)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _ipc_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(rank)
+        from paper_1707_09414_b200.comm import DevicePtr
+        comm = B.Comm.connect_torch(world, rank, rank, heap_bytes=96 << 20, timeout_s=10)
+        cap = 70 << 20
+        buf = torch.as_tensor(DevicePtr(comm.alloc(cap), cap), device=f"cuda:{rank}")
+        ok = True
+        for it, (algo, m, root) in enumerate([("chain_pipelined", 64 << 20, 0), ("knomial", 12345, world - 1),
+                                              ("scatter_ring_allgather", 3 << 20, 1 % world),
+                                              ("chain_pipelined", 1, 0), ("direct", 777, 0)]):
+            payload = O.payload(it, m)
+            if rank == root:
+                buf[:m].copy_(torch.frombuffer(bytearray(payload), dtype=torch.uint8))
+            else:
+                buf[:m].zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            comm.bcast(buf, m, "uint8", root, cfg_of(algo, 524288, 2))
+            comm.check()
+            ok &= buf[:m].cpu().numpy().tobytes() == payload
+        q.put((rank, ok, None))
+        comm.close()
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, False, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@needs2
+def test_one_process_per_gpu_over_ipc():
+    import torch.multiprocessing as mp
+    world = min(ngpu(), 4)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, err in res:
+        assert ok, (rank, err)
