@@ -68,8 +68,10 @@ std::string format_failures(const std::vector<RankFailure>& f) {
 GroupOptions GroupOptions::from_env() {
   GroupOptions o;
   if (const char* v = std::getenv("BCL_POLL_NS")) o.poll_ns = static_cast<std::uint32_t>(std::strtoul(v, nullptr, 10));
-  if (const char* v = std::getenv("BCL_SLICE_BYTES")) o.slice_target = std::max<std::uint64_t>(16, std::strtoull(v, nullptr, 10));
+  if (const char* v = std::getenv("BCL_WINDOW_BYTES")) o.window_bytes = std::max<std::uint64_t>(16, std::strtoull(v, nullptr, 10));
+  if (const char* v = std::getenv("BCL_MIN_SLICE")) o.min_slice = std::max<std::uint64_t>(16, std::strtoull(v, nullptr, 10));
   if (const char* v = std::getenv("BCL_MAX_CTAS")) o.max_ctas_per_rank = std::atoi(v);
+  if (const char* v = std::getenv("BCL_STRICT_SYS")) o.strict_sys = std::atoi(v) != 0;
   return o;
 }
 
@@ -121,14 +123,18 @@ void Group::upload_peers(LocalRank& r) {
 
 namespace {
 
-int lanes_for(int device, int ranks_per_device, int cap) {
+int lanes_for(int device, int ranks_per_device, int cap, const GroupOptions& opt) {
   DeviceScope ds(device);
   int sms = 0;
   ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
+  (void)opt;
   int occ = 0;
   ck(static_cast<cudaError_t>(bcast_kernel_occupancy(&occ)), "occupancy");
-  int ctas = std::min(sms, std::max(1, sms * std::max(occ, 1) / std::max(ranks_per_device, 1)));
-  if (cap > 0) ctas = std::min(ctas, cap);
+  // Default: one CTA per SM per rank (fills every SM when a rank owns the
+  // GPU); ranks sharing a GPU split the co-resident CTA budget.
+  const int resident = sms * std::max(occ, 1);
+  int ctas = std::min(sms, std::max(1, resident / std::max(ranks_per_device, 1)));
+  if (cap > 0) ctas = std::min(cap, std::max(1, resident / std::max(ranks_per_device, 1)));
   return ctas * dev::kWarpsPerCta;
 }
 
@@ -167,7 +173,8 @@ std::shared_ptr<Group> Group::create_local(const std::vector<int>& devices, cons
       }
     }
   }
-  g->lanes_ = lanes_for(devices[0], rpd, opt.max_ctas_per_rank);
+  g->lanes_ = lanes_for(devices[0], rpd, opt.max_ctas_per_rank, opt);
+  for (const auto& kv : g->by_device_) if (kv.first != devices[0]) lanes_for(kv.first, rpd, opt.max_ctas_per_rank, opt);
   g->lanes_alloc_ = g->lanes_;
   g->single_device_ = g->by_device_.size() == 1;
   g->local_.resize(static_cast<std::size_t>(n));
@@ -201,7 +208,7 @@ std::shared_ptr<Group> Group::create_rank(int n, int rank, int device, std::size
   g->n_ = n;
   g->opt_ = opt;
   g->ipc_ = true;
-  g->lanes_ = lanes_for(device, 1, opt.max_ctas_per_rank);
+  g->lanes_ = lanes_for(device, 1, opt.max_ctas_per_rank, opt);
   g->lanes_alloc_ = g->lanes_;
   g->local_.resize(1);
   g->local_[0].rank = rank;
@@ -359,11 +366,22 @@ CallPlan Group::plan(const AlgorithmConfig& cfg, int root, std::uint64_t bytes) 
     }
     p->chunk_bytes = max_len;
   }
-  // Slices per chunk: the smallest divisor of L giving <= slice_target bytes.
-  const std::uint64_t want = std::max<std::uint64_t>(1, (max_len + opt_.slice_target - 1) / opt_.slice_target);
-  int q = lanes_;
-  for (int d = 1; d <= lanes_; ++d) {
-    if (lanes_ % d == 0 && static_cast<std::uint64_t>(d) >= want) { q = d; break; }
+  // Lane plan. ns = L / Q chunks are in flight per rank at once (one per
+  // pipe), so ns * C bytes is the window a hop must fill before its
+  // downstream can start: keep it near `window` (enough to cover NVLink
+  // bandwidth x latency) but never cut slices below `min_slice`.
+  const std::uint64_t win_chunks = std::max<std::uint64_t>(1, opt_.window_bytes / std::max<std::uint64_t>(max_len, 1));
+  const std::uint64_t q_floor = (static_cast<std::uint64_t>(lanes_) + win_chunks - 1) / win_chunks;
+  const std::uint64_t q_cap = std::max<std::uint64_t>(1, max_len / std::max<std::uint64_t>(opt_.min_slice, 16));
+  int q = 0;
+  for (int d = 1; d <= lanes_; ++d) {  // smallest divisor of L reaching q_floor
+    if (lanes_ % d == 0 && static_cast<std::uint64_t>(d) >= q_floor) { q = d; break; }
+  }
+  if (static_cast<std::uint64_t>(q) > q_cap) {  // too thin: largest divisor within q_cap
+    q = 1;
+    for (int d = 1; d <= lanes_; ++d) {
+      if (lanes_ % d == 0 && static_cast<std::uint64_t>(d) <= q_cap) q = d;
+    }
   }
   p->slices = q;
   const std::uint64_t per = (max_len + static_cast<std::uint64_t>(q) - 1) / static_cast<std::uint64_t>(q);
@@ -435,6 +453,7 @@ void Group::launch_group(const std::vector<int>& locals, const std::vector<void*
   P.timeout_ns = opt_.timeout_ns;
   P.poll_ns = opt_.poll_ns;
   P.sys_scope = single_device_ ? 0 : 1;
+  P.strict_sys = (opt_.strict_sys && !single_device_) ? 1 : 0;
   std::uint64_t epoch = 0;
   for (std::size_t i = 0; i < locals.size(); ++i) {
     LocalRank& r = local_[static_cast<std::size_t>(locals[i])];

@@ -71,9 +71,11 @@ class AggregateRankError : public std::runtime_error {
 
 struct GroupOptions {
   std::uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;  // device spin bound
-  std::uint64_t slice_target = 16384;                       // bytes per lane per chunk
+  std::uint64_t window_bytes = 4ull << 20;                  // bytes in flight per rank (chunks x slices)
+  std::uint64_t min_slice = 2048;                           // smallest per-lane slice of a chunk
   int max_ctas_per_rank = 0;                                // 0 = SM count
   std::uint32_t poll_ns = 64;                               // back-off between flag polls (ns)
+  bool strict_sys = false;                                  // system-scope fence before every flag
   static GroupOptions from_env();                           // BCL_* overrides (tuning runs)
 };
 

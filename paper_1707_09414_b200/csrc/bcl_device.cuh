@@ -17,6 +17,7 @@
 // downstream lane still reads it.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 
 namespace bcl {
@@ -26,7 +27,7 @@ constexpr int kMaxLocal = 16;    // ranks served by one launch (ranks sharing a 
 constexpr int kMaxEvents = 64;   // explicit per-rank event list (trees, SRA)
 constexpr int kMaxRanks = 64;    // communicator size limit
 constexpr int kWarpsPerCta = 8;  // lanes per CTA
-constexpr int kThreads = kWarpsPerCta * 32;
+constexpr int kThreads = (kWarpsPerCta + 1) * 32;  // + one publisher warp
 
 // Explicit event word: chunk (bits 0-23) | peer (24-30) | recv (31) |
 // pair index within the lane class (32-55).
@@ -100,7 +101,8 @@ struct LaunchParamsT {
   std::uint64_t epoch;        // >= 1, per call
   std::uint64_t timeout_ns;
   std::uint32_t poll_ns;      // __nanosleep between polls (0 = spin)
-  std::uint32_t sys_scope;    // 1: peers on other GPUs (fence.sys); 0: one GPU (fence.gpu)
+  std::uint32_t sys_scope;    // 1: peers on other GPUs; 0: every rank on this GPU
+  std::uint32_t strict_sys;   // 1: system-scope fence before every flag (see run_publisher)
   RankWork ranks[NL];
 };
 using LaunchParams = LaunchParamsT<kMaxLocal>;

@@ -1,12 +1,20 @@
 // bcl_kernels.cu — sm_100a broadcast executor (see bcl_device.cuh).
 //
-// One launch per GPU serves every rank that GPU hosts (normally one). Each
-// warp is a lane: it owns slice q = lane % Q of the chunks c with
-// c % (L/Q) == lane / Q and walks the rank's schedule, pulling those slices
-// from its upstream peer's buffer with 16-byte vector loads as soon as the
-// peer's per-lane counter says they are ready, then publishing its own counter
-// to its downstream peers (release at system scope). Data never leaves HBM /
-// NVLink: no staging buffers, no cudaMemcpy, no NCCL.
+// One launch per GPU serves every rank that GPU hosts (normally one). A CTA
+// holds kWarpsPerCta *copy warps* (the lanes) and one *publisher warp*:
+//
+//  * a copy warp owns slice q = lane % Q of the chunks c with
+//    c % (L/Q) == lane / Q and walks its rank's schedule: it waits for the
+//    upstream peer's per-lane counter, pulls the slice straight out of the
+//    peer's buffer with 16-byte vector loads (every load of a batch in
+//    flight), stores it locally, and hands "store value v to flag f" to the
+//    publisher through a shared-memory ring (CTA-scope release);
+//  * the publisher drains the rings of its CTA and issues ONE system-scope
+//    fence per batch before the remote flag stores. Under NVLink load a
+//    fence.acq_rel.sys costs ~10 us (measured), so it must not sit in the copy
+//    warps' per-chunk path.
+//
+// Data never leaves HBM / NVLink: no staging buffers, no cudaMemcpy, no NCCL.
 #include <cuda_runtime.h>
 
 #include <cstddef>
@@ -18,6 +26,8 @@
 namespace bcl {
 namespace dev {
 namespace {
+
+constexpr int kRing = 16;  // pending publishes per copy warp
 
 __device__ __forceinline__ std::uint64_t ld_relaxed_sys(const std::uint64_t* p) {
   std::uint64_t v;
@@ -32,11 +42,21 @@ __device__ __forceinline__ std::uint64_t ld_acquire_sys(const std::uint64_t* p) 
 __device__ __forceinline__ void st_relaxed_sys(std::uint64_t* p, std::uint64_t v) {
   asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ void fence_acq_rel_sys() {
-  asm volatile("fence.acq_rel.sys;" ::: "memory");
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ std::uint32_t ld_acquire_cta(const std::uint32_t* p) {
+  std::uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];"
+               : "=r"(v)
+               : "r"(static_cast<std::uint32_t>(__cvta_generic_to_shared(p)))
+               : "memory");
+  return v;
 }
-__device__ __forceinline__ void fence_acq_rel_gpu() {
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+__device__ __forceinline__ void st_release_cta(std::uint32_t* p, std::uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(
+                   static_cast<std::uint32_t>(__cvta_generic_to_shared(p))),
+               "r"(v)
+               : "memory");
 }
 __device__ __forceinline__ std::uint64_t globaltimer() {
   std::uint64_t t;
@@ -56,24 +76,37 @@ __device__ __forceinline__ uint4 ld_v4(const uint4* p) {
   return v;
 }
 __device__ __forceinline__ void st_v4(uint4* p, const uint4& v) {
-  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
-               "r"(v.w)
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
 }
 
-// Header fields shared by every LaunchParamsT<NL> (the ranks[] tail differs).
+// Shared-memory hand-off from the copy warps to the publisher warp.
+struct Publication {
+  std::uint64_t* addr;
+  std::uint64_t value;
+};
+struct CtaShared {
+  Publication ring[kWarpsPerCta][kRing];
+  std::uint32_t tail[kWarpsPerCta];  // written by copy warp w (release)
+  std::uint32_t head[kWarpsPerCta];  // written by the publisher (release)
+  std::uint32_t done;                // copy warps finished enqueueing
+};
+
 struct Ctx {
   const LaunchParamsT<1>* P;
   const RankWork* W;
-  int lane_id;   // 0..31
-  int ell;       // lane (warp) index within the rank
+  CtaShared* sh;
+  int lane_id;         // 0..31
+  int warp;            // copy warp index within the CTA
+  int ell;             // lane (copy warp) index within the rank
+  std::uint32_t tail;  // private copy of sh->tail[warp] (lane 0)
 };
 
-// Record the first failure of this rank; every lane then drains out.
+// Record the first failure of this rank; every waiting lane then drains out.
 __device__ void fail(const Ctx& c, int code, int peer, std::uint64_t chunk, std::uint64_t seen,
                      std::uint64_t want) {
-  ErrorRecord* e = c.W->err;
   atomicExch(c.W->abort, 1);
+  ErrorRecord* e = c.W->err;
   if (atomicCAS(&e->code, 0, code) == 0) {
     e->rank = c.W->rank;
     e->peer = peer;
@@ -85,9 +118,9 @@ __device__ void fail(const Ctx& c, int code, int peer, std::uint64_t chunk, std:
   }
 }
 
-// Warp-wide wait until *p >= target. Lane 0 polls (relaxed), then every
-// thread performs its own acquire so its later loads observe the producer's
-// data. Returns false on timeout/abort.
+// Warp-wide wait until *p >= target. Lane 0 polls (relaxed, with back-off);
+// then every thread performs its own system-scope acquire so its later loads
+// observe the producer's data. Returns false on timeout / abort.
 __device__ bool wait_geq(const Ctx& c, const std::uint64_t* p, std::uint64_t target, int peer,
                          std::uint64_t chunk) {
   int ok = 1;
@@ -99,7 +132,10 @@ __device__ bool wait_geq(const Ctx& c, const std::uint64_t* p, std::uint64_t tar
       while ((v = ld_relaxed_sys(p)) < target) {
         if (c.P->poll_ns) __nanosleep(c.P->poll_ns);
         if ((++spins & 255u) == 0) {
-          if (*(volatile int*)c.W->abort != 0) { ok = 0; break; }
+          if (*(volatile int*)c.W->abort != 0) {
+            ok = 0;
+            break;
+          }
           if (globaltimer() - t0 > c.P->timeout_ns) {
             fail(c, 1, peer, chunk, v, target);
             ok = 0;
@@ -115,51 +151,102 @@ __device__ bool wait_geq(const Ctx& c, const std::uint64_t* p, std::uint64_t tar
   return ok != 0;
 }
 
-// Publish a counter / ack after this warp's preceding stores: warp barrier,
-// then lane 0 issues a system-scope release store.
-__device__ __forceinline__ void publish(const Ctx& c, std::uint64_t* p, std::uint64_t v) {
+// Queue "*addr = value" behind this warp's preceding stores. The warp
+// barrier orders every lane's stores before lane 0's CTA-scope release; the
+// publisher's acquire + system fence then makes them visible before the flag.
+__device__ void publish(Ctx& c, std::uint64_t* addr, std::uint64_t value) {
   __syncwarp();
   if (c.lane_id == 0) {
-    if (c.P->sys_scope) fence_acq_rel_sys(); else fence_acq_rel_gpu();
-    st_relaxed_sys(p, v);
+    while (c.tail - ld_acquire_cta(&c.sh->head[c.warp]) >= static_cast<std::uint32_t>(kRing)) {
+      __nanosleep(32);
+    }
+    c.sh->ring[c.warp][c.tail % kRing] = Publication{addr, value};
+    c.tail += 1;
+    st_release_cta(&c.sh->tail[c.warp], c.tail);
   }
   __syncwarp();
 }
 
+// The publisher warp (lane 0): drain every ring, one fence per batch.
+__device__ void run_publisher(const LaunchParamsT<1>& P, CtaShared* sh) {
+  if ((threadIdx.x & 31) != 0) return;
+  std::uint32_t head[kWarpsPerCta] = {};
+  for (;;) {
+    const std::uint32_t done = ld_acquire_cta(&sh->done);
+    std::uint32_t tail[kWarpsPerCta];
+    bool any = false;
+#pragma unroll
+    for (int w = 0; w < kWarpsPerCta; ++w) {
+      tail[w] = ld_acquire_cta(&sh->tail[w]);
+      any |= tail[w] != head[w];
+    }
+    if (!any) {
+      if (done == static_cast<std::uint32_t>(kWarpsPerCta)) return;
+      __nanosleep(20);
+      continue;
+    }
+    // Every flag published here names data in this GPU's own memory, which
+    // peers read through this GPU's L2 (its point of coherence): once the
+    // stores are performed at gpu scope they are visible to NVLink readers.
+    // strict_sys keeps the textbook system-scope release instead.
+    if (P.strict_sys) {
+      fence_acq_rel_sys();
+    } else {
+      fence_acq_rel_gpu();
+    }
+#pragma unroll
+    for (int w = 0; w < kWarpsPerCta; ++w) {
+      for (std::uint32_t i = head[w]; i != tail[w]; ++i) {
+        const Publication e = sh->ring[w][i % kRing];
+        st_relaxed_sys(e.addr, e.value);
+      }
+      if (head[w] != tail[w]) {
+        head[w] = tail[w];
+        st_release_cta(&sh->head[w], head[w]);
+      }
+    }
+  }
+}
+
 // Warp copy of bytes [lo, hi) from src to dst (same offsets in both buffers).
-__device__ void warp_copy(const Ctx& c, const std::uint8_t* src, std::uint8_t* dst,
-                          std::uint64_t lo, std::uint64_t hi) {
+// Every 16-byte load of a batch is issued before the batch's stores, so a
+// batch costs one load round trip however short the slice is.
+__device__ void warp_copy(const Ctx& c, const std::uint8_t* src, std::uint8_t* dst, std::uint64_t lo,
+                          std::uint64_t hi) {
   if (hi <= lo) return;
   const int t = c.lane_id;
   const std::uintptr_t s0 = reinterpret_cast<std::uintptr_t>(src + lo);
   const std::uintptr_t d0 = reinterpret_cast<std::uintptr_t>(dst + lo);
-  if (((s0 ^ d0) & 15u) != 0) {
+  if (((s0 ^ d0) & 15u) != 0) {  // relative misalignment: byte path
     for (std::uint64_t i = lo + t; i < hi; i += 32) dst[i] = ld_u8(src + i);
     return;
   }
-  // head up to the first 16-byte boundary, vector body, byte tail
-  const std::uint64_t head = ((16u - (d0 & 15u)) & 15u);
+  const std::uint64_t head = (16u - (d0 & 15u)) & 15u;
   const std::uint64_t body_lo = lo + (head < hi - lo ? head : hi - lo);
   if (t < static_cast<int>(body_lo - lo)) dst[lo + t] = ld_u8(src + lo + t);
   const std::uint64_t nvec = (hi - body_lo) / 16;
   const uint4* vs = reinterpret_cast<const uint4*>(src + body_lo);
   uint4* vd = reinterpret_cast<uint4*>(dst + body_lo);
   constexpr int U = 8;
-  std::uint64_t i = t;
-  for (; i + (U - 1) * 32 < nvec; i += U * 32) {
+  for (std::uint64_t base = 0; base < nvec; base += U * 32) {
     uint4 r[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) r[u] = ld_v4(vs + i + u * 32);
+    for (int u = 0; u < U; ++u) {
+      const std::uint64_t i = base + t + u * 32;
+      if (i < nvec) r[u] = ld_v4(vs + i);
+    }
 #pragma unroll
-    for (int u = 0; u < U; ++u) st_v4(vd + i + u * 32, r[u]);
+    for (int u = 0; u < U; ++u) {
+      const std::uint64_t i = base + t + u * 32;
+      if (i < nvec) st_v4(vd + i, r[u]);
+    }
   }
-  for (; i < nvec; i += 32) st_v4(vd + i, ld_v4(vs + i));
   const std::uint64_t tail_lo = body_lo + nvec * 16;
   if (tail_lo + t < hi) dst[tail_lo + t] = ld_u8(src + tail_lo + t);
 }
 
-__device__ __forceinline__ void chunk_range(const LaunchParamsT<1>& P, std::uint32_t ch,
-                                            std::uint64_t* off, std::uint64_t* len) {
+__device__ __forceinline__ void chunk_range(const LaunchParamsT<1>& P, std::uint32_t ch, std::uint64_t* off,
+                                            std::uint64_t* len) {
   if (P.chunk_mode == kFixedChunks) {
     *off = static_cast<std::uint64_t>(ch) * P.chunk_bytes;
     *len = P.bytes - *off < P.chunk_bytes ? P.bytes - *off : P.chunk_bytes;
@@ -174,8 +261,8 @@ __device__ __forceinline__ void chunk_range(const LaunchParamsT<1>& P, std::uint
   }
 }
 
-__device__ __forceinline__ void pull_slice(const Ctx& c, std::uint32_t ch, int q,
-                                           const std::uint8_t* src, int src_rank) {
+__device__ __forceinline__ void pull_slice(const Ctx& c, std::uint32_t ch, int q, const std::uint8_t* src,
+                                           int src_rank) {
   std::uint64_t off, len;
   chunk_range(*c.P, ch, &off, &len);
   const std::uint64_t lo = static_cast<std::uint64_t>(q) * c.P->slice_bytes;
@@ -188,9 +275,20 @@ __device__ __forceinline__ void pull_slice(const Ctx& c, std::uint32_t ch, int q
   }
 }
 
+__device__ __forceinline__ void trace_pull(const Ctx& c, std::uint32_t k, std::uint64_t t_wait,
+                                           std::uint64_t t_ready) {
+  const RankWork& W = *c.W;
+  if (W.trace && c.lane_id == 0 && k + 1 < W.trace_cap) {
+    unsigned long long* rec = W.trace + (static_cast<std::size_t>(c.ell) * W.trace_cap + k) * 4;
+    rec[0] = t_wait;
+    rec[1] = t_ready;
+    rec[2] = globaltimer();
+  }
+}
+
 // Implicit pipelined chain (schedule_chain_pipelined, schedules.cpp:161-187):
 // logical rank l pulls from l-1 and serves l+1.
-__device__ void run_chain(const Ctx& c, int pipe, int q, int ns) {
+__device__ void run_chain(Ctx& c, int pipe, int q, int ns) {
   const LaunchParamsT<1>& P = *c.P;
   const RankWork& W = *c.W;
   const int n = P.n_ranks;
@@ -207,19 +305,16 @@ __device__ void run_chain(const Ctx& c, int pipe, int q, int ns) {
   const std::uint64_t tag = P.epoch << 32;
   const std::size_t slot = static_cast<std::size_t>(me) * L + c.ell;
 
-  if (has_next && c.lane_id == 0) st_relaxed_sys(W.peers->mbox[next] + slot, W.pub);
+  if (has_next && c.lane_id == 0) {
+    st_relaxed_sys(W.peers->mbox[next] + slot, W.pub);
+    if (P.sys_scope) fence_acq_rel_sys();  // remote mailbox lands before any remote flag
+  }
   if (!has_prev) {
     publish(c, W.peers->flags[next] + slot, tag | mine);  // the head owns every chunk
   } else {
     const std::uint64_t* ready = W.flags + static_cast<std::size_t>(prev) * L + c.ell;
     const std::uint8_t* src = nullptr;
-    std::uint32_t published = 0;
     for (std::uint32_t k = 0; k < mine; ++k) {
-      // Forward what we hold before blocking on the next chunk.
-      if (has_next && published < k) {
-        publish(c, W.peers->flags[next] + slot, tag | k);
-        published = k;
-      }
       const std::uint64_t t_wait = W.trace ? globaltimer() : 0;
       if (!wait_geq(c, ready, tag | (k + 1), prev, pipe + static_cast<std::uint64_t>(k) * ns)) return;
       const std::uint64_t t_ready = W.trace ? globaltimer() : 0;
@@ -228,19 +323,10 @@ __device__ void run_chain(const Ctx& c, int pipe, int q, int ns) {
             W.peers->addr_base[prev] + ld_relaxed_sys(W.mbox + static_cast<std::size_t>(prev) * L + c.ell));
       }
       pull_slice(c, pipe + k * ns, q, src, prev);
-      if (W.trace && c.lane_id == 0 && k + 1 < W.trace_cap) {
-        unsigned long long* rec = W.trace + (static_cast<std::size_t>(c.ell) * W.trace_cap + k) * 4;
-        rec[0] = t_wait;
-        rec[1] = t_ready;
-        rec[2] = globaltimer();
-        rec[3] = 0;
-      }
+      if (has_next) publish(c, W.peers->flags[next] + slot, tag | (k + 1));  // forward chunk k
+      trace_pull(c, k, t_wait, t_ready);
     }
-    if (has_next) publish(c, W.peers->flags[next] + slot, tag | mine);
     publish(c, W.peers->acks[prev] + slot, P.epoch);  // done reading prev's buffer
-  }
-  if (W.trace && c.lane_id == 0 && W.trace_cap > 0) {
-    W.trace[(static_cast<std::size_t>(c.ell) * W.trace_cap + W.trace_cap - 1) * 4 + 1] = globaltimer();
   }
   if (has_next) {
     (void)wait_geq(c, W.acks + static_cast<std::size_t>(next) * L + c.ell, P.epoch, next, K);
@@ -249,7 +335,7 @@ __device__ void run_chain(const Ctx& c, int pipe, int q, int ns) {
 
 // Explicit schedule (direct, chain, knomial, scatter_ring_allgather): walk
 // the rank's event list, keeping the events of this lane's chunk class.
-__device__ void run_events(const Ctx& c, int pipe, int q, int ns) {
+__device__ void run_events(Ctx& c, int pipe, int q, int ns) {
   const LaunchParamsT<1>& P = *c.P;
   const RankWork& W = *c.W;
   const int L = P.lanes;
@@ -268,7 +354,9 @@ __device__ void run_events(const Ctx& c, int pipe, int q, int ns) {
       if (c.lane_id == 0) st_relaxed_sys(W.peers->mbox[peer] + slot, W.pub);
     }
   }
+  if (sent_mask && c.lane_id == 0 && P.sys_scope) fence_acq_rel_sys();  // mailboxes before flags
   const std::uint8_t* src_of[kMaxRanks];
+  std::uint32_t k = 0;
   for (int i = 0; i < W.n_events; ++i) {
     const std::uint64_t ev = W.events[i];
     const std::uint32_t ch = static_cast<std::uint32_t>(ev & 0xFFFFFFu);
@@ -278,13 +366,16 @@ __device__ void run_events(const Ctx& c, int pipe, int q, int ns) {
     const std::uint64_t idx = ((ev >> 32) & 0xFFFFFFu) + 1;
     if (is_recv) {
       const std::uint64_t* ready = W.flags + static_cast<std::size_t>(peer) * L + c.ell;
+      const std::uint64_t t_wait = W.trace ? globaltimer() : 0;
       if (!wait_geq(c, ready, tag | idx, peer, ch)) return;
+      const std::uint64_t t_ready = W.trace ? globaltimer() : 0;
       if (!((recv_mask >> peer) & 1u)) {
         recv_mask |= 1ull << peer;
         src_of[peer] = reinterpret_cast<const std::uint8_t*>(
             W.peers->addr_base[peer] + ld_relaxed_sys(W.mbox + static_cast<std::size_t>(peer) * L + c.ell));
       }
       pull_slice(c, ch, q, src_of[peer], peer);
+      trace_pull(c, k++, t_wait, t_ready);
     } else {
       publish(c, W.peers->flags[peer] + slot, tag | idx);
     }
@@ -300,27 +391,50 @@ __device__ void run_events(const Ctx& c, int pipe, int q, int ns) {
 
 template <int NL>
 __global__ void __launch_bounds__(kThreads) bcast_kernel(const __grid_constant__ LaunchParamsT<NL> P) {
+  __shared__ CtaShared sh;
   const int local = NL == 1 ? 0 : static_cast<int>(blockIdx.x) / P.ctas_per_rank;
   const int cta = NL == 1 ? static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x) % P.ctas_per_rank;
-  Ctx c;
-  c.P = reinterpret_cast<const LaunchParamsT<1>*>(&P);
-  c.W = &P.ranks[local];
-  c.lane_id = threadIdx.x & 31;
-  c.ell = cta * kWarpsPerCta + (threadIdx.x >> 5);
-  if (c.ell >= P.lanes) return;
-  const int ns = P.lanes / P.slices;
-  const int pipe = c.ell / P.slices;
-  const int q = c.ell % P.slices;
-  const std::uint64_t t_enter = c.W->trace ? globaltimer() : 0;
-  if (c.W->n_events < 0) {
-    run_chain(c, pipe, q, ns);
-  } else {
-    run_events(c, pipe, q, ns);
+  const int warp = static_cast<int>(threadIdx.x >> 5);
+  if (threadIdx.x < kWarpsPerCta) {
+    sh.tail[threadIdx.x] = 0;
+    sh.head[threadIdx.x] = 0;
   }
-  if (c.W->trace && c.lane_id == 0 && c.W->trace_cap > 0) {
-    unsigned long long* rec = c.W->trace + (static_cast<std::size_t>(c.ell) * c.W->trace_cap + c.W->trace_cap - 1) * 4;
-    rec[0] = t_enter;
-    rec[3] = globaltimer();
+  if (threadIdx.x == 0) sh.done = 0;
+  __syncthreads();
+  const auto* hdr = reinterpret_cast<const LaunchParamsT<1>*>(&P);
+  if (warp == kWarpsPerCta) {
+    run_publisher(*hdr, &sh);
+    return;
+  }
+  Ctx c;
+  c.P = hdr;
+  c.W = &P.ranks[local];
+  c.sh = &sh;
+  c.lane_id = static_cast<int>(threadIdx.x & 31);
+  c.warp = warp;
+  c.ell = cta * kWarpsPerCta + warp;
+  c.tail = 0;
+  if (c.ell < P.lanes) {
+    const std::uint64_t t_enter = c.W->trace ? globaltimer() : 0;
+    const int ns = P.lanes / P.slices;
+    const int pipe = c.ell / P.slices;
+    const int q = c.ell % P.slices;
+    if (c.W->n_events < 0) {
+      run_chain(c, pipe, q, ns);
+    } else {
+      run_events(c, pipe, q, ns);
+    }
+    if (c.W->trace && c.lane_id == 0 && c.W->trace_cap > 0) {
+      unsigned long long* rec =
+          c.W->trace + (static_cast<std::size_t>(c.ell) * c.W->trace_cap + c.W->trace_cap - 1) * 4;
+      rec[0] = t_enter;
+      rec[3] = globaltimer();
+    }
+  }
+  __syncwarp();
+  if (c.lane_id == 0) {
+    __threadfence_block();  // the last tail release is ordered before the count
+    atomicAdd_block(&sh.done, 1u);
   }
 }
 
