@@ -175,12 +175,24 @@ def main():
         bench_multi(args, torch, rank, world)
 
 
-def time_steps(torch, steps, warmup, prepare, body, verify, stream):
-    """Runs warmup+steps iterations; returns the per-step body times (s)."""
+GATE_CYCLES = 1_000_000  # ~0.5 ms spin: the host enqueues the timed ops behind it
+
+
+def time_steps(torch, steps, warmup, prepare, body, verify, stream, align=None):
+    """Runs warmup+steps iterations; returns the per-step body times (s).
+
+    Per step: prepare (buffer reset, L2 flush) -> a GPU-side gate
+    (torch.cuda._sleep) so that everything after it is already enqueued when
+    the GPU reaches it -> align (device barrier across ranks) -> ev0 -> body
+    -> ev1. Host launch overhead therefore never lands inside [ev0, ev1]."""
     times = []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for it in range(warmup + steps):
         prepare(it)
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(GATE_CYCLES)
+        if align is not None:
+            align()
         ev0.record(stream)
         body(it)
         ev1.record(stream)
@@ -204,6 +216,7 @@ def bench_single(args, torch):
     bufs = [torch.zeros(m, dtype=torch.uint8, device=dev) for _ in range(n)]
     bufs[0].copy_(torch.randint(0, 256, (m,), dtype=torch.uint8, device=dev, generator=g))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()  # setup ran on the default stream; the timed loop uses `stream`
 
     def prepare(it):
         with torch.cuda.stream(stream):
@@ -288,6 +301,7 @@ def bench_multi(args, torch, rank, world):
     g = torch.Generator(device=dev).manual_seed(1)
     ref_all.copy_(torch.randint(0, 256, (cap,), dtype=torch.uint8, device=dev, generator=g))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()  # setup ran on the default stream; the timed loop uses `stream`
 
     def run(size, steps, warmup, ours, cfg=None, flush_l2=True):
         buf = buf_all[:size]
@@ -301,10 +315,8 @@ def bench_multi(args, torch, rank, world):
                     buf.zero_()
                 if flush_l2:
                     flush.fill_(it & 0xFF)
-                if ours:
-                    comm.barrier(stream)
-            if not ours:
-                torch.cuda.current_stream().wait_stream(stream)
+            if it == 0:
+                stream.synchronize()
                 dist.barrier(device_ids=[local])
 
         def body(it):
@@ -317,7 +329,8 @@ def bench_multi(args, torch, rank, world):
         def verify(it):
             return torch.equal(buf, ref)
 
-        times = time_steps(torch, steps, warmup, prepare, body, verify, stream)
+        times = time_steps(torch, steps, warmup, prepare, body, verify, stream,
+                           align=lambda: comm.barrier(stream))
         t = torch.tensor(times, dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ok = torch.tensor([1.0], device=dev)

@@ -72,6 +72,8 @@ GroupOptions GroupOptions::from_env() {
   if (const char* v = std::getenv("BCL_MIN_SLICE")) o.min_slice = std::max<std::uint64_t>(16, std::strtoull(v, nullptr, 10));
   if (const char* v = std::getenv("BCL_MAX_CTAS")) o.max_ctas_per_rank = std::atoi(v);
   if (const char* v = std::getenv("BCL_STRICT_SYS")) o.strict_sys = std::atoi(v) != 0;
+  if (const char* v = std::getenv("BCL_STAGES")) o.stages = static_cast<std::uint32_t>(std::clamp(std::atoi(v), 2, dev::kMaxStages));
+  if (const char* v = std::getenv("BCL_STAGE_BYTES")) o.stage_bytes = static_cast<std::int64_t>(std::strtoul(v, nullptr, 10)) / 16 * 16;
   return o;
 }
 
@@ -127,9 +129,12 @@ int lanes_for(int device, int ranks_per_device, int cap, const GroupOptions& opt
   DeviceScope ds(device);
   int sms = 0;
   ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
-  (void)opt;
+  const std::size_t smem =
+      opt.stage_bytes > 0 ? bcast_smem_bytes(opt.stages, static_cast<std::uint32_t>(opt.stage_bytes)) : 0;
+  ck(static_cast<cudaError_t>(prepare_bcast_kernels(smem)), "cudaFuncSetAttribute(smem)");
   int occ = 0;
-  ck(static_cast<cudaError_t>(bcast_kernel_occupancy(&occ)), "occupancy");
+  ck(static_cast<cudaError_t>(bcast_kernel_occupancy(&occ, smem)), "occupancy");
+  if (occ < 1) throw std::invalid_argument("stage_bytes does not fit in shared memory");
   // Default: one CTA per SM per rank (fills every SM when a rank owns the
   // GPU); ranks sharing a GPU split the co-resident CTA budget.
   const int resident = sms * std::max(occ, 1);
@@ -173,8 +178,13 @@ std::shared_ptr<Group> Group::create_local(const std::vector<int>& devices, cons
       }
     }
   }
-  g->lanes_ = lanes_for(devices[0], rpd, opt.max_ctas_per_rank, opt);
-  for (const auto& kv : g->by_device_) if (kv.first != devices[0]) lanes_for(kv.first, rpd, opt.max_ctas_per_rank, opt);
+  // TMA bulk stages pay off on NVLink pulls; ranks sharing one GPU (HBM
+  // bound, several CTAs per SM needed for co-residency) use vector loads.
+  if (g->opt_.stage_bytes < 0) g->opt_.stage_bytes = g->by_device_.size() > 1 ? 8192 : 0;
+  g->lanes_ = lanes_for(devices[0], rpd, opt.max_ctas_per_rank, g->opt_);
+  for (const auto& kv : g->by_device_) {
+    if (kv.first != devices[0]) lanes_for(kv.first, rpd, opt.max_ctas_per_rank, g->opt_);
+  }
   g->lanes_alloc_ = g->lanes_;
   g->single_device_ = g->by_device_.size() == 1;
   g->local_.resize(static_cast<std::size_t>(n));
@@ -208,7 +218,8 @@ std::shared_ptr<Group> Group::create_rank(int n, int rank, int device, std::size
   g->n_ = n;
   g->opt_ = opt;
   g->ipc_ = true;
-  g->lanes_ = lanes_for(device, 1, opt.max_ctas_per_rank, opt);
+  if (g->opt_.stage_bytes < 0) g->opt_.stage_bytes = n > 1 ? 8192 : 0;
+  g->lanes_ = lanes_for(device, 1, opt.max_ctas_per_rank, g->opt_);
   g->lanes_alloc_ = g->lanes_;
   g->local_.resize(1);
   g->local_[0].rank = rank;
@@ -372,11 +383,17 @@ CallPlan Group::plan(const AlgorithmConfig& cfg, int root, std::uint64_t bytes) 
   // bandwidth x latency) but never cut slices below `min_slice`.
   const std::uint64_t win_chunks = std::max<std::uint64_t>(1, opt_.window_bytes / std::max<std::uint64_t>(max_len, 1));
   const std::uint64_t q_floor = (static_cast<std::uint64_t>(lanes_) + win_chunks - 1) / win_chunks;
-  const std::uint64_t q_cap = std::max<std::uint64_t>(1, max_len / std::max<std::uint64_t>(opt_.min_slice, 16));
+  std::uint64_t q_floor_stage = 1;  // bulk path: one slice per stage
+  if (opt_.stage_bytes > 0) {
+    const std::uint64_t sb = static_cast<std::uint64_t>(opt_.stage_bytes);
+    q_floor_stage = (max_len + sb - 1) / sb;
+  }
+  const std::uint64_t q_cap = std::max<std::uint64_t>(q_floor_stage, max_len / std::max<std::uint64_t>(opt_.min_slice, 16));
   int q = 0;
   for (int d = 1; d <= lanes_; ++d) {  // smallest divisor of L reaching q_floor
-    if (lanes_ % d == 0 && static_cast<std::uint64_t>(d) >= q_floor) { q = d; break; }
+    if (lanes_ % d == 0 && static_cast<std::uint64_t>(d) >= std::max(q_floor, q_floor_stage)) { q = d; break; }
   }
+  if (q == 0) q = lanes_;  // even one slice per lane cannot meet the floor
   if (static_cast<std::uint64_t>(q) > q_cap) {  // too thin: largest divisor within q_cap
     q = 1;
     for (int d = 1; d <= lanes_; ++d) {
@@ -454,6 +471,8 @@ void Group::launch_group(const std::vector<int>& locals, const std::vector<void*
   P.poll_ns = opt_.poll_ns;
   P.sys_scope = single_device_ ? 0 : 1;
   P.strict_sys = (opt_.strict_sys && !single_device_) ? 1 : 0;
+  P.stage_bytes = static_cast<std::uint32_t>(std::max<std::int64_t>(opt_.stage_bytes, 0));
+  P.stages = opt_.stages;
   std::uint64_t epoch = 0;
   for (std::size_t i = 0; i < locals.size(); ++i) {
     LocalRank& r = local_[static_cast<std::size_t>(locals[i])];

@@ -76,6 +76,9 @@ struct GroupOptions {
   int max_ctas_per_rank = 0;                                // 0 = SM count
   std::uint32_t poll_ns = 64;                               // back-off between flag polls (ns)
   bool strict_sys = false;                                  // system-scope fence before every flag
+  std::int64_t stage_bytes = -1;                            // bulk-copy stage per warp: 0 = vector loads,
+                                                            // -1 = auto (8 KiB across GPUs, 0 on one GPU)
+  std::uint32_t stages = 2;                                 // bulk-copy stages per copy warp
   static GroupOptions from_env();                           // BCL_* overrides (tuning runs)
 };
 

@@ -28,6 +28,7 @@ constexpr int kMaxEvents = 64;   // explicit per-rank event list (trees, SRA)
 constexpr int kMaxRanks = 64;    // communicator size limit
 constexpr int kWarpsPerCta = 8;  // lanes per CTA
 constexpr int kThreads = (kWarpsPerCta + 1) * 32;  // + one publisher warp
+constexpr int kMaxStages = 4;    // bulk-copy stages per copy warp
 
 // Explicit event word: chunk (bits 0-23) | peer (24-30) | recv (31) |
 // pair index within the lane class (32-55).
@@ -103,6 +104,8 @@ struct LaunchParamsT {
   std::uint32_t poll_ns;      // __nanosleep between polls (0 = spin)
   std::uint32_t sys_scope;    // 1: peers on other GPUs; 0: every rank on this GPU
   std::uint32_t strict_sys;   // 1: system-scope fence before every flag (see run_publisher)
+  std::uint32_t stage_bytes;  // bytes per bulk-copy stage; 0 = vector loads only
+  std::uint32_t stages;       // bulk-copy stages per copy warp (2..kMaxStages)
   RankWork ranks[NL];
 };
 using LaunchParams = LaunchParamsT<kMaxLocal>;
@@ -123,6 +126,8 @@ struct BarrierParams {
 // Launchers (bcl_kernels.cu). Return cudaError_t as int.
 int launch_bcast(const dev::LaunchParams& p, int cooperative, void* stream);
 int launch_barrier(const dev::BarrierParams& p, void* stream);
-int bcast_kernel_occupancy(int* blocks_per_sm);
+int bcast_kernel_occupancy(int* blocks_per_sm, std::size_t smem);
+std::size_t bcast_smem_bytes(std::uint32_t stages, std::uint32_t stage_bytes);
+int prepare_bcast_kernels(std::size_t smem);
 
 }  // namespace bcl

@@ -80,6 +80,49 @@ __device__ __forceinline__ void st_v4(uint4* p, const uint4& v) {
                : "memory");
 }
 
+__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
+  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, std::uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P;\nBCL_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      " @!P bra BCL_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// TMA-engine bulk copies (SASS UBLKCP): global -> shared completing on an
+// mbarrier, and shared -> global tracked by bulk async-groups.
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gsrc, std::uint32_t bytes, std::uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* smem, std::uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(smem)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
 // Shared-memory hand-off from the copy warps to the publisher warp.
 struct Publication {
   std::uint64_t* addr;
@@ -87,6 +130,7 @@ struct Publication {
 };
 struct CtaShared {
   Publication ring[kWarpsPerCta][kRing];
+  std::uint64_t full[kWarpsPerCta][kMaxStages];  // bulk-copy mbarriers (one per stage)
   std::uint32_t tail[kWarpsPerCta];  // written by copy warp w (release)
   std::uint32_t head[kWarpsPerCta];  // written by the publisher (release)
   std::uint32_t done;                // copy warps finished enqueueing
@@ -100,6 +144,7 @@ struct Ctx {
   int warp;            // copy warp index within the CTA
   int ell;             // lane (copy warp) index within the rank
   std::uint32_t tail;  // private copy of sh->tail[warp] (lane 0)
+  std::uint8_t* stage; // 2 x stage_bytes of dynamic shared memory (bulk path), or null
 };
 
 // Record the first failure of this rank; every waiting lane then drains out.
@@ -286,6 +331,153 @@ __device__ __forceinline__ void trace_pull(const Ctx& c, std::uint32_t k, std::u
   }
 }
 
+
+__device__ __forceinline__ void bulk_wait_n(int n) {
+  switch (n) {
+    case 0: bulk_wait<0>(); break;
+    case 1: bulk_wait<1>(); break;
+    case 2: bulk_wait<2>(); break;
+    default: bulk_wait<3>(); break;
+  }
+}
+__device__ __forceinline__ void bulk_wait_read_n(int n) {
+  switch (n) {
+    case 0: bulk_wait_read<0>(); break;
+    case 1: bulk_wait_read<1>(); break;
+    case 2: bulk_wait_read<2>(); break;
+    default: bulk_wait_read<3>(); break;
+  }
+}
+
+// Bulk-copy variant of the chain's middle/tail loop, driven by lane 0 alone.
+// Slices of the lane's chunks stream through a ring of S shared-memory
+// stages: a TMA load (global -> smem, mbarrier completion) is issued for
+// every chunk the upstream has already published while a stage is free, the
+// oldest landed slice is written back with a TMA store, and chunks are
+// published as soon as their stores have completed (async-group
+// accounting). When nothing is in flight the lane finishes and publishes
+// what it holds before blocking on the upstream, so downstream progress
+// never waits for this rank's upstream. Requires 16-byte aligned slices; the
+// ragged end of the message goes byte-wise.
+__device__ bool chain_pull_bulk(Ctx& c, int pipe, int q, int ns, std::uint32_t mine, const std::uint64_t* ready,
+                                const std::uint8_t* src, int prev, bool has_next, std::uint64_t* next_flag,
+                                std::uint64_t tag) {
+  const LaunchParamsT<1>& P = *c.P;
+  const RankWork& W = *c.W;
+  std::uint64_t* bars = c.sh->full[c.warp];
+  const std::uint32_t sb = P.stage_bytes;
+  const std::uint32_t S = P.stages;
+  std::uint32_t parity = 0;
+  int ok = 1;
+  // Slice geometry of the lane's k-th chunk: [gofs, gofs + len), body = 16 B multiple.
+  auto geom = [&](std::uint32_t k, std::uint64_t* gofs, std::uint32_t* body, std::uint32_t* len) {
+    std::uint64_t off, clen;
+    chunk_range(P, pipe + k * ns, &off, &clen);
+    const std::uint64_t lo = static_cast<std::uint64_t>(q) * P.slice_bytes;
+    const std::uint64_t hi = lo < clen ? (lo + P.slice_bytes < clen ? lo + P.slice_bytes : clen) : lo;
+    *gofs = off + lo;
+    *len = static_cast<std::uint32_t>(hi - lo);
+    *body = *len & ~15u;
+  };
+  auto stamp = [&](std::uint32_t k, int field) {
+    if (W.trace && k + 1 < W.trace_cap) {
+      W.trace[(static_cast<std::size_t>(c.ell) * W.trace_cap + k) * 4 + field] = globaltimer();
+    }
+  };
+  std::uint32_t issued = 0, landed = 0, posted = 0;
+  auto issue = [&]() {  // load the lane's chunk `issued` into stage issued % S
+    if (issued >= S) bulk_wait_read_n(static_cast<int>(landed + S - 1 - issued));  // stage's last store read it
+    std::uint64_t g;
+    std::uint32_t body, len;
+    geom(issued, &g, &body, &len);
+    const std::uint32_t st = issued % S;
+    fence_proxy_async();  // generic-proxy acquire of the flag before async-proxy reads
+    mbar_expect_tx(&bars[st], body);
+    if (body) bulk_g2s(c.stage + static_cast<std::size_t>(st) * sb, src + g, body, &bars[st]);
+    stamp(issued, 0);
+    ++issued;
+  };
+  auto post = [&](std::uint32_t count) {  // "chunks 0..count-1 forwarded"
+    if (count <= posted) return;
+    posted = count;
+    stamp(count - 1, 3);
+    if (!has_next) return;
+    fence_proxy_async();  // completed TMA writes ordered before the generic-proxy hand-off
+    while (c.tail - ld_acquire_cta(&c.sh->head[c.warp]) >= static_cast<std::uint32_t>(kRing)) __nanosleep(32);
+    c.sh->ring[c.warp][c.tail % kRing] = Publication{next_flag, tag | count};
+    c.tail += 1;
+    st_release_cta(&c.sh->tail[c.warp], c.tail);
+  };
+  auto block_for = [&](std::uint32_t j) -> bool {  // wait until the lane's chunk j is ready upstream
+    const std::uint64_t want = tag | (j + 1);
+    std::uint64_t v = ld_relaxed_sys(ready);
+    if (v < want) {
+      const std::uint64_t t0 = globaltimer();
+      unsigned spins = 0;
+      while ((v = ld_relaxed_sys(ready)) < want) {
+        if (P.poll_ns) __nanosleep(P.poll_ns);
+        if ((++spins & 255u) == 0) {
+          if (*(volatile int*)W.abort != 0) return false;
+          if (globaltimer() - t0 > P.timeout_ns) {
+            fail(c, 1, prev, pipe + static_cast<std::uint64_t>(j) * ns, v, want);
+            return false;
+          }
+        }
+      }
+    }
+    (void)ld_acquire_sys(ready);
+    return true;
+  };
+  if (c.lane_id == 0) {
+    issue();  // chunk 0 was acquired by the caller
+    while (landed < mine) {
+      // Prefetch every chunk the upstream has already published, up to S in flight.
+      while (issued < mine && issued - landed < S && ld_relaxed_sys(ready) >= (tag | (issued + 1))) {
+        (void)ld_acquire_sys(ready);
+        issue();
+      }
+      if (issued == landed) {  // nothing in flight: publish what we hold, then block
+        bulk_wait<0>();
+        post(landed);
+        if (!block_for(issued)) {
+          ok = 0;
+          break;
+        }
+        issue();
+        continue;
+      }
+      const std::uint32_t st = landed % S;
+      mbar_wait(&bars[st], (parity >> st) & 1u);
+      parity ^= 1u << st;
+      stamp(landed, 1);
+      std::uint64_t g;
+      std::uint32_t body, len;
+      geom(landed, &g, &body, &len);
+      if (body) bulk_s2g(W.buf + g, c.stage + static_cast<std::size_t>(st) * sb, body);
+      bulk_commit();
+      stamp(landed, 2);
+      for (std::uint32_t i = body; i < len; ++i) W.buf[g + i] = ld_u8(src + g + i);  // ragged end
+      if (W.prov != nullptr && len) {
+        atomicAdd(&W.prov[static_cast<std::uint64_t>(prev) * P.n_chunks + pipe + landed * ns],
+                  static_cast<unsigned long long>(len));
+      }
+      ++landed;
+      if (issued > landed) {
+        bulk_wait<1>();  // every store but the newest is complete
+        post(landed - 1);
+      } else {
+        bulk_wait<0>();
+        post(landed);
+      }
+    }
+    bulk_wait<0>();
+    if (ok) post(mine);
+  }
+  ok = __shfl_sync(0xffffffffu, ok, 0);
+  __syncwarp();
+  return ok != 0;
+}
+
 // Implicit pipelined chain (schedule_chain_pipelined, schedules.cpp:161-187):
 // logical rank l pulls from l-1 and serves l+1.
 __device__ void run_chain(Ctx& c, int pipe, int q, int ns) {
@@ -314,6 +506,22 @@ __device__ void run_chain(Ctx& c, int pipe, int q, int ns) {
   } else {
     const std::uint64_t* ready = W.flags + static_cast<std::size_t>(prev) * L + c.ell;
     const std::uint8_t* src = nullptr;
+    if (c.stage != nullptr) {
+      if (!wait_geq(c, ready, tag | 1, prev, pipe)) return;
+      src = reinterpret_cast<const std::uint8_t*>(
+          W.peers->addr_base[prev] + ld_relaxed_sys(W.mbox + static_cast<std::size_t>(prev) * L + c.ell));
+      const bool aligned = ((reinterpret_cast<std::uintptr_t>(src) | reinterpret_cast<std::uintptr_t>(W.buf)) & 15u) == 0 &&
+                           (P.chunk_bytes & 15u) == 0 && (P.slice_bytes & 15u) == 0 &&
+                           P.slice_bytes <= P.stage_bytes;
+      if (aligned) {
+        if (!chain_pull_bulk(c, pipe, q, ns, mine, ready, src, prev, has_next, W.peers->flags[next] + slot, tag)) {
+          return;
+        }
+        publish(c, W.peers->acks[prev] + slot, P.epoch);
+        if (has_next) (void)wait_geq(c, W.acks + static_cast<std::size_t>(next) * L + c.ell, P.epoch, next, K);
+        return;
+      }
+    }
     for (std::uint32_t k = 0; k < mine; ++k) {
       const std::uint64_t t_wait = W.trace ? globaltimer() : 0;
       if (!wait_geq(c, ready, tag | (k + 1), prev, pipe + static_cast<std::uint64_t>(k) * ns)) return;
@@ -400,6 +608,11 @@ __global__ void __launch_bounds__(kThreads) bcast_kernel(const __grid_constant__
     sh.head[threadIdx.x] = 0;
   }
   if (threadIdx.x == 0) sh.done = 0;
+  extern __shared__ __align__(128) std::uint8_t dyn_smem[];
+  if (P.stage_bytes && warp < kWarpsPerCta && (threadIdx.x & 31) == 0) {
+    for (std::uint32_t i = 0; i < P.stages; ++i) mbar_init(&sh.full[warp][i]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
   const auto* hdr = reinterpret_cast<const LaunchParamsT<1>*>(&P);
   if (warp == kWarpsPerCta) {
@@ -414,6 +627,7 @@ __global__ void __launch_bounds__(kThreads) bcast_kernel(const __grid_constant__
   c.warp = warp;
   c.ell = cta * kWarpsPerCta + warp;
   c.tail = 0;
+  c.stage = P.stage_bytes ? dyn_smem + static_cast<std::size_t>(warp) * P.stages * P.stage_bytes : nullptr;
   if (c.ell < P.lanes) {
     const std::uint64_t t_enter = c.W->trace ? globaltimer() : 0;
     const int ns = P.lanes / P.slices;
@@ -474,10 +688,23 @@ __global__ void barrier_kernel(const __grid_constant__ BarrierParams B) {
 }  // namespace
 }  // namespace dev
 
+std::size_t bcast_smem_bytes(std::uint32_t stages, std::uint32_t stage_bytes) {
+  return static_cast<std::size_t>(dev::kWarpsPerCta) * stages * stage_bytes;
+}
+
+int prepare_bcast_kernels(std::size_t smem) {
+  cudaError_t e = cudaFuncSetAttribute(dev::bcast_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return static_cast<int>(e);
+  return static_cast<int>(cudaFuncSetAttribute(dev::bcast_kernel<dev::kMaxLocal>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+}
+
 int launch_bcast(const dev::LaunchParams& p, int cooperative, void* stream) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(p.n_local * p.ctas_per_rank));
   cfg.blockDim = dim3(dev::kThreads);
+  cfg.dynamicSmemBytes = p.stage_bytes ? bcast_smem_bytes(p.stages, p.stage_bytes) : 0;
   cfg.stream = static_cast<cudaStream_t>(stream);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
@@ -507,9 +734,9 @@ int launch_barrier(const dev::BarrierParams& p, void* stream) {
   return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::barrier_kernel, p));
 }
 
-int bcast_kernel_occupancy(int* blocks_per_sm) {
+int bcast_kernel_occupancy(int* blocks_per_sm, std::size_t smem) {
   return static_cast<int>(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      blocks_per_sm, dev::bcast_kernel<dev::kMaxLocal>, dev::kThreads, 0));
+      blocks_per_sm, dev::bcast_kernel<dev::kMaxLocal>, dev::kThreads, smem));
 }
 
 }  // namespace bcl

@@ -1,0 +1,78 @@
+#!/usr/bin/env python3
+"""Dev tool (torchrun, one process per GPU): bench-shaped broadcast with the
+device timeline enabled; each rank prints its kernel time (CUDA events) and
+its in-kernel lane span, plus the first/last lane entry relative to ev0."""
+import os, statistics, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch, torch.distributed as dist
+import paper_1707_09414_b200 as B
+from paper_1707_09414_b200.comm import DevicePtr
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+local = int(os.environ.get("LOCAL_RANK", rank))
+torch.cuda.set_device(local)
+dev = torch.device("cuda", local)
+dist.init_process_group("nccl", device_id=dev)
+m = int(os.environ.get("TRACE_BYTES", 1 << 30)); chunk = int(os.environ.get("TRACE_CHUNK", 512 << 10))
+comm = B.Comm.connect_torch(world, rank, local, heap_bytes=m + (64 << 20), timeout_s=30)
+L = comm.info()["lanes"]
+buf = torch.as_tensor(DevicePtr(comm.alloc(m), m), device=dev)
+ref = torch.randint(0, 256, (m,), dtype=torch.uint8, device=dev, generator=torch.Generator(device=dev).manual_seed(1))
+torch.cuda.synchronize()  # ref is written on the default stream; s reads it
+cap = 1024
+tr = torch.zeros(L * cap * 4, dtype=torch.int64, device=dev)
+cfg = B.AlgorithmConfig(B.Algorithm.chain_pipelined, 0, chunk)
+s = torch.cuda.Stream(device=dev)
+ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+evb = torch.cuda.Event(enable_timing=True)
+tstamp = torch.zeros(2, dtype=torch.int64, device=dev)
+def chk(tag):
+    torch.cuda.synchronize()
+    if rank == 0 and not torch.equal(buf, ref):
+        bad = int((buf != ref).sum())
+        print(f"rank 0 CHECK {tag}: {bad} bad bytes", flush=True)
+for it in range(5):
+    with torch.cuda.stream(s):
+        (buf.copy_(ref) if rank == 0 else buf.zero_())
+    if it == 0: chk("after copy_")
+    with torch.cuda.stream(s):
+        tr.zero_()
+    if it == 0: chk("after tr.zero_")
+    comm.set_trace(tr if it == 4 else None, cap)
+    s.synchronize(); dist.barrier(device_ids=[local])
+    if rank == 0 and not torch.equal(buf, ref):
+        print(f"rank 0 iter {it}: root buffer differs BEFORE the broadcast", flush=True)
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(1_000_000)
+    evb.record(s)
+    comm.barrier(s)
+    ev0.record(s)
+    comm.bcast(buf, m, "uint8", 0, cfg, stream=s)
+    ev1.record(s)
+    ev1.synchronize()
+    comm.check(s)
+    if not torch.equal(buf, ref):
+        bad = (buf != ref).nonzero().flatten()
+        print(f"rank {rank} iter {it}: {len(bad)} bad bytes first {int(bad[0])} last {int(bad[-1])} "
+              f"chunk {int(bad[0]) // chunk} off {int(bad[0]) % chunk}", flush=True)
+        if rank == 0:
+            b0 = int(bad[0])
+            print("root buf", buf[b0:b0+16].tolist(), "ref", ref[b0:b0+16].tolist(), flush=True)
+            # runs of bad bytes
+            d = (bad[1:] - bad[:-1])
+            brk = (d != 1).nonzero().flatten()
+            print("bad runs:", int(len(brk)) + 1, "first run len", int(brk[0]) + 1 if len(brk) else len(bad), flush=True)
+        raise SystemExit(1)
+life = tr.view(L, cap, 4)[:, cap - 1].cpu()
+rec = tr.view(L, cap, 4)[:, :cap - 1].cpu()
+act = life[:, 0] > 0
+t_in = int(life[:, 0][act].min()); t_in_max = int(life[:, 0][act].max()); t_out = int(life[:, 3][act].max())
+land = rec[:, :, 1]; lm = land > 0
+msg = (f"rank {rank}: barrier {evb.elapsed_time(ev0)*1e3:.1f}us kernel(ev0-ev1) {ev0.elapsed_time(ev1)*1e3:.1f}us "
+       f"lanes enter span {(t_in_max-t_in)/1e3:.1f}us exit at {(t_out-t_in)/1e3:.1f}us")
+if lm.any():
+    msg += f" first_land {(int(land[lm].min())-t_in)/1e3:.1f}us last_land {(int(land[lm].max())-t_in)/1e3:.1f}us"
+out = [None] * world
+dist.all_gather_object(out, msg)
+if rank == 0:
+    print("\n".join(out))
+dist.barrier(device_ids=[local]); comm.close(); dist.destroy_process_group()
