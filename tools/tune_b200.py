@@ -1,0 +1,100 @@
+#!/usr/bin/env python3
+"""Re-derive the tuning table on B200 from MEASURED latencies (the paper's
+collective tuning framework, with a Measured oracle).
+
+  torchrun --nproc-per-node N tools/tune_b200.py --out tables/b200_measured_nN.csv
+
+Runs the reference tuner algorithm (bcl::tune: argmin per swept size,
+geometric-mean range bounds, merged ranges, tie-breaks of tuner.cpp:84-92)
+with cost(config, n, M) = median over iterations of the max-over-ranks device
+latency of our broadcast (GPU-gated, device-barrier-aligned, CUDA events).
+Every rank evaluates the same candidate sequence, so each cost call is a
+collective measurement."""
+import argparse
+import math
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+import paper_1707_09414_b200 as B  # noqa: E402
+from paper_1707_09414_b200.comm import DevicePtr  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--out", required=True)
+ap.add_argument("--min", type=int, default=4)
+ap.add_argument("--max", type=int, default=1 << 30)
+ap.add_argument("--iters", type=int, default=5)
+ap.add_argument("--chunks", default="65536,131072,262144,524288,1048576,2097152,4194304")
+ap.add_argument("--cands", default="direct,knomial,scatter_ring_allgather,chain_pipelined")
+a = ap.parse_args()
+
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+local = int(os.environ.get("LOCAL_RANK", rank))
+torch.cuda.set_device(local)
+dev = torch.device("cuda", local)
+dist.init_process_group("nccl", device_id=dev)
+comm = B.Comm.connect_torch(world, rank, local, heap_bytes=a.max + (64 << 20), timeout_s=30)
+buf = torch.as_tensor(DevicePtr(comm.alloc(a.max), a.max), device=dev)
+buf.fill_(7 if rank == 0 else 0)
+stream = torch.cuda.Stream(device=dev)
+torch.cuda.synchronize()
+ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+n_eval = [0]
+
+
+def quantize(t):
+    """2 significant digits: costs closer than the timer noise tie, and ties
+    fall to the reference's tie-break order (tuner.cpp:84-92)."""
+    if t <= 0:
+        return t
+    e = math.floor(math.log10(t)) - 1
+    return round(t / 10 ** e) * 10 ** e
+
+
+def cost(cfg, n, m):
+    n_eval[0] += 1
+    times = []
+    iters = a.iters * 4 if m <= (1 << 20) else a.iters
+    for it in range(2 + iters):
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(400_000)
+        comm.barrier(stream)
+        ev0.record(stream)
+        comm.bcast(buf, m, "uint8", 0, cfg, stream=stream)
+        ev1.record(stream)
+        ev1.synchronize()
+        if it >= 2:
+            times.append(ev0.elapsed_time(ev1) * 1e-3)
+    t = torch.tensor(times, dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return quantize(float(statistics.median(t.cpu().tolist())))
+
+
+sizes = []
+s = a.min
+while s <= a.max:
+    sizes.append(s)
+    s *= 2
+cands = []
+for name in a.cands.split(","):
+    cands.append(B.AlgorithmConfig.of(name, radix_k=2 if "knomial" in name else 0))
+chunks = [int(x) for x in a.chunks.split(",")]
+t0 = time.time()
+table = B.tune_measured([world], sizes, cands, chunks, cost,
+                        provenance=f"B200 x{world}, NVLink P2P pulls, median of {a.iters}-{4 * a.iters} "
+                                   f"device-timed runs (max over ranks, 2 significant digits), "
+                                   f"{time.strftime('%Y-%m-%d')}")
+comm.check(stream)
+if rank == 0:
+    os.makedirs(os.path.dirname(os.path.abspath(a.out)), exist_ok=True)
+    B.save_table(table, a.out)
+    print(f"wrote {a.out}: {len(table.entries)} entries from {n_eval[0]} measurements in {time.time() - t0:.1f}s")
+    print(table.text())
+dist.barrier(device_ids=[local])
+comm.close()
+dist.destroy_process_group()
