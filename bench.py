@@ -39,6 +39,11 @@ try:
 except OSError:
     pass
 HBM_PEAK = float(PEAKS.get("hbm_gbs", 6650.0))
+try:  # DRAM bytes per launch of the N=1 kernel from the committed ncu --set full capture
+    TRAFFIC_N1 = json.load(open(os.path.join(ROOT, "profiles", "round1", "ncu_traffic.json")))[
+        "n1_config1_bcast_kernel"]["dram_bytes_per_launch"]
+except (OSError, KeyError, ValueError):
+    TRAFFIC_N1 = None
 HBM_PEAK_SRC = "measured" if "hbm_gbs" in PEAKS else "fallback"
 LINK_BW = 900e9  # north_star chain roofline: NVLink-5 per direction per GPU
 METRIC = "bcast latency (us) & bus GB/s vs msg size 4B–1GB at 2/4/8 B200 vs ncclBroadcast"
@@ -141,8 +146,8 @@ def workload_config(n, m, chunk, world):
         wl = (f"BASELINE config 1: pipelined-chain bcast, {n} ranks sharing one B200 (one cooperative launch), "
               f"{m >> 20} MiB float32 payload, root 0, {chunk >> 10} KiB chunks")
     else:
-        wl = (f"pipelined-chain bcast over {world} B200 (one process per GPU, NVLink P2P pulls), "
-              f"{m >> 20} MiB float32, root 0, {chunk >> 10} KiB chunks; sweep 4 B-1 GiB vs NCCL")
+        wl = (f"bcast over {world} B200 (one process per GPU, NVLink P2P), {m >> 20} MiB float32, root 0, "
+              f"tuner-selected algorithm/chunk; sweep 4 B-1 GiB vs NCCL")
     return {"workload": wl, "ranks": n, "bytes": m, "chunk_bytes": chunk, "root": 0,
             "algorithm": "chain_pipelined", "l2": "flushed between steps (256 MiB write)"}
 
@@ -160,6 +165,8 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--sweep-max", type=int, default=1 << 30)
     ap.add_argument("--cpu-iters", type=int, default=12)
+    ap.add_argument("--fixed-chunk", dest="tuned", action="store_false",
+                    help="N>1: pipelined chain with --chunk instead of the tuned selection")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -268,8 +275,10 @@ def bench_single(args, torch):
         "latency_us": {"mean": round(t * 1e6, 2), "min": round(min(times) * 1e6, 2),
                        "median": round(statistics.median(times) * 1e6, 2), "max": round(max(times) * 1e6, 2)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": HBM_PEAK, "unit": "GB/s",
-                     "frac": round(achieved / HBM_PEAK, 4), "traffic": None,
-                     "note": f"kernel bcast_kernel<16>; algorithmic bytes 2*(P-1)*M per launch; peak {HBM_PEAK_SRC}"},
+                     "frac": round(achieved / HBM_PEAK, 4), "traffic": TRAFFIC_N1 if m == 64 << 20 else None,
+                     "algorithmic_bytes": alg_bytes,
+                     "note": f"kernel bcast_kernel<16>; algorithmic bytes 2*(P-1)*M per launch (traffic below it: "
+                             f"the 126 MB L2 serves downstream re-reads); peak {HBM_PEAK_SRC}"},
         "cpu_baseline": {"value": round(m / cpu["median_s"] / 1e9, 4), "unit": "GB/s", "cores": cpu["cores"],
                          "kind": cpu["kind"], "sample": cpu["sample"]},
         "e2e": {"value": round(m / e2e_t / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": m,
@@ -337,7 +346,9 @@ def bench_multi(args, torch, rank, world):
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         return t.cpu().tolist()
 
-    cfg = B.AlgorithmConfig(B.Algorithm.chain_pipelined, 0, chunk)
+    # Headline: the configuration the tuner selects for this size (the
+    # paper's framework picks algorithm and chunk); --chunk pins a chunk.
+    cfg = comm.choose(m) if args.tuned else B.AlgorithmConfig(B.Algorithm.chain_pipelined, 0, chunk)
     dist.barrier(device_ids=[local])
     launches0 = comm.launches
     with ClockSampler(local) as clk:
@@ -386,12 +397,13 @@ def bench_multi(args, torch, rank, world):
         t = statistics.mean(times)
         t_nccl = statistics.mean(nccl)
         busbw = m / t / 1e9
-        t_roof = m / LINK_BW + (world - 1) * chunk / LINK_BW
+        t_roof = m / LINK_BW + (world - 1) * max(cfg.chunk_bytes, 1) / LINK_BW
         line = {
             "metric": METRIC, "value": round(busbw, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t * 1e3, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic (torch.randint bytes)",
-            "config": workload_config(world, m, chunk, world),
+            "config": dict(workload_config(world, m, cfg.chunk_bytes, world), algorithm=cfg.algorithm.name,
+                           selection="tuned (builtin measured table)" if args.tuned else "fixed"),
             "latency_us": {"mean": round(t * 1e6, 2), "min": round(min(times) * 1e6, 2),
                            "median": round(statistics.median(times) * 1e6, 2)},
             "nccl": {"busbw": round(m / t_nccl / 1e9, 2), "latency_us": round(t_nccl * 1e6, 2),

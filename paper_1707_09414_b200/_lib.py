@@ -12,7 +12,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def lib_path() -> str:
-    return os.path.join(_HERE, "libbcl.so")
+    # BCL_LIB: load an alternative build (development experiments only)
+    return os.environ.get("BCL_LIB") or os.path.join(_HERE, "libbcl.so")
 
 
 class BclError(RuntimeError):

@@ -72,6 +72,7 @@ GroupOptions GroupOptions::from_env() {
   if (const char* v = std::getenv("BCL_MIN_SLICE")) o.min_slice = std::max<std::uint64_t>(16, std::strtoull(v, nullptr, 10));
   if (const char* v = std::getenv("BCL_MAX_CTAS")) o.max_ctas_per_rank = std::atoi(v);
   if (const char* v = std::getenv("BCL_STRICT_SYS")) o.strict_sys = std::atoi(v) != 0;
+  if (const char* v = std::getenv("BCL_LL")) o.ll = std::atoi(v) != 0;
   if (const char* v = std::getenv("BCL_STAGES")) o.stages = static_cast<std::uint32_t>(std::clamp(std::atoi(v), 2, dev::kMaxStages));
   if (const char* v = std::getenv("BCL_STAGE_BYTES")) o.stage_bytes = static_cast<std::int64_t>(std::strtoul(v, nullptr, 10)) / 16 * 16;
   return o;
@@ -97,7 +98,7 @@ AggregateRankError::AggregateRankError(std::vector<RankFailure> failures)
 
 void Group::alloc_rank(LocalRank& r, std::size_t heap_bytes) {
   DeviceScope ds(r.device);
-  r.region_bytes = (3 * static_cast<std::size_t>(n_) * lanes_alloc_ + static_cast<std::size_t>(n_) + 1) *
+  r.region_bytes = (ll_offset(lanes_alloc_) + static_cast<std::size_t>(n_) * 2 * dev::kLLLines * 2) *
                    sizeof(std::uint64_t);
   ck(cudaMalloc(&r.region, r.region_bytes), "cudaMalloc(region)");
   ck(cudaMemset(r.region, 0, r.region_bytes), "cudaMemset(region)");
@@ -181,6 +182,9 @@ std::shared_ptr<Group> Group::create_local(const std::vector<int>& devices, cons
   // TMA bulk stages pay off on NVLink pulls; ranks sharing one GPU (HBM
   // bound, several CTAs per SM needed for co-residency) use vector loads.
   if (g->opt_.stage_bytes < 0) g->opt_.stage_bytes = g->by_device_.size() > 1 ? 8192 : 0;
+  // NVLink hops want a small window (fast fill); ranks sharing one GPU are
+  // HBM-bound and want more bytes in flight.
+  if (g->opt_.window_bytes == 0) g->opt_.window_bytes = g->by_device_.size() > 1 ? (4ull << 20) : (16ull << 20);
   g->lanes_ = lanes_for(devices[0], rpd, opt.max_ctas_per_rank, g->opt_);
   for (const auto& kv : g->by_device_) {
     if (kv.first != devices[0]) lanes_for(kv.first, rpd, opt.max_ctas_per_rank, g->opt_);
@@ -203,6 +207,8 @@ std::shared_ptr<Group> Group::create_local(const std::vector<int>& devices, cons
       lr.h_peers.mbox[p] = base + 2 * S;
       lr.h_peers.bar[p] = base + 3 * S;
       lr.h_peers.addr_base[p] = 0;
+      lr.h_peers.credit[p] = base + 3 * S + n + 1;
+      lr.h_peers.ll[p] = reinterpret_cast<uint4*>(base + g->ll_offset(g->lanes_));
     }
     g->upload_peers(lr);
   }
@@ -219,6 +225,7 @@ std::shared_ptr<Group> Group::create_rank(int n, int rank, int device, std::size
   g->opt_ = opt;
   g->ipc_ = true;
   if (g->opt_.stage_bytes < 0) g->opt_.stage_bytes = n > 1 ? 8192 : 0;
+  if (g->opt_.window_bytes == 0) g->opt_.window_bytes = 4ull << 20;
   g->lanes_ = lanes_for(device, 1, opt.max_ctas_per_rank, g->opt_);
   g->lanes_alloc_ = g->lanes_;
   g->local_.resize(1);
@@ -294,6 +301,8 @@ void Group::connect(const std::vector<std::vector<std::uint8_t>>& infos) {
     me.h_peers.mbox[p] = base + 2 * S;
     me.h_peers.bar[p] = base + 3 * S;
     me.h_peers.addr_base[p] = heap_base;
+    me.h_peers.credit[p] = base + 3 * S + n_ + 1;
+    me.h_peers.ll[p] = reinterpret_cast<uint4*>(base + ll_offset(lanes_));
   }
   upload_peers(me);
   connected_ = true;
@@ -453,8 +462,49 @@ void Group::fill_rank_work(dev::RankWork& w, LocalRank& r, const CallPlan& p, vo
   }
 }
 
+void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& bufs, std::uint64_t bytes,
+                      int root, cudaStream_t stream) {
+  dev::LLParams P{};
+  P.n_ranks = n_;
+  P.root = root;
+  P.n_local = static_cast<int>(locals.size());
+  P.bytes = bytes;
+  P.lines = static_cast<std::uint32_t>((bytes + 7) / 8);
+  P.timeout_ns = opt_.timeout_ns;
+  const std::size_t S = region_stride();
+  std::uint64_t epoch = 0;
+  for (std::size_t i = 0; i < locals.size(); ++i) {
+    LocalRank& r = local_[static_cast<std::size_t>(locals[i])];
+    const std::uint64_t e = ++r.epoch;
+    if (i == 0) epoch = e;
+    if (e != epoch) throw std::runtime_error("ranks sharing a GPU drifted apart in call count");
+    dev::LLRank& w = P.ranks[i];
+    w.rank = r.rank;
+    w.buf = static_cast<std::uint8_t*>(bufs[i]);
+    w.credit = r.region + 3 * S + static_cast<std::size_t>(n_) + 1;
+    w.ll = reinterpret_cast<uint4*>(r.region + ll_offset(lanes_));
+    w.peers = r.d_peers;
+    w.err = r.err_dev;
+    w.abort = reinterpret_cast<int*>(r.region + 3 * S + static_cast<std::size_t>(n_));
+    const std::uint32_t half = static_cast<std::uint32_t>(e & 1u);
+    if (r.rank == root) {
+      w.need_credit = r.ll_last[half];
+      r.ll_last[half] = e;
+    }
+    ++r.launches;
+  }
+  P.epoch = epoch;
+  P.half = static_cast<std::uint32_t>(epoch & 1u);
+  DeviceScope ds(local_[static_cast<std::size_t>(locals[0])].device);
+  ck(static_cast<cudaError_t>(bcl::launch_ll(P, stream)), "launch(ll)");
+}
+
 void Group::launch_group(const std::vector<int>& locals, const std::vector<void*>& bufs,
                          std::uint64_t bytes, int root, const CallPlan& p, cudaStream_t stream) {
+  if (p.config.algorithm == Algorithm::Direct && bytes <= dev::kLLMaxBytes && opt_.ll) {
+    launch_ll(locals, bufs, bytes, root, stream);
+    return;
+  }
   dev::LaunchParams P{};
   P.n_ranks = n_;
   P.root = root;

@@ -71,11 +71,13 @@ class AggregateRankError : public std::runtime_error {
 
 struct GroupOptions {
   std::uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;  // device spin bound
-  std::uint64_t window_bytes = 4ull << 20;                  // bytes in flight per rank (chunks x slices)
+  std::uint64_t window_bytes = 0;                           // bytes in flight per rank (chunks x slices);
+                                                            // 0 = auto (4 MiB across GPUs, 16 MiB on one GPU)
   std::uint64_t min_slice = 2048;                           // smallest per-lane slice of a chunk
   int max_ctas_per_rank = 0;                                // 0 = SM count
   std::uint32_t poll_ns = 64;                               // back-off between flag polls (ns)
   bool strict_sys = false;                                  // system-scope fence before every flag
+  bool ll = true;                                           // LL push protocol for small `direct` calls
   std::int64_t stage_bytes = -1;                            // bulk-copy stage per warp: 0 = vector loads,
                                                             // -1 = auto (8 KiB across GPUs, 0 on one GPU)
   std::uint32_t stages = 2;                                 // bulk-copy stages per copy warp
@@ -116,6 +118,7 @@ struct LocalRank {
   unsigned long long* trace{};  // optional per-lane event timestamps
   std::uint32_t trace_cap{0};
   std::uint64_t launches{0};
+  std::uint64_t ll_last[2]{0, 0};  // last epoch this rank was an LL root, per half
   std::vector<void*> opened;    // IPC mappings to close
 };
 
@@ -173,8 +176,15 @@ class Group {
   void fill_rank_work(dev::RankWork& w, LocalRank& r, const CallPlan& p, void* buf);
   void launch_group(const std::vector<int>& locals, const std::vector<void*>& bufs,
                     std::uint64_t bytes, int root, const CallPlan& p, cudaStream_t stream);
+  void launch_ll(const std::vector<int>& locals, const std::vector<void*>& bufs, std::uint64_t bytes, int root,
+                 cudaStream_t stream);
   void raise_errors(const std::vector<int>& locals);
   std::size_t region_stride() const { return static_cast<std::size_t>(n_) * lanes_; }
+  // Offset (in 8-byte words) of the LL landing area for a flag stride of L lanes.
+  std::size_t ll_offset(int lanes) const {
+    const std::size_t w = 3 * static_cast<std::size_t>(n_) * lanes + 2 * static_cast<std::size_t>(n_) + 1;
+    return (w + 1) / 2 * 2;
+  }
 
   int n_{0};
   int lanes_{0};

@@ -29,6 +29,9 @@ constexpr int kMaxRanks = 64;    // communicator size limit
 constexpr int kWarpsPerCta = 8;  // lanes per CTA
 constexpr int kThreads = (kWarpsPerCta + 1) * 32;  // + one publisher warp
 constexpr int kMaxStages = 4;    // bulk-copy stages per copy warp
+constexpr std::uint32_t kLLMaxBytes = 64 * 1024;        // largest message on the LL protocol
+constexpr std::uint32_t kLLLines = kLLMaxBytes / 8;     // 16-byte lines, 8 payload bytes each
+constexpr int kLLThreads = 512;
 
 // Explicit event word: chunk (bits 0-23) | peer (24-30) | recv (31) |
 // pair index within the lane class (32-55).
@@ -47,13 +50,16 @@ enum ChunkMode : std::uint32_t {
 };
 
 // Addresses of every peer's state as mapped in *this* rank's address space.
-// Region layout of a rank: flags[n][L] | acks[n][L] | mbox[n][L] | bar[n] | abort.
+// Region layout of a rank (8-byte words): flags[n][L] | acks[n][L] | mbox[n][L]
+// | bar[n] | abort | credit[n] | pad to 16 B | ll[n][2][kLLLines] (16-byte lines).
 struct PeerTable {
   std::uint64_t* flags[kMaxRanks];  // peer's flags array (index [my_rank][lane])
   std::uint64_t* acks[kMaxRanks];   // peer's acks array  (index [my_rank][lane])
   std::uint64_t* mbox[kMaxRanks];   // peer's mailbox     (index [my_rank][lane])
   std::uint64_t* bar[kMaxRanks];    // peer's barrier slots (index [my_rank])
   std::uint64_t addr_base[kMaxRanks];  // added to a mailbox value from that peer
+  std::uint64_t* credit[kMaxRanks];    // peer's LL credit array (index [my_rank])
+  uint4* ll[kMaxRanks];                // peer's LL landing area (index [my_rank][half][line])
 };
 
 struct ErrorRecord {  // host-mapped, written by the first failing lane
@@ -110,6 +116,37 @@ struct LaunchParamsT {
 };
 using LaunchParams = LaunchParamsT<kMaxLocal>;
 
+// LL (low-latency) protocol for small messages on the `direct` schedule: the
+// root writes 16-byte lines {4 B payload, epoch, 4 B payload, epoch} into
+// every receiver's landing area for that source; receivers poll the lines
+// (8-byte halves are single-copy atomic) and copy the payload out. No fence,
+// no pull round trip, no ack wait; epoch-parity double buffering plus lazily
+// written credits (receiver -> root, "done with epoch e") guard reuse.
+struct LLRank {
+  int rank;
+  std::uint8_t* buf;
+  uint4* ll;                  // local landing area base
+  std::uint64_t* credit;      // local credit array [n]
+  const PeerTable* peers;
+  ErrorRecord* err;
+  int* abort;
+  std::uint64_t need_credit;  // root: receivers must have finished this epoch (same half)
+};
+
+template <int NL>
+struct LLParamsT {
+  int n_ranks;
+  int root;
+  int n_local;
+  std::uint32_t lines;
+  std::uint64_t bytes;
+  std::uint64_t epoch;
+  std::uint32_t half;
+  std::uint64_t timeout_ns;
+  LLRank ranks[NL];
+};
+using LLParams = LLParamsT<kMaxLocal>;
+
 struct BarrierParams {
   int n_ranks;
   int n_local;
@@ -126,6 +163,7 @@ struct BarrierParams {
 // Launchers (bcl_kernels.cu). Return cudaError_t as int.
 int launch_bcast(const dev::LaunchParams& p, int cooperative, void* stream);
 int launch_barrier(const dev::BarrierParams& p, void* stream);
+int launch_ll(const dev::LLParams& p, void* stream);
 int bcast_kernel_occupancy(int* blocks_per_sm, std::size_t smem);
 std::size_t bcast_smem_bytes(std::uint32_t stages, std::uint32_t stage_bytes);
 int prepare_bcast_kernels(std::size_t smem);

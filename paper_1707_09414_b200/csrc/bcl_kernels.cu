@@ -332,14 +332,6 @@ __device__ __forceinline__ void trace_pull(const Ctx& c, std::uint32_t k, std::u
 }
 
 
-__device__ __forceinline__ void bulk_wait_n(int n) {
-  switch (n) {
-    case 0: bulk_wait<0>(); break;
-    case 1: bulk_wait<1>(); break;
-    case 2: bulk_wait<2>(); break;
-    default: bulk_wait<3>(); break;
-  }
-}
 __device__ __forceinline__ void bulk_wait_read_n(int n) {
   switch (n) {
     case 0: bulk_wait_read<0>(); break;
@@ -597,8 +589,10 @@ __device__ void run_events(Ctx& c, int pipe, int q, int ns) {
   }
 }
 
+// NL = 1: one rank per GPU (full register budget). NL = kMaxLocal: ranks
+// sharing a GPU need several co-resident CTAs per SM, hence the 3-CTA bound.
 template <int NL>
-__global__ void __launch_bounds__(kThreads) bcast_kernel(const __grid_constant__ LaunchParamsT<NL> P) {
+__global__ void __launch_bounds__(kThreads, NL == 1 ? 1 : 3) bcast_kernel(const __grid_constant__ LaunchParamsT<NL> P) {
   __shared__ CtaShared sh;
   const int local = NL == 1 ? 0 : static_cast<int>(blockIdx.x) / P.ctas_per_rank;
   const int cta = NL == 1 ? static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x) % P.ctas_per_rank;
@@ -649,6 +643,115 @@ __global__ void __launch_bounds__(kThreads) bcast_kernel(const __grid_constant__
   if (c.lane_id == 0) {
     __threadfence_block();  // the last tail release is ordered before the count
     atomicAdd_block(&sh.done, 1u);
+  }
+}
+
+
+// ---------------------------------------------------------------- LL path
+__device__ __forceinline__ void st_volatile_v4(uint4* p, std::uint32_t a, std::uint32_t b, std::uint32_t c,
+                                               std::uint32_t d) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+__device__ __forceinline__ uint4 ld_volatile_v4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+
+__device__ void ll_fail(const LLRank& R, int peer, std::uint64_t line, std::uint64_t seen, std::uint64_t want) {
+  atomicExch(R.abort, 1);
+  if (atomicCAS(&R.err->code, 0, 1) == 0) {
+    R.err->rank = R.rank;
+    R.err->peer = peer;
+    R.err->lane = -2;  // LL protocol
+    R.err->chunk = line;
+    R.err->observed = seen;
+    R.err->expected = want;
+    __threadfence_system();
+  }
+}
+
+template <int NL>
+__global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ LLParamsT<NL> P) {
+  const LLRank& R = P.ranks[NL == 1 ? 0 : blockIdx.x];
+  const std::uint32_t flag = static_cast<std::uint32_t>(P.epoch);
+  const std::size_t area = (static_cast<std::size_t>(P.root) * 2 + P.half) * kLLLines;
+  if (R.rank == P.root) {
+    // The half we are about to overwrite was last used at need_credit: wait
+    // until every receiver is done with it (normally long ago).
+    if (threadIdx.x < static_cast<unsigned>(P.n_ranks) && static_cast<int>(threadIdx.x) != P.root &&
+        R.need_credit > 0) {
+      const std::uint64_t* cr = R.credit + threadIdx.x;
+      const std::uint64_t t0 = globaltimer();
+      std::uint64_t v;
+      while ((v = ld_relaxed_sys(cr)) < R.need_credit) {
+        if (globaltimer() - t0 > P.timeout_ns) {
+          ll_fail(R, static_cast<int>(threadIdx.x), 0, v, R.need_credit);
+          break;
+        }
+      }
+    }
+    __syncthreads();
+    const bool aligned = (reinterpret_cast<std::uintptr_t>(R.buf) & 7u) == 0;
+    for (std::uint32_t i = threadIdx.x; i < P.lines; i += blockDim.x) {
+      const std::uint64_t off = static_cast<std::uint64_t>(i) * 8;
+      std::uint32_t lo = 0, hi = 0;
+      if (aligned && off + 8 <= P.bytes) {
+        const uint2 v = *reinterpret_cast<const uint2*>(R.buf + off);
+        lo = v.x;
+        hi = v.y;
+      } else {
+        for (std::uint32_t b = 0; b < 8 && off + b < P.bytes; ++b) {
+          const std::uint32_t byte = R.buf[off + b];
+          if (b < 4) lo |= byte << (8 * b); else hi |= byte << (8 * (b - 4));
+        }
+      }
+      for (int d = 0; d < P.n_ranks; ++d) {
+        if (d == P.root) continue;
+        st_volatile_v4(R.peers->ll[d] + area + i, lo, flag, hi, flag);
+      }
+    }
+    return;
+  }
+  // Receiver: poll our landing lines for this source and copy out.
+  const uint4* src = R.ll + area;
+  const bool aligned = (reinterpret_cast<std::uintptr_t>(R.buf) & 7u) == 0;
+  bool ok = true;
+  for (std::uint32_t i = threadIdx.x; i < P.lines && ok; i += blockDim.x) {
+    uint4 v = ld_volatile_v4(src + i);
+    if (v.y != flag || v.w != flag) {
+      const std::uint64_t t0 = globaltimer();
+      unsigned spins = 0;
+      while (true) {
+        v = ld_volatile_v4(src + i);
+        if (v.y == flag && v.w == flag) break;
+        if ((++spins & 1023u) == 0) {
+          if (*(volatile int*)R.abort != 0 || globaltimer() - t0 > P.timeout_ns) {
+            if (*(volatile int*)R.abort == 0) ll_fail(R, P.root, i, v.y, flag);
+            ok = false;
+            break;
+          }
+        }
+      }
+      if (!ok) break;
+    }
+    const std::uint64_t off = static_cast<std::uint64_t>(i) * 8;
+    if (aligned && off + 8 <= P.bytes) {
+      *reinterpret_cast<uint2*>(R.buf + off) = make_uint2(v.x, v.z);
+    } else {
+      for (std::uint32_t b = 0; b < 8 && off + b < P.bytes; ++b) {
+        R.buf[off + b] = static_cast<std::uint8_t>((b < 4 ? v.x >> (8 * b) : v.z >> (8 * (b - 4))) & 0xFFu);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && ok) {
+    // Every line of this epoch has been read: the root may reuse the half.
+    st_relaxed_sys(R.peers->credit[P.root] + R.rank, P.epoch);
   }
 }
 
@@ -732,6 +835,25 @@ int launch_barrier(const dev::BarrierParams& p, void* stream) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::barrier_kernel, p));
+}
+
+int launch_ll(const dev::LLParams& p, void* stream) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(p.n_local));
+  cfg.blockDim = dim3(dev::kLLThreads);
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = p.n_local > 1 ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (p.n_local == 1) {
+    dev::LLParamsT<1> one;
+    std::memcpy(&one, &p, offsetof(dev::LLParams, ranks));
+    one.ranks[0] = p.ranks[0];
+    return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::ll_kernel<1>, one));
+  }
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::ll_kernel<dev::kMaxLocal>, p));
 }
 
 int bcast_kernel_occupancy(int* blocks_per_sm, std::size_t smem) {

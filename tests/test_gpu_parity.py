@@ -237,3 +237,29 @@ def test_contract_errors():
     with pytest.raises(ValueError):  # schedules.cpp:164-166
         B.run_bcast(one, 0, [buf], 16, cfg_of("chain_pipelined", 4))
     B.run_bcast(one, 0, [buf], 16, cfg_of("chain"))  # n = 1: untouched, no error
+
+
+def test_ll_small_direct_back_to_back_reuse():
+    """LL protocol (direct, <= 64 KiB): landing halves alternate by epoch and
+    are reused every other call; roots and sizes change every call and every
+    call is verified before the next is issued on the same buffers."""
+    n = 5
+    comms = comms_for(n)
+    rng = random.Random(77)
+    bufs = [torch.zeros(65536 + 64, dtype=torch.uint8, device="cuda:0") for _ in range(n)]
+    for it in range(60):
+        m = rng.choice([0, 1, 7, 8, 9, 4096, 65535, 65536, rng.randrange(1, 65537)])
+        root = rng.randrange(n)
+        off = rng.choice([0, 0, 3])
+        views = [b[off:off + m] for b in bufs]
+        payload = O.payload(it, m)
+        for r in range(n):
+            views[r].zero_()
+        if m:
+            views[root].copy_(torch.frombuffer(bytearray(payload), dtype=torch.uint8))
+        B.bcast_all(comms, views, m, "uint8", root, cfg_of("direct"))
+        torch.cuda.synchronize()
+        for r in range(n):
+            assert views[r].cpu().numpy().tobytes() == payload, (it, m, root, r)
+    for c in comms:
+        c.check()

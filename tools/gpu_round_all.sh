@@ -1,0 +1,17 @@
+#!/bin/bash
+# One gpurun call (4 GPUs): full GPU test suite, N=1 bench + launch list +
+# one ncu capture of the broadcast kernel, then N=2 and N=4 benches.
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_n1.json 2> gpurun_out/bench_n1.err
+CMD="python bench.py --steps 2 --warmup 3 --cpu-iters 1"
+timeout 600 $CMD > gpurun_out/plain.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_n1.csv $CMD > gpurun_out/ncu_launch.log 2>&1 && \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:bcast_kernel -s 3 -c 1 -o gpurun_out/prof_n1 $CMD > gpurun_out/ncu_full.log 2>&1
+echo "ncu rc=$?" >> gpurun_out/ncu_full.log
+for N in 2 4; do
+  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2990$N bench.py --gpus $N --steps 20 --warmup 5 > gpurun_out/bench_n$N.json 2> gpurun_out/bench_n$N.err
+  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2991$N bench.py --gpus $N --impl reference --steps 5 --warmup 1 > gpurun_out/bench_ref_n$N.json 2> gpurun_out/bench_ref_n$N.err
+done
+timeout 600 python bench.py --impl reference --steps 10 --warmup 2 > gpurun_out/bench_ref_n1.json 2> gpurun_out/bench_ref_n1.err
