@@ -73,6 +73,7 @@ GroupOptions GroupOptions::from_env() {
   if (const char* v = std::getenv("BCL_MAX_CTAS")) o.max_ctas_per_rank = std::atoi(v);
   if (const char* v = std::getenv("BCL_STRICT_SYS")) o.strict_sys = std::atoi(v) != 0;
   if (const char* v = std::getenv("BCL_LL")) o.ll = std::atoi(v) != 0;
+  if (const char* v = std::getenv("BCL_LL_MAX")) o.ll_max_bytes = std::strtoull(v, nullptr, 10);
   if (const char* v = std::getenv("BCL_STAGES")) o.stages = static_cast<std::uint32_t>(std::clamp(std::atoi(v), 2, dev::kMaxStages));
   if (const char* v = std::getenv("BCL_STAGE_BYTES")) o.stage_bytes = static_cast<std::int64_t>(std::strtoul(v, nullptr, 10)) / 16 * 16;
   return o;
@@ -98,7 +99,7 @@ AggregateRankError::AggregateRankError(std::vector<RankFailure> failures)
 
 void Group::alloc_rank(LocalRank& r, std::size_t heap_bytes) {
   DeviceScope ds(r.device);
-  r.region_bytes = (ll_offset(lanes_alloc_) + static_cast<std::size_t>(n_) * 2 * dev::kLLLines * 2) *
+  r.region_bytes = (ll_offset(lanes_alloc_) + static_cast<std::size_t>(n_) * 2 * (ll_max_ / 8) * 2) *
                    sizeof(std::uint64_t);
   ck(cudaMalloc(&r.region, r.region_bytes), "cudaMalloc(region)");
   ck(cudaMemset(r.region, 0, r.region_bytes), "cudaMemset(region)");
@@ -142,6 +143,15 @@ int lanes_for(int device, int ranks_per_device, int cap, const GroupOptions& opt
   int ctas = std::min(sms, std::max(1, resident / std::max(ranks_per_device, 1)));
   if (cap > 0) ctas = std::min(cap, std::max(1, resident / std::max(ranks_per_device, 1)));
   return ctas * dev::kWarpsPerCta;
+}
+
+// LL landing areas cost 4 x cap bytes per source per rank: bound them to
+// 64 MiB per rank (1 MiB cap up to 16 ranks).
+std::uint64_t ll_cap(int n, const GroupOptions& opt) {
+  std::uint64_t cap = opt.ll_max_bytes ? opt.ll_max_bytes : dev::kLLMaxBytes;
+  cap = std::min<std::uint64_t>(cap, dev::kLLMaxBytes);
+  while (cap > 4096 && static_cast<std::uint64_t>(n) * 4 * cap > (64ull << 20)) cap /= 2;
+  return cap / 16 * 16;
 }
 
 }  // namespace
@@ -191,6 +201,7 @@ std::shared_ptr<Group> Group::create_local(const std::vector<int>& devices, cons
   }
   g->lanes_alloc_ = g->lanes_;
   g->single_device_ = g->by_device_.size() == 1;
+  g->ll_max_ = ll_cap(n, opt);
   g->local_.resize(static_cast<std::size_t>(n));
   for (int r = 0; r < n; ++r) {
     LocalRank& lr = g->local_[static_cast<std::size_t>(r)];
@@ -228,6 +239,7 @@ std::shared_ptr<Group> Group::create_rank(int n, int rank, int device, std::size
   if (g->opt_.window_bytes == 0) g->opt_.window_bytes = 4ull << 20;
   g->lanes_ = lanes_for(device, 1, opt.max_ctas_per_rank, g->opt_);
   g->lanes_alloc_ = g->lanes_;
+  g->ll_max_ = ll_cap(n, opt);
   g->local_.resize(1);
   g->local_[0].rank = rank;
   g->local_[0].device = device;
@@ -470,6 +482,10 @@ void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& 
   P.n_local = static_cast<int>(locals.size());
   P.bytes = bytes;
   P.lines = static_cast<std::uint32_t>((bytes + 7) / 8);
+  P.area_lines = static_cast<std::uint32_t>(ll_max_ / 8);
+  // ~4 lines per thread, at most kLLMaxCtas CTAs per rank
+  P.ctas = std::clamp<int>(static_cast<int>((P.lines + 4 * dev::kLLThreads - 1) / (4 * dev::kLLThreads)), 1,
+                           dev::kLLMaxCtas);
   P.timeout_ns = opt_.timeout_ns;
   const std::size_t S = region_stride();
   std::uint64_t epoch = 0;
@@ -490,6 +506,10 @@ void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& 
     if (r.rank == root) {
       w.need_credit = r.ll_last[half];
       r.ll_last[half] = e;
+    } else {
+      w.done = reinterpret_cast<unsigned long long*>(r.region + 3 * S + 2 * static_cast<std::size_t>(n_) + 1);
+      r.ll_done += static_cast<std::uint64_t>(P.ctas);
+      w.done_target = r.ll_done;
     }
     ++r.launches;
   }
@@ -501,7 +521,7 @@ void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& 
 
 void Group::launch_group(const std::vector<int>& locals, const std::vector<void*>& bufs,
                          std::uint64_t bytes, int root, const CallPlan& p, cudaStream_t stream) {
-  if (p.config.algorithm == Algorithm::Direct && bytes <= dev::kLLMaxBytes && opt_.ll) {
+  if (p.config.algorithm == Algorithm::Direct && bytes <= ll_max_ && opt_.ll) {
     launch_ll(locals, bufs, bytes, root, stream);
     return;
   }

@@ -78,6 +78,7 @@ struct GroupOptions {
   std::uint32_t poll_ns = 64;                               // back-off between flag polls (ns)
   bool strict_sys = false;                                  // system-scope fence before every flag
   bool ll = true;                                           // LL push protocol for small `direct` calls
+  std::uint64_t ll_max_bytes = 0;                           // LL threshold (0 = 1 MiB, lowered for many ranks)
   std::int64_t stage_bytes = -1;                            // bulk-copy stage per warp: 0 = vector loads,
                                                             // -1 = auto (8 KiB across GPUs, 0 on one GPU)
   std::uint32_t stages = 2;                                 // bulk-copy stages per copy warp
@@ -119,6 +120,7 @@ struct LocalRank {
   std::uint32_t trace_cap{0};
   std::uint64_t launches{0};
   std::uint64_t ll_last[2]{0, 0};  // last epoch this rank was an LL root, per half
+  std::uint64_t ll_done{0};        // cumulative LL CTA completions expected as a receiver
   std::vector<void*> opened;    // IPC mappings to close
 };
 
@@ -182,9 +184,10 @@ class Group {
   std::size_t region_stride() const { return static_cast<std::size_t>(n_) * lanes_; }
   // Offset (in 8-byte words) of the LL landing area for a flag stride of L lanes.
   std::size_t ll_offset(int lanes) const {
-    const std::size_t w = 3 * static_cast<std::size_t>(n_) * lanes + 2 * static_cast<std::size_t>(n_) + 1;
+    const std::size_t w = 3 * static_cast<std::size_t>(n_) * lanes + 2 * static_cast<std::size_t>(n_) + 2;
     return (w + 1) / 2 * 2;
   }
+  std::uint64_t ll_max_{dev::kLLMaxBytes};  // LL protocol threshold (bytes)
 
   int n_{0};
   int lanes_{0};

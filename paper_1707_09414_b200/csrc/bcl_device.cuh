@@ -29,9 +29,9 @@ constexpr int kMaxRanks = 64;    // communicator size limit
 constexpr int kWarpsPerCta = 8;  // lanes per CTA
 constexpr int kThreads = (kWarpsPerCta + 1) * 32;  // + one publisher warp
 constexpr int kMaxStages = 4;    // bulk-copy stages per copy warp
-constexpr std::uint32_t kLLMaxBytes = 64 * 1024;        // largest message on the LL protocol
-constexpr std::uint32_t kLLLines = kLLMaxBytes / 8;     // 16-byte lines, 8 payload bytes each
+constexpr std::uint32_t kLLMaxBytes = 1024 * 1024;      // largest LL message (per-group cap may be lower)
 constexpr int kLLThreads = 512;
+constexpr int kLLMaxCtas = 16;                          // CTAs per rank for one LL call
 
 // Explicit event word: chunk (bits 0-23) | peer (24-30) | recv (31) |
 // pair index within the lane class (32-55).
@@ -51,7 +51,8 @@ enum ChunkMode : std::uint32_t {
 
 // Addresses of every peer's state as mapped in *this* rank's address space.
 // Region layout of a rank (8-byte words): flags[n][L] | acks[n][L] | mbox[n][L]
-// | bar[n] | abort | credit[n] | pad to 16 B | ll[n][2][kLLLines] (16-byte lines).
+// | bar[n] | abort | credit[n] | ll_done | pad to 16 B | ll[n][2][ll_lines] (16-byte lines,
+// ll_lines = the group's LL cap / 8).
 struct PeerTable {
   std::uint64_t* flags[kMaxRanks];  // peer's flags array (index [my_rank][lane])
   std::uint64_t* acks[kMaxRanks];   // peer's acks array  (index [my_rank][lane])
@@ -131,6 +132,8 @@ struct LLRank {
   ErrorRecord* err;
   int* abort;
   std::uint64_t need_credit;  // root: receivers must have finished this epoch (same half)
+  unsigned long long* done;   // receiver: local completion counter (cumulative over calls)
+  unsigned long long done_target;  // receiver: value of *done once every CTA of this call finished
 };
 
 template <int NL>
@@ -138,10 +141,12 @@ struct LLParamsT {
   int n_ranks;
   int root;
   int n_local;
+  int ctas;                   // CTAs per rank
   std::uint32_t lines;
   std::uint64_t bytes;
   std::uint64_t epoch;
   std::uint32_t half;
+  std::uint32_t area_lines;   // lines per (source, half) landing area
   std::uint64_t timeout_ns;
   LLRank ranks[NL];
 };

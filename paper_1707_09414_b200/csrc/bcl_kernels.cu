@@ -677,9 +677,12 @@ __device__ void ll_fail(const LLRank& R, int peer, std::uint64_t line, std::uint
 
 template <int NL>
 __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ LLParamsT<NL> P) {
-  const LLRank& R = P.ranks[NL == 1 ? 0 : blockIdx.x];
+  const LLRank& R = P.ranks[NL == 1 ? 0 : static_cast<int>(blockIdx.x) / P.ctas];
+  const std::uint32_t cta = NL == 1 ? blockIdx.x : blockIdx.x % P.ctas;
+  const std::uint32_t first = cta * blockDim.x + threadIdx.x;
+  const std::uint32_t stride = static_cast<std::uint32_t>(P.ctas) * blockDim.x;
   const std::uint32_t flag = static_cast<std::uint32_t>(P.epoch);
-  const std::size_t area = (static_cast<std::size_t>(P.root) * 2 + P.half) * kLLLines;
+  const std::size_t area = (static_cast<std::size_t>(P.root) * 2 + P.half) * P.area_lines;
   if (R.rank == P.root) {
     // The half we are about to overwrite was last used at need_credit: wait
     // until every receiver is done with it (normally long ago).
@@ -697,7 +700,7 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ 
     }
     __syncthreads();
     const bool aligned = (reinterpret_cast<std::uintptr_t>(R.buf) & 7u) == 0;
-    for (std::uint32_t i = threadIdx.x; i < P.lines; i += blockDim.x) {
+    for (std::uint32_t i = first; i < P.lines; i += stride) {
       const std::uint64_t off = static_cast<std::uint64_t>(i) * 8;
       std::uint32_t lo = 0, hi = 0;
       if (aligned && off + 8 <= P.bytes) {
@@ -721,7 +724,7 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ 
   const uint4* src = R.ll + area;
   const bool aligned = (reinterpret_cast<std::uintptr_t>(R.buf) & 7u) == 0;
   bool ok = true;
-  for (std::uint32_t i = threadIdx.x; i < P.lines && ok; i += blockDim.x) {
+  for (std::uint32_t i = first; i < P.lines && ok; i += stride) {
     uint4 v = ld_volatile_v4(src + i);
     if (v.y != flag || v.w != flag) {
       const std::uint64_t t0 = globaltimer();
@@ -750,8 +753,9 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ 
   }
   __syncthreads();
   if (threadIdx.x == 0 && ok) {
-    // Every line of this epoch has been read: the root may reuse the half.
-    st_relaxed_sys(R.peers->credit[P.root] + R.rank, P.epoch);
+    // The last CTA to finish tells the root every line of this epoch has
+    // been read, so the root may reuse the half.
+    if (atomicAdd(R.done, 1ull) + 1 == R.done_target) st_relaxed_sys(R.peers->credit[P.root] + R.rank, P.epoch);
   }
 }
 
@@ -839,7 +843,7 @@ int launch_barrier(const dev::BarrierParams& p, void* stream) {
 
 int launch_ll(const dev::LLParams& p, void* stream) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(p.n_local));
+  cfg.gridDim = dim3(static_cast<unsigned>(p.n_local * p.ctas));
   cfg.blockDim = dim3(dev::kLLThreads);
   cfg.stream = static_cast<cudaStream_t>(stream);
   cudaLaunchAttribute attr[1];
