@@ -146,7 +146,7 @@ int lanes_for(int device, int ranks_per_device, int cap, const GroupOptions& opt
 }
 
 // LL landing areas cost 4 x cap bytes per source per rank: bound them to
-// 64 MiB per rank (1 MiB cap up to 16 ranks).
+// 64 MiB per rank (2 MiB cap up to 8 ranks, 1 MiB up to 16).
 std::uint64_t ll_cap(int n, const GroupOptions& opt) {
   std::uint64_t cap = opt.ll_max_bytes ? opt.ll_max_bytes : dev::kLLMaxBytes;
   cap = std::min<std::uint64_t>(cap, dev::kLLMaxBytes);
@@ -484,8 +484,11 @@ void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& 
   P.lines = static_cast<std::uint32_t>((bytes + 7) / 8);
   P.area_lines = static_cast<std::uint32_t>(ll_max_ / 8);
   // ~4 lines per thread, at most kLLMaxCtas CTAs per rank
-  P.ctas = std::clamp<int>(static_cast<int>((P.lines + 4 * dev::kLLThreads - 1) / (4 * dev::kLLThreads)), 1,
-                           dev::kLLMaxCtas);
+  // ~2 lines per thread; ranks sharing a GPU must stay co-resident
+  // (cooperative launch): at most 4 LL CTAs per SM in total.
+  const int resident = std::max(1, 148 * 4 / std::max<int>(1, P.n_local));
+  P.ctas = std::clamp<int>(static_cast<int>((P.lines + 2 * dev::kLLThreads - 1) / (2 * dev::kLLThreads)), 1,
+                           std::min(dev::kLLMaxCtas, resident));
   P.timeout_ns = opt_.timeout_ns;
   const std::size_t S = region_stride();
   std::uint64_t epoch = 0;

@@ -78,7 +78,7 @@ struct GroupOptions {
   std::uint32_t poll_ns = 64;                               // back-off between flag polls (ns)
   bool strict_sys = false;                                  // system-scope fence before every flag
   bool ll = true;                                           // LL push protocol for small `direct` calls
-  std::uint64_t ll_max_bytes = 0;                           // LL threshold (0 = 1 MiB, lowered for many ranks)
+  std::uint64_t ll_max_bytes = 0;                           // LL threshold (0 = 2 MiB, lowered for many ranks)
   std::int64_t stage_bytes = -1;                            // bulk-copy stage per warp: 0 = vector loads,
                                                             // -1 = auto (8 KiB across GPUs, 0 on one GPU)
   std::uint32_t stages = 2;                                 // bulk-copy stages per copy warp

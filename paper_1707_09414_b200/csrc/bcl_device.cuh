@@ -29,9 +29,9 @@ constexpr int kMaxRanks = 64;    // communicator size limit
 constexpr int kWarpsPerCta = 8;  // lanes per CTA
 constexpr int kThreads = (kWarpsPerCta + 1) * 32;  // + one publisher warp
 constexpr int kMaxStages = 4;    // bulk-copy stages per copy warp
-constexpr std::uint32_t kLLMaxBytes = 1024 * 1024;      // largest LL message (per-group cap may be lower)
+constexpr std::uint32_t kLLMaxBytes = 2048 * 1024;      // largest LL message (per-group cap may be lower)
 constexpr int kLLThreads = 512;
-constexpr int kLLMaxCtas = 16;                          // CTAs per rank for one LL call
+constexpr int kLLMaxCtas = 64;                          // CTAs per rank for one LL call
 
 // Explicit event word: chunk (bits 0-23) | peer (24-30) | recv (31) |
 // pair index within the lane class (32-55).
