@@ -74,6 +74,7 @@ GroupOptions GroupOptions::from_env() {
   if (const char* v = std::getenv("BCL_STRICT_SYS")) o.strict_sys = std::atoi(v) != 0;
   if (const char* v = std::getenv("BCL_LL")) o.ll = std::atoi(v) != 0;
   if (const char* v = std::getenv("BCL_LL_MAX")) o.ll_max_bytes = std::strtoull(v, nullptr, 10);
+  if (const char* v = std::getenv("BCL_HOST_PIECE")) o.host_piece = std::max<std::uint64_t>(4096, std::strtoull(v, nullptr, 10));
   if (const char* v = std::getenv("BCL_STAGES")) o.stages = static_cast<std::uint32_t>(std::clamp(std::atoi(v), 2, dev::kMaxStages));
   if (const char* v = std::getenv("BCL_STAGE_BYTES")) o.stage_bytes = static_cast<std::int64_t>(std::strtoul(v, nullptr, 10)) / 16 * 16;
   return o;
@@ -112,6 +113,8 @@ void Group::alloc_rank(LocalRank& r, std::size_t heap_bytes) {
   // Blocking stream: ordered after work on the legacy default stream (e.g. torch
   // fills of the buffers), as the synchronous run_bcast contract expects.
   ck(cudaStreamCreateWithFlags(&r.stream, cudaStreamDefault), "cudaStreamCreate");
+  ck(cudaStreamCreateWithFlags(&r.copy_in, cudaStreamNonBlocking), "cudaStreamCreate(copy_in)");
+  ck(cudaStreamCreateWithFlags(&r.copy_out, cudaStreamNonBlocking), "cudaStreamCreate(copy_out)");
   if (heap_bytes > 0) {
     ck(cudaMalloc(&r.heap, heap_bytes), "cudaMalloc(heap)");
     r.heap_bytes = heap_bytes;
@@ -331,6 +334,9 @@ Group::~Group() {
     if (r.scratch && !ipc_) cudaFree(r.scratch);
     if (r.err_host) cudaFreeHost(r.err_host);
     if (r.stream) cudaStreamDestroy(r.stream);
+    if (r.copy_in) cudaStreamDestroy(r.copy_in);
+    if (r.copy_out) cudaStreamDestroy(r.copy_out);
+    for (cudaEvent_t e : r.events) cudaEventDestroy(e);
   }
 }
 
@@ -606,26 +612,79 @@ void Group::bcast_all(const std::vector<void*>& bufs, std::uint64_t bytes, int r
   }
 }
 
+// Host-buffer broadcasts stage through device scratch in pieces on three
+// streams per rank: H2D of piece i+1 (root) overlaps the device broadcast and
+// the D2H of piece i (receivers). Each piece is an ordinary broadcast call,
+// issued identically on every rank.
+namespace {
+
+struct Piece {
+  std::uint64_t off, len;
+};
+
+std::vector<Piece> pieces_of(std::uint64_t bytes, std::uint64_t piece) {
+  std::vector<Piece> v;
+  if (bytes == 0) return {Piece{0, 0}};
+  for (std::uint64_t off = 0; off < bytes; off += piece) v.push_back(Piece{off, std::min(piece, bytes - off)});
+  return v;
+}
+
+}  // namespace
+
+cudaEvent_t Group::event(LocalRank& r, std::size_t i) {
+  while (r.events.size() <= i) {
+    cudaEvent_t e;
+    ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    r.events.push_back(e);
+  }
+  return r.events[i];
+}
+
+void Group::ensure_scratch(int li, std::uint64_t bytes) {
+  LocalRank& r = local_.at(static_cast<std::size_t>(li));
+  if (bytes <= r.scratch_bytes) return;
+  DeviceScope ds(r.device);
+  if (ipc_) {
+    r.scratch = static_cast<std::uint8_t*>(mem_alloc(li, bytes));
+  } else {
+    if (r.scratch) ck(cudaFree(r.scratch), "cudaFree(scratch)");
+    ck(cudaMalloc(&r.scratch, bytes), "cudaMalloc(scratch)");
+  }
+  r.scratch_bytes = bytes;
+}
+
 void Group::bcast_host(int li, void* host_buf, std::uint64_t bytes, int root,
                        const AlgorithmConfig* cfg, cudaStream_t stream) {
   LocalRank& r = local_.at(static_cast<std::size_t>(li));
+  if (root < 0 || root >= n_) throw std::invalid_argument("root out of range");
+  if (bytes > 0 && host_buf == nullptr) throw std::invalid_argument("null buffer");
+  ensure_scratch(li, bytes);
   DeviceScope ds(r.device);
-  if (bytes > r.scratch_bytes) {
-    if (ipc_) {
-      r.scratch = static_cast<std::uint8_t*>(mem_alloc(li, bytes));
-    } else {
-      if (r.scratch) ck(cudaFree(r.scratch), "cudaFree(scratch)");
-      ck(cudaMalloc(&r.scratch, bytes), "cudaMalloc(scratch)");
+  auto* hb = static_cast<std::uint8_t*>(host_buf);
+  const auto ps = pieces_of(bytes, opt_.host_piece);
+  std::size_t ev = 0;
+  const cudaEvent_t start = event(r, ev++);
+  ck(cudaEventRecord(start, stream), "cudaEventRecord");
+  ck(cudaStreamWaitEvent(r.copy_in, start, 0), "cudaStreamWaitEvent");
+  ck(cudaStreamWaitEvent(r.copy_out, start, 0), "cudaStreamWaitEvent");
+  for (const Piece& p : ps) {
+    if (r.rank == root && p.len) {
+      ck(cudaMemcpyAsync(r.scratch + p.off, hb + p.off, p.len, cudaMemcpyHostToDevice, r.copy_in), "H2D");
+      const cudaEvent_t in = event(r, ev++);
+      ck(cudaEventRecord(in, r.copy_in), "cudaEventRecord");
+      ck(cudaStreamWaitEvent(stream, in, 0), "cudaStreamWaitEvent");
     }
-    r.scratch_bytes = bytes;
+    bcast(li, r.scratch + p.off, p.len, root, cfg, stream);
+    if (r.rank != root && p.len) {
+      const cudaEvent_t done = event(r, ev++);
+      ck(cudaEventRecord(done, stream), "cudaEventRecord");
+      ck(cudaStreamWaitEvent(r.copy_out, done, 0), "cudaStreamWaitEvent");
+      ck(cudaMemcpyAsync(hb + p.off, r.scratch + p.off, p.len, cudaMemcpyDeviceToHost, r.copy_out), "D2H");
+    }
   }
-  if (r.rank == root && bytes > 0) {
-    ck(cudaMemcpyAsync(r.scratch, host_buf, bytes, cudaMemcpyHostToDevice, stream), "H2D");
-  }
-  bcast(li, r.scratch, bytes, root, cfg, stream);
-  if (r.rank != root && bytes > 0) {
-    ck(cudaMemcpyAsync(host_buf, r.scratch, bytes, cudaMemcpyDeviceToHost, stream), "D2H");
-  }
+  const cudaEvent_t out = event(r, ev++);
+  ck(cudaEventRecord(out, r.copy_out), "cudaEventRecord");
+  ck(cudaStreamWaitEvent(stream, out, 0), "cudaStreamWaitEvent");
 }
 
 void Group::raise_errors(const std::vector<int>& locals) {
@@ -678,42 +737,54 @@ double Group::run_bcast_host(const std::vector<void*>& host_bufs, std::uint64_t 
   if (static_cast<int>(host_bufs.size()) != n_ || local_count() != n_) {
     throw std::invalid_argument("one buffer per rank required");
   }
-  for (LocalRank& r : local_) {
-    if (bytes > r.scratch_bytes) {
-      DeviceScope ds(r.device);
-      if (r.scratch) ck(cudaFree(r.scratch), "cudaFree(scratch)");
-      ck(cudaMalloc(&r.scratch, bytes), "cudaMalloc(scratch)");
-      r.scratch_bytes = bytes;
-    }
-  }
-  const auto t0 = std::chrono::steady_clock::now();
   const int root_li = local_index_of(root);
   if (root_li < 0) throw std::invalid_argument("root out of range");
-  const int root_dev = local_[static_cast<std::size_t>(root_li)].device;
-  cudaStream_t root_stream = local_[static_cast<std::size_t>(by_device_.at(root_dev).front())].stream;
-  if (bytes > 0) {
-    DeviceScope ds(root_dev);
-    ck(cudaMemcpyAsync(local_[static_cast<std::size_t>(root_li)].scratch, host_bufs[static_cast<std::size_t>(root)],
-                       bytes, cudaMemcpyHostToDevice, root_stream), "H2D");
+  for (int li = 0; li < n_; ++li) {
+    if (bytes > 0 && host_bufs[static_cast<std::size_t>(li)] == nullptr) throw std::invalid_argument("null buffer");
+    ensure_scratch(li, bytes);
   }
-  std::vector<void*> dbufs;
-  for (LocalRank& r : local_) dbufs.push_back(r.scratch);
-  bcast_all(dbufs, bytes, root, cfg, {});
-  for (const auto& kv : by_device_) {
-    DeviceScope ds(kv.first);
-    cudaStream_t s = local_[static_cast<std::size_t>(kv.second.front())].stream;
-    for (int li : kv.second) {
-      LocalRank& r = local_[static_cast<std::size_t>(li)];
-      if (r.rank != root && bytes > 0) {
-        ck(cudaMemcpyAsync(host_bufs[static_cast<std::size_t>(r.rank)], r.scratch, bytes,
-                           cudaMemcpyDeviceToHost, s), "D2H");
+  const auto ps = pieces_of(bytes, opt_.host_piece);
+  const auto t0 = std::chrono::steady_clock::now();
+  LocalRank& R = local_[static_cast<std::size_t>(root_li)];
+  // Ranks sharing a GPU run in one launch on the first local rank's stream.
+  auto compute_of = [this](int dev) { return local_[static_cast<std::size_t>(by_device_.at(dev).front())].stream; };
+  auto owner_of = [this](int dev) -> LocalRank& { return local_[static_cast<std::size_t>(by_device_.at(dev).front())]; };
+  std::map<int, std::size_t> ev;  // per device event cursor
+  for (const auto& kv : by_device_) ev[kv.first] = 0;
+  for (const Piece& p : ps) {
+    if (p.len) {
+      DeviceScope ds(R.device);
+      ck(cudaMemcpyAsync(R.scratch + p.off, static_cast<std::uint8_t*>(host_bufs[static_cast<std::size_t>(root)]) + p.off,
+                         p.len, cudaMemcpyHostToDevice, R.copy_in), "H2D");
+      const cudaEvent_t in = event(owner_of(R.device), ev[R.device]++);
+      ck(cudaEventRecord(in, R.copy_in), "cudaEventRecord");
+      ck(cudaStreamWaitEvent(compute_of(R.device), in, 0), "cudaStreamWaitEvent");
+    }
+    std::vector<void*> dbufs;
+    for (LocalRank& r : local_) dbufs.push_back(r.scratch + p.off);
+    bcast_all(dbufs, p.len, root, cfg, {});
+    if (!p.len) continue;
+    for (const auto& kv : by_device_) {
+      DeviceScope ds(kv.first);
+      LocalRank& owner = owner_of(kv.first);
+      const cudaEvent_t done = event(owner, ev[kv.first]++);
+      ck(cudaEventRecord(done, compute_of(kv.first)), "cudaEventRecord");
+      ck(cudaStreamWaitEvent(owner.copy_out, done, 0), "cudaStreamWaitEvent");
+      for (int li : kv.second) {
+        LocalRank& r = local_[static_cast<std::size_t>(li)];
+        if (r.rank == root) continue;
+        ck(cudaMemcpyAsync(static_cast<std::uint8_t*>(host_bufs[static_cast<std::size_t>(r.rank)]) + p.off,
+                           r.scratch + p.off, p.len, cudaMemcpyDeviceToHost, owner.copy_out), "D2H");
       }
     }
   }
   std::vector<int> all;
   for (const auto& kv : by_device_) {
     DeviceScope ds(kv.first);
-    ck(cudaStreamSynchronize(local_[static_cast<std::size_t>(kv.second.front())].stream), "synchronize");
+    LocalRank& owner = owner_of(kv.first);
+    ck(cudaStreamSynchronize(owner.copy_out), "synchronize");
+    ck(cudaStreamSynchronize(owner.stream), "synchronize");
+    ck(cudaStreamSynchronize(owner.copy_in), "synchronize");
     all.insert(all.end(), kv.second.begin(), kv.second.end());
   }
   const auto t1 = std::chrono::steady_clock::now();

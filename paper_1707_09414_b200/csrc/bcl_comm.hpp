@@ -79,6 +79,7 @@ struct GroupOptions {
   bool strict_sys = false;                                  // system-scope fence before every flag
   bool ll = true;                                           // LL push protocol for small `direct` calls
   std::uint64_t ll_max_bytes = 0;                           // LL threshold (0 = 2 MiB, lowered for many ranks)
+  std::uint64_t host_piece = 4ull << 20;                    // host-buffer calls: H2D/bcast/D2H pipeline piece
   std::int64_t stage_bytes = -1;                            // bulk-copy stage per warp: 0 = vector loads,
                                                             // -1 = auto (8 KiB across GPUs, 0 on one GPU)
   std::uint32_t stages = 2;                                 // bulk-copy stages per copy warp
@@ -115,6 +116,9 @@ struct LocalRank {
   std::uint8_t* scratch{};      // device staging for host-buffer calls
   std::size_t scratch_bytes{};
   cudaStream_t stream{};        // internal stream for run_bcast
+  cudaStream_t copy_in{};       // host-buffer calls: H2D stream
+  cudaStream_t copy_out{};      // host-buffer calls: D2H stream
+  std::vector<cudaEvent_t> events;
   unsigned long long* prov{};   // optional provenance counters
   unsigned long long* trace{};  // optional per-lane event timestamps
   std::uint32_t trace_cap{0};
@@ -178,6 +182,8 @@ class Group {
   void fill_rank_work(dev::RankWork& w, LocalRank& r, const CallPlan& p, void* buf);
   void launch_group(const std::vector<int>& locals, const std::vector<void*>& bufs,
                     std::uint64_t bytes, int root, const CallPlan& p, cudaStream_t stream);
+  cudaEvent_t event(LocalRank& r, std::size_t i);
+  void ensure_scratch(int local_index, std::uint64_t bytes);
   void launch_ll(const std::vector<int>& locals, const std::vector<void*>& bufs, std::uint64_t bytes, int root,
                  cudaStream_t stream);
   void raise_errors(const std::vector<int>& locals);

@@ -212,6 +212,18 @@ def test_dtype_count_and_nan_payloads_are_bit_exact():
         assert torch.equal(bufs[r].view(torch.int32), bits)
 
 
+def test_host_buffer_run_bcast_pieces():
+    """Host-buffer run_bcast pipelines 4 MiB pieces: > 2 pieces, ragged end."""
+    n, m = 3, (9 << 20) + 13
+    comms = B.Comm.local([0] * n, timeout_s=10)
+    payload = O.payload(5, m)
+    hosts = [bytearray(m) for _ in range(n)]
+    hosts[2][:] = payload
+    B.run_bcast_host(comms, 2, hosts, m, None)
+    for r in range(n):
+        assert bytes(hosts[r]) == payload
+
+
 def test_host_buffer_run_bcast():
     n, m = 4, 777777
     comms = B.Comm.local([0] * n, timeout_s=10)

@@ -109,6 +109,16 @@ def _ipc_worker(rank, world, port, q):
             comm.bcast(buf, m, "uint8", root, cfg_of(algo, 524288, 2))
             comm.check()
             ok &= buf[:m].cpu().numpy().tobytes() == payload
+        # host-buffer entry point (pipelined H2D / broadcast / D2H pieces)
+        m = (9 << 20) + 3
+        payload = O.payload(99, m)
+        host = torch.zeros(m, dtype=torch.uint8).pin_memory()
+        if rank == 1 % world:
+            host.copy_(torch.frombuffer(bytearray(payload), dtype=torch.uint8))
+        dist.barrier()
+        comm.bcast_host(host, m, "uint8", 1 % world, cfg_of("chain_pipelined", 262144))
+        comm.check()
+        ok &= host.numpy().tobytes() == payload
         q.put((rank, ok, None))
         comm.close()
     except Exception as e:  # noqa: BLE001
