@@ -165,6 +165,9 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--sweep-max", type=int, default=1 << 30)
     ap.add_argument("--cpu-iters", type=int, default=12)
+    ap.add_argument("--workload", default="config1", choices=["config1", "vgg16", "alexnet", "resnet50", "lenet"],
+                    help="config1 (default) or a layer-wise parameter broadcast (BASELINE configs 4/5)")
+    ap.add_argument("--bucket", type=int, default=0, help="parameter workloads: coalesce tensors into >= this")
     ap.add_argument("--fixed-chunk", dest="tuned", action="store_false",
                     help="N>1: pipelined chain with --chunk instead of the tuned selection")
     args = ap.parse_args()
@@ -176,7 +179,11 @@ def main():
         run_reference_arm(args, rank, world)
         return
     import torch
-    if world == 1:
+    if args.workload != "config1":
+        if world == 1:
+            raise SystemExit("parameter workloads need >= 2 GPUs (torchrun)")
+        bench_params(args, torch, rank, world)
+    elif world == 1:
         bench_single(args, torch)
     else:
         bench_multi(args, torch, rank, world)
@@ -419,6 +426,79 @@ def bench_multi(args, torch, rank, world):
             "clocks": clk.summary(),
             "sweep": sweep,
         }
+        print(json.dumps(line), flush=True)
+    dist.barrier(device_ids=[local])
+    comm.close()
+    dist.destroy_process_group()
+
+
+def bench_params(args, torch, rank, world):
+    """BASELINE configs 4/5: broadcast every parameter tensor of a CNN from a
+    root (layer-wise, algorithm and chunk tuned per tensor size), per
+    iteration, next to NCCL broadcasting the same tensors."""
+    import torch.distributed as dist
+    import paper_1707_09414_b200 as B
+    from paper_1707_09414_b200.comm import DevicePtr
+    from paper_1707_09414_b200.params import ParamBroadcaster
+    from paper_1707_09414_b200.workloads import MODELS
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    pb = ParamBroadcaster(MODELS[args.workload], bucket_bytes=args.bucket)
+    comm = B.Comm.connect_torch(world, rank, local, heap_bytes=pb.total_bytes + (16 << 20), timeout_s=30)
+    flat = torch.as_tensor(DevicePtr(comm.alloc(pb.total_bytes), pb.total_bytes), device=dev)
+    g = torch.Generator(device=dev).manual_seed(2)
+    ref = torch.randint(0, 256, (pb.total_bytes,), dtype=torch.uint8, device=dev, generator=g)
+    views = [flat[o:o + n] for o, n in pb.msgs]
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.synchronize()
+    roots = [0] if args.workload == "vgg16" else [world - 1, world // 2]
+    results = {}
+    for root in roots:
+        for impl in ("ours", "nccl"):
+            def prepare(it):
+                with torch.cuda.stream(stream):
+                    if rank == root:
+                        flat.copy_(ref)
+                    else:
+                        flat.zero_()
+                if it == 0:
+                    stream.synchronize()
+                    dist.barrier(device_ids=[local])
+
+            def body(it):
+                if impl == "ours":
+                    pb.bcast(comm, flat, root, stream)
+                else:
+                    with torch.cuda.stream(stream):
+                        for v in views:
+                            dist.broadcast(v, src=root)
+
+            def verify(it):
+                return all(torch.equal(flat[o:o + n], ref[o:o + n]) for o, n in zip(pb.offsets, pb.sizes))
+
+            times = time_steps(torch, args.steps, args.warmup, prepare, body, verify, stream,
+                               align=lambda: comm.barrier(stream))
+            t = torch.tensor(times, dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            results[(root, impl)] = statistics.mean(t.cpu().tolist())
+    if rank == 0:
+        ours = statistics.mean(results[(r, "ours")] for r in roots)
+        nccl = statistics.mean(results[(r, "nccl")] for r in roots)
+        line = {"metric": f"{args.workload} layer-wise parameter broadcast time per iteration",
+                "value": round(ours * 1e3, 4), "unit": "ms", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ours * 1e3, 4), "higher_is_better": False,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32 (moved as bytes)",
+                "data": "synthetic parameters (random bytes), torchvision layer shapes",
+                "config": {"workload": f"{args.workload}: {len(pb.sizes)} tensors, {sum(pb.sizes)} bytes, "
+                                       f"{len(pb.msgs)} broadcasts per iteration (bucket {args.bucket} B), roots {roots}",
+                           "tensors": len(pb.sizes), "bytes": sum(pb.sizes), "messages": len(pb.msgs)},
+                "per_root_ms": {str(r): {"ours": round(results[(r, 'ours')] * 1e3, 4),
+                                         "nccl": round(results[(r, 'nccl')] * 1e3, 4)} for r in roots},
+                "nccl_ms": round(nccl * 1e3, 4),
+                "link_bound_ms": round(sum(pb.sizes) / LINK_BW * 1e3, 4),
+                "gpu_launches": len(pb.msgs) * args.steps}
         print(json.dumps(line), flush=True)
     dist.barrier(device_ids=[local])
     comm.close()

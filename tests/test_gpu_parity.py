@@ -275,3 +275,23 @@ def test_ll_small_direct_back_to_back_reuse():
             assert views[r].cpu().numpy().tobytes() == payload, (it, m, root, r)
     for c in comms:
         c.check()
+
+
+@pytest.mark.parametrize("model,bucket", [("lenet", 0), ("alexnet", 0), ("alexnet", 1 << 20), ("resnet50", 4 << 20)])
+def test_layerwise_parameter_broadcast(model, bucket):
+    """BASELINE configs 4/5 shape: every parameter tensor broadcast from a
+    non-zero root with the tuned algorithm per tensor size."""
+    from paper_1707_09414_b200.params import ParamBroadcaster
+    from paper_1707_09414_b200.workloads import MODELS
+    n, root = 4, 3
+    pb = ParamBroadcaster(MODELS[model], bucket_bytes=bucket)
+    comms = comms_for(n)
+    g = torch.Generator(device="cuda:0").manual_seed(len(pb))
+    flats = [torch.zeros(pb.total_bytes, dtype=torch.uint8, device="cuda:0") for _ in range(n)]
+    flats[root].copy_(torch.randint(0, 256, (pb.total_bytes,), dtype=torch.uint8, device="cuda:0", generator=g))
+    torch.cuda.synchronize()
+    pb.bcast_all(comms, flats, root)
+    torch.cuda.synchronize()
+    for r in range(n):
+        for off, size in zip(pb.offsets, pb.sizes):
+            assert torch.equal(flats[r][off:off + size], flats[root][off:off + size]), (model, r, off)
