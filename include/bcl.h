@@ -172,6 +172,10 @@ bcl_status_t bcl_comm_info(bcl_comm_t c, int* n, int* rank, int* device, int* la
 /* Tuning table consulted when a call passes config == NULL; the builtin
  * measured B200 table is used until one is set. The table is copied. */
 bcl_status_t bcl_comm_set_table(bcl_comm_t c, bcl_table_t t);
+/* Pipelined-chain transport protocol: 0 auto (the table's measured
+ * "# bcl-push-from" rule), 1 pull (consumers load from the upstream buffer),
+ * 2 push (producers store into the downstream buffer). */
+bcl_status_t bcl_comm_set_protocol(bcl_comm_t c, int protocol);
 /* The config a NULL-config call would run for this size (select + clamp). */
 bcl_status_t bcl_comm_choose(bcl_comm_t c, uint64_t message_bytes, bcl_config_t* out);
 bcl_status_t bcl_mem_alloc(bcl_comm_t c, size_t bytes, void** ptr);

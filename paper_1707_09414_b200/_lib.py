@@ -98,6 +98,7 @@ _SIGS = {
                                 C.POINTER(C.c_int)]),
     "bcl_comm_set_table": (C.c_int, [C.c_void_p, C.c_void_p]),
     "bcl_comm_choose": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(_Config)]),
+    "bcl_comm_set_protocol": (C.c_int, [C.c_void_p, C.c_int]),
     "bcl_mem_alloc": (C.c_int, [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
     "bcl_mem_reset": (C.c_int, [C.c_void_p]),
     "bcl_bcast": (C.c_int, [C.c_void_p, C.c_size_t, C.c_int, C.c_int, C.c_void_p, C.POINTER(_Config), C.c_void_p]),

@@ -120,6 +120,11 @@ class Comm:
     def set_table(self, table) -> None:
         _check(lib().bcl_comm_set_table(self._h, table._h))
 
+    def set_protocol(self, protocol) -> None:
+        """Chain transport: "auto" (table rule), "pull" or "push"."""
+        code = {"auto": 0, "pull": 1, "push": 2}[protocol] if isinstance(protocol, str) else int(protocol)
+        _check(lib().bcl_comm_set_protocol(self._h, code))
+
     def choose(self, message_bytes: int) -> AlgorithmConfig:
         out = _Config()
         _check(lib().bcl_comm_choose(self._h, message_bytes, C.byref(out)))

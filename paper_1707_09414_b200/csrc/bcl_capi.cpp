@@ -405,6 +405,13 @@ bcl_status_t bcl_comm_set_table(bcl_comm_t c, bcl_table_t t) {
   });
 }
 
+bcl_status_t bcl_comm_set_protocol(bcl_comm_t c, int protocol) {
+  return guard([&] {
+    need(c, "comm");
+    c->g->set_protocol(protocol);
+  });
+}
+
 bcl_status_t bcl_comm_choose(bcl_comm_t c, uint64_t m, bcl_config_t* out) {
   return guard([&] {
     need(c, "comm");

@@ -73,6 +73,7 @@ GroupOptions GroupOptions::from_env() {
   if (const char* v = std::getenv("BCL_MAX_CTAS")) o.max_ctas_per_rank = std::atoi(v);
   if (const char* v = std::getenv("BCL_STRICT_SYS")) o.strict_sys = std::atoi(v) != 0;
   if (const char* v = std::getenv("BCL_LL")) o.ll = std::atoi(v) != 0;
+  if (const char* v = std::getenv("BCL_PROTOCOL")) o.protocol = std::atoi(v);
   if (const char* v = std::getenv("BCL_LL_MAX")) o.ll_max_bytes = std::strtoull(v, nullptr, 10);
   if (const char* v = std::getenv("BCL_HOST_PIECE")) o.host_piece = std::max<std::uint64_t>(4096, std::strtoull(v, nullptr, 10));
   if (const char* v = std::getenv("BCL_STAGES")) o.stages = static_cast<std::uint32_t>(std::clamp(std::atoi(v), 2, dev::kMaxStages));
@@ -355,6 +356,20 @@ void Group::set_table(const TuningTable& t) {
   have_table_ = true;
 }
 void Group::clear_table() { have_table_ = false; }
+
+void Group::set_protocol(int protocol) {
+  if (protocol < 0 || protocol > 2) throw std::invalid_argument("protocol must be 0 (auto), 1 (pull) or 2 (push)");
+  opt_.protocol = protocol;
+}
+
+// Push needs middle ranks to pay off (measured, see tools/tune_b200.py); the
+// table records from which size on it wins.
+bool Group::use_push(const CallPlan& p, std::uint64_t bytes) const {
+  if (!p.implicit_chain || n_ < 2) return false;
+  if (opt_.protocol == 1) return false;
+  if (opt_.protocol == 2) return true;
+  return select_push(table(), n_, bytes);
+}
 const TuningTable& Group::table() const { return have_table_ ? table_ : builtin_table(); }
 
 // `bcast --algo auto` semantics: select per size, clamp the chunk to the
@@ -552,6 +567,7 @@ void Group::launch_group(const std::vector<int>& locals, const std::vector<void*
   P.strict_sys = (opt_.strict_sys && !single_device_) ? 1 : 0;
   P.stage_bytes = static_cast<std::uint32_t>(std::max<std::int64_t>(opt_.stage_bytes, 0));
   P.stages = opt_.stages;
+  P.push = use_push(p, bytes) ? 1 : 0;
   std::uint64_t epoch = 0;
   for (std::size_t i = 0; i < locals.size(); ++i) {
     LocalRank& r = local_[static_cast<std::size_t>(locals[i])];

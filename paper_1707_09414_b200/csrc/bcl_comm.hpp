@@ -78,6 +78,7 @@ struct GroupOptions {
   std::uint32_t poll_ns = 64;                               // back-off between flag polls (ns)
   bool strict_sys = false;                                  // system-scope fence before every flag
   bool ll = true;                                           // LL push protocol for small `direct` calls
+  int protocol = 0;                                         // chain: 0 auto (table), 1 pull, 2 push
   std::uint64_t ll_max_bytes = 0;                           // LL threshold (0 = 2 MiB, lowered for many ranks)
   std::uint64_t host_piece = 4ull << 20;                    // host-buffer calls: H2D/bcast/D2H pipeline piece
   std::int64_t stage_bytes = -1;                            // bulk-copy stage per warp: 0 = vector loads,
@@ -149,6 +150,7 @@ class Group {
   int local_index_of(int rank) const;
 
   void set_table(const TuningTable& t);
+  void set_protocol(int protocol);  // 0 auto (table's push-from rule), 1 pull, 2 push
   void clear_table();
   const TuningTable& table() const;
   AlgorithmConfig choose(std::uint64_t bytes, const AlgorithmConfig* cfg) const;
@@ -182,6 +184,7 @@ class Group {
   void fill_rank_work(dev::RankWork& w, LocalRank& r, const CallPlan& p, void* buf);
   void launch_group(const std::vector<int>& locals, const std::vector<void*>& bufs,
                     std::uint64_t bytes, int root, const CallPlan& p, cudaStream_t stream);
+  bool use_push(const CallPlan& p, std::uint64_t bytes) const;
   cudaEvent_t event(LocalRank& r, std::size_t i);
   void ensure_scratch(int local_index, std::uint64_t bytes);
   void launch_ll(const std::vector<int>& locals, const std::vector<void*>& bufs, std::uint64_t bytes, int root,

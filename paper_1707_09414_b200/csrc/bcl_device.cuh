@@ -113,6 +113,7 @@ struct LaunchParamsT {
   std::uint32_t strict_sys;   // 1: system-scope fence before every flag (see run_publisher)
   std::uint32_t stage_bytes;  // bytes per bulk-copy stage; 0 = vector loads only
   std::uint32_t stages;       // bulk-copy stages per copy warp (2..kMaxStages)
+  std::uint32_t push;         // chain: producers store into the consumer's buffer
   RankWork ranks[NL];
 };
 using LaunchParams = LaunchParamsT<kMaxLocal>;

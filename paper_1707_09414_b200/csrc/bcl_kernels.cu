@@ -234,7 +234,7 @@ __device__ void run_publisher(const LaunchParamsT<1>& P, CtaShared* sh) {
     // peers read through this GPU's L2 (its point of coherence): once the
     // stores are performed at gpu scope they are visible to NVLink readers.
     // strict_sys keeps the textbook system-scope release instead.
-    if (P.strict_sys) {
+    if (P.strict_sys || P.push) {  // push mode: the published data is in the peer's memory
       fence_acq_rel_sys();
     } else {
       fence_acq_rel_gpu();
@@ -352,8 +352,8 @@ __device__ __forceinline__ void bulk_wait_read_n(int n) {
 // never waits for this rank's upstream. Requires 16-byte aligned slices; the
 // ragged end of the message goes byte-wise.
 __device__ bool chain_pull_bulk(Ctx& c, int pipe, int q, int ns, std::uint32_t mine, const std::uint64_t* ready,
-                                const std::uint8_t* src, int prev, bool has_next, std::uint64_t* next_flag,
-                                std::uint64_t tag) {
+                                const std::uint8_t* src, std::uint8_t* dst, int prev, bool has_next,
+                                std::uint64_t* next_flag, std::uint64_t tag) {
   const LaunchParamsT<1>& P = *c.P;
   const RankWork& W = *c.W;
   std::uint64_t* bars = c.sh->full[c.warp];
@@ -400,7 +400,11 @@ __device__ bool chain_pull_bulk(Ctx& c, int pipe, int q, int ns, std::uint32_t m
     c.tail += 1;
     st_release_cta(&c.sh->tail[c.warp], c.tail);
   };
+  auto ready_now = [&](std::uint32_t j) {  // chunk j available (a null `ready` means always)
+    return ready == nullptr || ld_relaxed_sys(ready) >= (tag | (j + 1));
+  };
   auto block_for = [&](std::uint32_t j) -> bool {  // wait until the lane's chunk j is ready upstream
+    if (ready == nullptr) return true;
     const std::uint64_t want = tag | (j + 1);
     std::uint64_t v = ld_relaxed_sys(ready);
     if (v < want) {
@@ -424,8 +428,8 @@ __device__ bool chain_pull_bulk(Ctx& c, int pipe, int q, int ns, std::uint32_t m
     issue();  // chunk 0 was acquired by the caller
     while (landed < mine) {
       // Prefetch every chunk the upstream has already published, up to S in flight.
-      while (issued < mine && issued - landed < S && ld_relaxed_sys(ready) >= (tag | (issued + 1))) {
-        (void)ld_acquire_sys(ready);
+      while (issued < mine && issued - landed < S && ready_now(issued)) {
+        if (ready != nullptr) (void)ld_acquire_sys(ready);
         issue();
       }
       if (issued == landed) {  // nothing in flight: publish what we hold, then block
@@ -445,11 +449,11 @@ __device__ bool chain_pull_bulk(Ctx& c, int pipe, int q, int ns, std::uint32_t m
       std::uint64_t g;
       std::uint32_t body, len;
       geom(landed, &g, &body, &len);
-      if (body) bulk_s2g(W.buf + g, c.stage + static_cast<std::size_t>(st) * sb, body);
+      if (body) bulk_s2g(dst + g, c.stage + static_cast<std::size_t>(st) * sb, body);
       bulk_commit();
       stamp(landed, 2);
-      for (std::uint32_t i = body; i < len; ++i) W.buf[g + i] = ld_u8(src + g + i);  // ragged end
-      if (W.prov != nullptr && len) {
+      for (std::uint32_t i = body; i < len; ++i) dst[g + i] = ld_u8(src + g + i);  // ragged end
+      if (W.prov != nullptr && len && dst == W.buf) {
         atomicAdd(&W.prov[static_cast<std::uint64_t>(prev) * P.n_chunks + pipe + landed * ns],
                   static_cast<unsigned long long>(len));
       }
@@ -468,6 +472,66 @@ __device__ bool chain_pull_bulk(Ctx& c, int pipe, int q, int ns, std::uint32_t m
   ok = __shfl_sync(0xffffffffu, ok, 0);
   __syncwarp();
   return ok != 0;
+}
+
+
+// Push-mode chain: logical rank l writes its chunks straight into l+1's
+// buffer (NVLink stores instead of loads). Each consumer lane first tells its
+// producer where to write and that its buffer is free (mailbox + "ready" in
+// the producer's ack slot); a producer lane forwards chunk k once it has
+// landed locally (or immediately at the head) and publishes it with a
+// system-scope release (the data now lives in the peer's memory).
+__device__ void run_chain_push(Ctx& c, int pipe, int q, int ns) {
+  const LaunchParamsT<1>& P = *c.P;
+  const RankWork& W = *c.W;
+  const int n = P.n_ranks;
+  const int L = P.lanes;
+  const int me = W.rank;
+  const int logical = (me - P.root + n) % n;
+  const int prev = (me + n - 1) % n;
+  const int next = (me + 1) % n;
+  const bool has_prev = logical > 0;
+  const bool has_next = logical + 1 < n;
+  const std::uint32_t K = P.n_chunks;
+  if (static_cast<std::uint32_t>(pipe) >= K) return;
+  const std::uint32_t mine = (K - 1 - pipe) / ns + 1;
+  const std::uint64_t tag = P.epoch << 32;
+  const std::size_t slot = static_cast<std::size_t>(me) * L + c.ell;
+  const std::uint64_t* arrived = has_prev ? W.flags + static_cast<std::size_t>(prev) * L + c.ell : nullptr;
+  if (has_prev) {  // consumer: announce the destination, then "ready"
+    if (c.lane_id == 0) {
+      st_relaxed_sys(W.peers->mbox[prev] + slot, W.pub);
+      fence_acq_rel_sys();
+    }
+    publish(c, W.peers->acks[prev] + slot, P.epoch);
+  }
+  if (!has_next) {  // tail: wait until every chunk of this lane has landed
+    (void)wait_geq(c, arrived, tag | mine, prev, K);
+    return;
+  }
+  if (!wait_geq(c, W.acks + static_cast<std::size_t>(next) * L + c.ell, P.epoch, next, 0)) return;
+  auto* dst = reinterpret_cast<std::uint8_t*>(
+      W.peers->addr_base[next] + ld_relaxed_sys(W.mbox + static_cast<std::size_t>(next) * L + c.ell));
+  std::uint64_t* next_flag = W.peers->flags[next] + slot;
+  const bool aligned = c.stage != nullptr &&
+                       ((reinterpret_cast<std::uintptr_t>(dst) | reinterpret_cast<std::uintptr_t>(W.buf)) & 15u) == 0 &&
+                       (P.chunk_bytes & 15u) == 0 && (P.slice_bytes & 15u) == 0 && P.slice_bytes <= P.stage_bytes;
+  if (aligned) {
+    if (has_prev && !wait_geq(c, arrived, tag | 1, prev, pipe)) return;
+    (void)chain_pull_bulk(c, pipe, q, ns, mine, arrived, W.buf, dst, prev, true, next_flag, tag);
+    return;
+  }
+  for (std::uint32_t k = 0; k < mine; ++k) {
+    if (has_prev && !wait_geq(c, arrived, tag | (k + 1), prev, pipe + static_cast<std::uint64_t>(k) * ns)) return;
+    std::uint64_t off, len;
+    chunk_range(P, pipe + k * ns, &off, &len);
+    const std::uint64_t lo = static_cast<std::uint64_t>(q) * P.slice_bytes;
+    if (lo < len) {
+      const std::uint64_t hi = lo + P.slice_bytes < len ? lo + P.slice_bytes : len;
+      warp_copy(c, W.buf, dst, off + lo, off + hi);
+    }
+    publish(c, next_flag, tag | (k + 1));
+  }
 }
 
 // Implicit pipelined chain (schedule_chain_pipelined, schedules.cpp:161-187):
@@ -506,7 +570,8 @@ __device__ void run_chain(Ctx& c, int pipe, int q, int ns) {
                            (P.chunk_bytes & 15u) == 0 && (P.slice_bytes & 15u) == 0 &&
                            P.slice_bytes <= P.stage_bytes;
       if (aligned) {
-        if (!chain_pull_bulk(c, pipe, q, ns, mine, ready, src, prev, has_next, W.peers->flags[next] + slot, tag)) {
+        if (!chain_pull_bulk(c, pipe, q, ns, mine, ready, src, W.buf, prev, has_next, W.peers->flags[next] + slot,
+                             tag)) {
           return;
         }
         publish(c, W.peers->acks[prev] + slot, P.epoch);
@@ -628,7 +693,11 @@ __global__ void __launch_bounds__(kThreads, NL == 1 ? 1 : 3) bcast_kernel(const 
     const int pipe = c.ell / P.slices;
     const int q = c.ell % P.slices;
     if (c.W->n_events < 0) {
-      run_chain(c, pipe, q, ns);
+      if (P.push) {
+        run_chain_push(c, pipe, q, ns);
+      } else {
+        run_chain(c, pipe, q, ns);
+      }
     } else {
       run_events(c, pipe, q, ns);
     }

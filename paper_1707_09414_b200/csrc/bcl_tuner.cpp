@@ -2,6 +2,7 @@
 #include "bcl_tuner.hpp"
 
 #include <algorithm>
+#include <cstdio>
 #include <charconv>
 #include <cmath>
 #include <fstream>
@@ -20,6 +21,7 @@ constexpr std::string_view kColumns =
     "n,msg_min_bytes,msg_max_bytes,algorithm,radix,chunk_bytes,predicted_cost_s";
 constexpr std::string_view kPragma = "# oracle:";
 constexpr std::string_view kMeasuredPragma = "# bcl-oracle: measured";
+constexpr std::string_view kPushPragma = "# bcl-push-from:";
 
 // Rounded geometric mean of two sizes (tuner.cpp:27-31).
 std::uint64_t geo_mid(std::uint64_t a, std::uint64_t b) {
@@ -214,6 +216,18 @@ AlgorithmConfig select(const TuningTable& t, int n, std::uint64_t m) {
   return hit->config;
 }
 
+bool select_push(const TuningTable& t, int n, std::uint64_t m) {
+  int best_n = -1;
+  std::uint64_t from = 0;
+  for (const auto& [pn, bytes] : t.push_from) {
+    if (pn <= n && pn > best_n) {
+      best_n = pn;
+      from = bytes;
+    }
+  }
+  return best_n >= 0 && m >= from;
+}
+
 TableParseError::TableParseError(std::size_t line, const std::string& what)
     : std::runtime_error("line " + std::to_string(line) + ": " + what), line_(line) {}
 
@@ -225,7 +239,12 @@ std::string save_table_text(const TuningTable& t) {
   } else {
     s.append(kPragma).append(" ").append(oracle_name(t.oracle));
   }
-  s.append("\n").append(kColumns).append("\n");
+  s.append("\n");
+  for (const auto& [pn, bytes] : t.push_from) {
+    s.append(kPushPragma).append(" n=").append(std::to_string(pn)).append(" bytes=").append(std::to_string(bytes));
+    s.append("\n");
+  }
+  s.append(kColumns).append("\n");
   char num[64];
   for (const TuningEntry& e : t.entries) {
     const Algorithm a = e.config.algorithm;
@@ -291,6 +310,15 @@ TuningTable load_table(std::istream& in) {
       if (name == "analytical") t.oracle = CostOracle::Analytical;
       else if (name == "simulated") t.oracle = CostOracle::Simulated;
       else throw TableParseError(no, "unknown oracle '" + name + "'");
+      continue;
+    }
+    if (line.rfind(kPushPragma, 0) == 0) {
+      int pn = 0;
+      unsigned long long bytes = 0;
+      if (std::sscanf(line.c_str() + kPushPragma.size(), " n=%d bytes=%llu", &pn, &bytes) != 2 || pn < 1) {
+        throw TableParseError(no, "bad push pragma");
+      }
+      t.push_from.emplace_back(pn, static_cast<std::uint64_t>(bytes));
       continue;
     }
     if (line.rfind(kMeasuredPragma, 0) == 0) {

@@ -60,6 +60,11 @@ struct TuningTable {
   CostOracle oracle{CostOracle::Analytical};
   std::string provenance;  // free text after "# bcl-oracle: measured"
   std::vector<TuningEntry> entries;
+  // B200 transport protocol for chain_pipelined: from this many bytes on, at
+  // this rank count (nearest smaller tuned n), producers push instead of
+  // consumers pulling. Stored as "# bcl-push-from: n=<n> bytes=<b>" lines,
+  // which the reference load_table skips as comments.
+  std::vector<std::pair<int, std::uint64_t>> push_from;
   bool operator==(const TuningTable& o) const {
     return oracle == o.oracle && entries == o.entries;
   }
@@ -89,6 +94,8 @@ TuningTable tune(const std::vector<int>& n_list,
 
 AlgorithmConfig select(const TuningTable& table, int n,
                        std::uint64_t message_bytes);
+// Whether a chain_pipelined call of this size should use the push protocol.
+bool select_push(const TuningTable& table, int n, std::uint64_t message_bytes);
 
 class TableParseError : public std::runtime_error {
  public:

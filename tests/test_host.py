@@ -164,6 +164,12 @@ def test_measured_tables_load_in_the_reference():
                         provenance="unit test")
     text = t.text()
     assert text.startswith("# bcl-oracle: measured unit test\n")
+    # the push-protocol rule rides in a comment line the reference skips
+    lines = text.splitlines()
+    lines.insert(1, "# bcl-push-from: n=4 bytes=268435456")
+    text = "\n".join(lines) + "\n"
+    t = B.load_table_text(text)
+    assert t.text() == text
     again = B.load_table_text(text)
     assert again == t and again.oracle == "measured"
     if not os.path.exists(HARNESS):

@@ -5,15 +5,16 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1707_09414_b200 as B
 out, inputs = sys.argv[1], sys.argv[2:]
-rows, prov = [], []
+rows, prov, push = [], [], []
 for p in inputs:
     t = B.load_table(p)
     assert t.oracle == "measured", p
     text = open(p).read().splitlines()
     prov.append(text[0][len("# bcl-oracle: measured "):])
-    rows += [l for l in text[2:] if l.strip()]
+    push += [l for l in text[1:] if l.startswith("# bcl-push-from:")]
+    rows += [l for l in text[1:] if l.strip() and not l.startswith("#") and not l.startswith("n,")]
 rows.sort(key=lambda l: (int(l.split(",")[0]), int(l.split(",")[1])))
-header = "# bcl-oracle: measured " + " | ".join(prov)
+header = "# bcl-oracle: measured " + " | ".join(prov) + "".join("\n" + l for l in push)
 text = header + "\nn,msg_min_bytes,msg_max_bytes,algorithm,radix,chunk_bytes,predicted_cost_s\n" + "\n".join(rows) + "\n"
 B.load_table_text(text)  # validates ordering / disjoint ranges
 open(out, "w").write(text)

@@ -90,6 +90,37 @@ table = B.tune_measured([world], sizes, cands, chunks, cost,
                                    f"device-timed runs (max over ranks, 2 significant digits), "
                                    f"{time.strftime('%Y-%m-%d')}")
 comm.check(stream)
+
+# Transport protocol for the pipelined chain: measure pull vs push at every
+# swept size >= 16 MiB where the table picks the chain; push wins from the
+# smallest size after which it always wins ("# bcl-push-from" rule).
+push_from = None
+if world >= 3:
+    wins = []
+    for m in [x for x in sizes if x >= (16 << 20)]:
+        cfg = table.select(world, m)
+        if cfg.algorithm != B.Algorithm.chain_pipelined:
+            wins.append((m, False))
+            continue
+        comm.set_protocol("pull")
+        t_pull = cost(cfg, world, m)
+        comm.set_protocol("push")
+        t_push = cost(cfg, world, m)
+        comm.set_protocol("auto")
+        wins.append((m, t_push < t_pull))
+        if rank == 0:
+            print(f"protocol {m}: pull {t_pull * 1e6:.1f} us push {t_push * 1e6:.1f} us")
+    for i, (m, w) in enumerate(wins):
+        if w and all(x for _, x in wins[i:]):
+            push_from = m
+            break
+    comm.check(stream)
+text = table.text()
+if push_from is not None:
+    lines = text.splitlines()
+    lines.insert(1, f"# bcl-push-from: n={world} bytes={push_from}")
+    text = "\n".join(lines) + "\n"
+    table = B.load_table_text(text)
 if rank == 0:
     os.makedirs(os.path.dirname(os.path.abspath(a.out)), exist_ok=True)
     B.save_table(table, a.out)
