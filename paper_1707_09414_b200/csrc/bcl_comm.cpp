@@ -198,7 +198,7 @@ std::shared_ptr<Group> Group::create_local(const std::vector<int>& devices, cons
   if (g->opt_.stage_bytes < 0) g->opt_.stage_bytes = g->by_device_.size() > 1 ? 8192 : 0;
   // NVLink hops want a small window (fast fill); ranks sharing one GPU are
   // HBM-bound and want more bytes in flight.
-  if (g->opt_.window_bytes == 0) g->opt_.window_bytes = g->by_device_.size() > 1 ? (4ull << 20) : (16ull << 20);
+  if (g->opt_.window_bytes == 0) g->opt_.window_bytes = g->by_device_.size() > 1 ? (4ull << 20) : (32ull << 20);
   g->lanes_ = lanes_for(devices[0], rpd, opt.max_ctas_per_rank, g->opt_);
   for (const auto& kv : g->by_device_) {
     if (kv.first != devices[0]) lanes_for(kv.first, rpd, opt.max_ctas_per_rank, g->opt_);

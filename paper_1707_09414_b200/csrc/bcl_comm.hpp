@@ -72,7 +72,7 @@ class AggregateRankError : public std::runtime_error {
 struct GroupOptions {
   std::uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;  // device spin bound
   std::uint64_t window_bytes = 0;                           // bytes in flight per rank (chunks x slices);
-                                                            // 0 = auto (4 MiB across GPUs, 16 MiB on one GPU)
+                                                            // 0 = auto (4 MiB across GPUs, 32 MiB on one GPU)
   std::uint64_t min_slice = 2048;                           // smallest per-lane slice of a chunk
   int max_ctas_per_rank = 0;                                // 0 = SM count
   std::uint32_t poll_ns = 64;                               // back-off between flag polls (ns)

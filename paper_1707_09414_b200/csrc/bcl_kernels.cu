@@ -39,6 +39,16 @@ __device__ __forceinline__ std::uint64_t ld_acquire_sys(const std::uint64_t* p) 
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ std::uint64_t ld_relaxed_gpu(const std::uint64_t* p) {
+  std::uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ std::uint64_t ld_acquire_gpu(const std::uint64_t* p) {
+  std::uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_relaxed_sys(std::uint64_t* p, std::uint64_t v) {
   asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -169,12 +179,14 @@ __device__ void fail(const Ctx& c, int code, int peer, std::uint64_t chunk, std:
 __device__ bool wait_geq(const Ctx& c, const std::uint64_t* p, std::uint64_t target, int peer,
                          std::uint64_t chunk) {
   int ok = 1;
+  // Every rank on one GPU: gpu-scope polling/acquire is the complete ordering.
+  const bool sys = c.P->sys_scope != 0;
   if (c.lane_id == 0) {
-    std::uint64_t v = ld_relaxed_sys(p);
+    std::uint64_t v = sys ? ld_relaxed_sys(p) : ld_relaxed_gpu(p);
     if (v < target) {
       const std::uint64_t t0 = globaltimer();
       unsigned spins = 0;
-      while ((v = ld_relaxed_sys(p)) < target) {
+      while ((v = sys ? ld_relaxed_sys(p) : ld_relaxed_gpu(p)) < target) {
         if (c.P->poll_ns) __nanosleep(c.P->poll_ns);
         if ((++spins & 255u) == 0) {
           if (*(volatile int*)c.W->abort != 0) {
@@ -191,7 +203,7 @@ __device__ bool wait_geq(const Ctx& c, const std::uint64_t* p, std::uint64_t tar
     }
   }
   ok = __shfl_sync(0xffffffffu, ok, 0);
-  if (ok) (void)ld_acquire_sys(p);
+  if (ok) (void)(sys ? ld_acquire_sys(p) : ld_acquire_gpu(p));
   __syncwarp();
   return ok != 0;
 }
