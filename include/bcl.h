@@ -172,6 +172,11 @@ bcl_status_t bcl_comm_info(bcl_comm_t c, int* n, int* rank, int* device, int* la
 /* Tuning table consulted when a call passes config == NULL; the builtin
  * measured B200 table is used until one is set. The table is copied. */
 bcl_status_t bcl_comm_set_table(bcl_comm_t c, bcl_table_t t);
+/* The device lane plan of a call (identical on every rank): Q slices per
+ * chunk, slice bytes, chunk count, CTAs per rank. Lane l serves slice l % Q of
+ * chunks c with c % (lanes / Q) == l / Q. */
+bcl_status_t bcl_comm_plan(bcl_comm_t c, const bcl_config_t* config, int root, uint64_t bytes, int* slices,
+                           uint64_t* slice_bytes, uint32_t* n_chunks, int* ctas);
 /* Pipelined-chain transport protocol: 0 auto (the table's measured
  * "# bcl-push-from" rule), 1 pull (consumers load from the upstream buffer),
  * 2 push (producers store into the downstream buffer). */

@@ -21,12 +21,16 @@
 //   bench ALGO N ROOT M CHUNK RADIX WARMUP ITERS T SEED
 //                                           -> JSON with min/median/avg/max us
 //   models N M CHUNK                         -> Eq.3/4/5 costs at desk params
+//   simulate ALGO N ROOT M CHUNK RADIX TS BW OUT.csv
+//                                           -> reference simulator trace CSV
+//                                              (simengine.hpp:61-70) + completions
 #include <algorithm>
 #include <barrier>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <random>
 #include <sstream>
 #include <string>
@@ -35,6 +39,7 @@
 #include "bcastlab/models.hpp"
 #include "bcastlab/runtime.hpp"
 #include "bcastlab/schedules.hpp"
+#include "bcastlab/simengine.hpp"
 #include "bcastlab/tuner.hpp"
 
 using namespace bcastlab;
@@ -246,6 +251,19 @@ int cmd_models(char** a) {
   return 0;
 }
 
+int cmd_simulate(char** a) {
+  const AlgorithmConfig cfg = parse_config(a[0], a[4], a[5]);
+  const NetworkParams p{std::strtod(a[6], nullptr), std::strtod(a[7], nullptr), 1e10};
+  const Schedule s = make_schedule(cfg, std::atoi(a[1]), std::atoi(a[2]), std::strtoull(a[3], nullptr, 10));
+  SimOptions opt;
+  opt.record_trace = true;
+  const SimResult r = simulate(s, p, opt);
+  std::ofstream out(a[8]);
+  write_trace_csv(r, out);
+  for (std::size_t i = 0; i < r.completion_s.size(); ++i) std::printf("rank %zu %.9g\n", i, r.completion_s[i]);
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -261,6 +279,7 @@ int main(int argc, char** argv) {
     if (cmd == "select" && argc >= 5) return cmd_select(argv + 2, argc - 2);
     if (cmd == "bench" && argc >= 12) return cmd_bench(argv + 2);
     if (cmd == "models" && argc >= 5) return cmd_models(argv + 2);
+    if (cmd == "simulate" && argc >= 11) return cmd_simulate(argv + 2);
   } catch (const std::exception& e) {
     std::printf("error %s\n", e.what());
     return 1;

@@ -120,6 +120,13 @@ class Comm:
     def set_table(self, table) -> None:
         _check(lib().bcl_comm_set_table(self._h, table._h))
 
+    def plan(self, config: AlgorithmConfig, root: int, nbytes: int) -> dict:
+        """Device lane plan of a call: slices per chunk, slice bytes, chunks, CTAs."""
+        q, sb, nc, ctas = C.c_int(), C.c_uint64(), C.c_uint32(), C.c_int()
+        _check(lib().bcl_comm_plan(self._h, C.byref(config._c()), root, nbytes, C.byref(q), C.byref(sb),
+                                   C.byref(nc), C.byref(ctas)))
+        return {"slices": q.value, "slice_bytes": sb.value, "n_chunks": nc.value, "ctas": ctas.value}
+
     def set_protocol(self, protocol) -> None:
         """Chain transport: "auto" (table rule), "pull" or "push"."""
         code = {"auto": 0, "pull": 1, "push": 2}[protocol] if isinstance(protocol, str) else int(protocol)

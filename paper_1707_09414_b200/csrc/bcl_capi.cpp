@@ -405,6 +405,19 @@ bcl_status_t bcl_comm_set_table(bcl_comm_t c, bcl_table_t t) {
   });
 }
 
+bcl_status_t bcl_comm_plan(bcl_comm_t c, const bcl_config_t* config, int root, uint64_t bytes, int* slices,
+                           uint64_t* slice_bytes, uint32_t* n_chunks, int* ctas) {
+  return guard([&] {
+    need(c, "comm");
+    need(config, "config");
+    const bcl::CallPlan p = c->g->plan(to_cfg(config), root, bytes);
+    if (slices) *slices = p.slices;
+    if (slice_bytes) *slice_bytes = p.slice_bytes;
+    if (n_chunks) *n_chunks = p.n_chunks;
+    if (ctas) *ctas = p.ctas;
+  });
+}
+
 bcl_status_t bcl_comm_set_protocol(bcl_comm_t c, int protocol) {
   return guard([&] {
     need(c, "comm");

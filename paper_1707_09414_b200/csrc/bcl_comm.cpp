@@ -72,6 +72,8 @@ GroupOptions GroupOptions::from_env() {
   if (const char* v = std::getenv("BCL_MIN_SLICE")) o.min_slice = std::max<std::uint64_t>(16, std::strtoull(v, nullptr, 10));
   if (const char* v = std::getenv("BCL_MAX_CTAS")) o.max_ctas_per_rank = std::atoi(v);
   if (const char* v = std::getenv("BCL_STRICT_SYS")) o.strict_sys = std::atoi(v) != 0;
+  if (const char* v = std::getenv("BCL_EAGER_POST")) o.eager_post = std::atoi(v) != 0;
+  if (const char* v = std::getenv("BCL_WRITER_FENCE")) o.writer_fence = std::atoi(v) != 0;
   if (const char* v = std::getenv("BCL_LL")) o.ll = std::atoi(v) != 0;
   if (const char* v = std::getenv("BCL_PROTOCOL")) o.protocol = std::atoi(v);
   if (const char* v = std::getenv("BCL_LL_MAX")) o.ll_max_bytes = std::strtoull(v, nullptr, 10);
@@ -568,6 +570,11 @@ void Group::launch_group(const std::vector<int>& locals, const std::vector<void*
   P.stage_bytes = static_cast<std::uint32_t>(std::max<std::int64_t>(opt_.stage_bytes, 0));
   P.stages = opt_.stages;
   P.push = use_push(p, bytes) ? 1 : 0;
+  P.eager_post = opt_.eager_post ? 1 : 0;
+  // Push publishes data that lives in the peer's memory: its sys-scope fence
+  // must wait for the remote stores anyway, so the publisher keeps it (a
+  // writer-side sys fence halves push bandwidth: 3.39 vs 1.73 ms, 1 GiB n=4).
+  P.writer_fence = (opt_.writer_fence && !P.strict_sys && !P.push) ? 1 : 0;
   std::uint64_t epoch = 0;
   for (std::size_t i = 0; i < locals.size(); ++i) {
     LocalRank& r = local_[static_cast<std::size_t>(locals[i])];

@@ -77,6 +77,8 @@ struct GroupOptions {
   int max_ctas_per_rank = 0;                                // 0 = SM count
   std::uint32_t poll_ns = 64;                               // back-off between flag polls (ns)
   bool strict_sys = false;                                  // system-scope fence before every flag
+  bool eager_post = true;                                   // bulk chain: forward a chunk once its store is done
+  bool writer_fence = true;                                 // copy warps fence their own data (see run_publisher)
   bool ll = true;                                           // LL push protocol for small `direct` calls
   int protocol = 0;                                         // chain: 0 auto (table), 1 pull, 2 push
   std::uint64_t ll_max_bytes = 0;                           // LL threshold (0 = 2 MiB, lowered for many ranks)

@@ -114,6 +114,8 @@ struct LaunchParamsT {
   std::uint32_t stage_bytes;  // bytes per bulk-copy stage; 0 = vector loads only
   std::uint32_t stages;       // bulk-copy stages per copy warp (2..kMaxStages)
   std::uint32_t push;         // chain: producers store into the consumer's buffer
+  std::uint32_t eager_post;   // bulk chain: publish each chunk as soon as its store completes
+  std::uint32_t writer_fence; // 1: each copy warp fences its own data before the hand-off; 0: the publisher does
   RankWork ranks[NL];
 };
 using LaunchParams = LaunchParamsT<kMaxLocal>;

@@ -108,6 +108,15 @@ __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t pari
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ bool mbar_test(std::uint64_t* bar, std::uint32_t parity) {  // non-blocking
+  std::uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred P;\n mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 // TMA-engine bulk copies (SASS UBLKCP): global -> shared completing on an
 // mbarrier, and shared -> global tracked by bulk async-groups.
 __device__ __forceinline__ void bulk_g2s(void* smem, const void* gsrc, std::uint32_t bytes, std::uint64_t* bar) {
@@ -208,12 +217,23 @@ __device__ bool wait_geq(const Ctx& c, const std::uint64_t* p, std::uint64_t tar
   return ok != 0;
 }
 
+// Writer-side fence (writer_fence = 1): the copy warp that produced the data
+// fences it before handing the flag to the publisher. A fence waits for the
+// issuing warp's outstanding writes; in the publisher that meant the previous
+// batch's remote flag stores, whose acknowledgements queue behind loaded
+// NVLink traffic (measured ~16 us per batch at n = 4, 64 MiB); the copy warp
+// has only its own, already completed, data writes outstanding.
+__device__ __forceinline__ void writer_fence(const LaunchParamsT<1>& P) {
+  if (P.writer_fence) fence_acq_rel_gpu();
+}
+
 // Queue "*addr = value" behind this warp's preceding stores. The warp
-// barrier orders every lane's stores before lane 0's CTA-scope release; the
-// publisher's acquire + system fence then makes them visible before the flag.
+// barrier orders every lane's stores before lane 0's fence and CTA-scope
+// release; the flag store follows in the publisher.
 __device__ void publish(Ctx& c, std::uint64_t* addr, std::uint64_t value) {
   __syncwarp();
   if (c.lane_id == 0) {
+    writer_fence(*c.P);
     while (c.tail - ld_acquire_cta(&c.sh->head[c.warp]) >= static_cast<std::uint32_t>(kRing)) {
       __nanosleep(32);
     }
@@ -225,9 +245,10 @@ __device__ void publish(Ctx& c, std::uint64_t* addr, std::uint64_t value) {
 }
 
 // The publisher warp (lane 0): drain every ring, one fence per batch.
-__device__ void run_publisher(const LaunchParamsT<1>& P, CtaShared* sh) {
+__device__ void run_publisher(const LaunchParamsT<1>& P, CtaShared* sh, const RankWork& W, int cta) {
   if ((threadIdx.x & 31) != 0) return;
   std::uint32_t head[kWarpsPerCta] = {};
+  std::uint32_t stamped = 0;  // timeline: lanes whose first hand-off has been stamped
   for (;;) {
     const std::uint32_t done = ld_acquire_cta(&sh->done);
     std::uint32_t tail[kWarpsPerCta];
@@ -246,16 +267,26 @@ __device__ void run_publisher(const LaunchParamsT<1>& P, CtaShared* sh) {
     // peers read through this GPU's L2 (its point of coherence): once the
     // stores are performed at gpu scope they are visible to NVLink readers.
     // strict_sys keeps the textbook system-scope release instead.
-    if (P.strict_sys || P.push) {  // push mode: the published data is in the peer's memory
-      fence_acq_rel_sys();
-    } else {
-      fence_acq_rel_gpu();
+    const std::uint64_t t_seen = W.trace ? globaltimer() : 0;
+    if (!P.writer_fence) {
+      if (P.strict_sys || P.push) {  // push mode: the published data is in the peer's memory
+        fence_acq_rel_sys();
+      } else {
+        fence_acq_rel_gpu();
+      }
     }
 #pragma unroll
     for (int w = 0; w < kWarpsPerCta; ++w) {
       for (std::uint32_t i = head[w]; i != tail[w]; ++i) {
         const Publication e = sh->ring[w][i % kRing];
         st_relaxed_sys(e.addr, e.value);
+      }
+      if (W.trace && head[w] != tail[w] && !((stamped >> w) & 1u) && W.trace_cap > 0) {
+        stamped |= 1u << w;  // lifecycle record fields 1/2: first batch seen / stored
+        unsigned long long* rec =
+            W.trace + (static_cast<std::size_t>(cta * kWarpsPerCta + w) * W.trace_cap + W.trace_cap - 1) * 4;
+        rec[1] = t_seen;
+        rec[2] = globaltimer();
       }
       if (head[w] != tail[w]) {
         head[w] = tail[w];
@@ -407,6 +438,7 @@ __device__ bool chain_pull_bulk(Ctx& c, int pipe, int q, int ns, std::uint32_t m
     stamp(count - 1, 3);
     if (!has_next) return;
     fence_proxy_async();  // completed TMA writes ordered before the generic-proxy hand-off
+    writer_fence(P);
     while (c.tail - ld_acquire_cta(&c.sh->head[c.warp]) >= static_cast<std::uint32_t>(kRing)) __nanosleep(32);
     c.sh->ring[c.warp][c.tail % kRing] = Publication{next_flag, tag | count};
     c.tail += 1;
@@ -455,7 +487,17 @@ __device__ bool chain_pull_bulk(Ctx& c, int pipe, int q, int ns, std::uint32_t m
         continue;
       }
       const std::uint32_t st = landed % S;
-      mbar_wait(&bars[st], (parity >> st) & 1u);
+      if (issued < mine && issued - landed < S) {
+        // A stage is free: watch the oldest load and the upstream flag of the
+        // next chunk together, so a chunk published while this lane waits
+        // goes out at once instead of after the landing.
+        bool got;
+        while (!(got = mbar_test(&bars[st], (parity >> st) & 1u)) && !ready_now(issued)) {
+        }
+        if (!got) continue;
+      } else {
+        mbar_wait(&bars[st], (parity >> st) & 1u);
+      }
       parity ^= 1u << st;
       stamp(landed, 1);
       std::uint64_t g;
@@ -470,7 +512,13 @@ __device__ bool chain_pull_bulk(Ctx& c, int pipe, int q, int ns, std::uint32_t m
                   static_cast<unsigned long long>(len));
       }
       ++landed;
-      if (issued > landed) {
+      if (has_next && P.eager_post && !P.push) {
+        // Forward now: a local store completes in about a microsecond, while
+        // waiting for the next slice to land (the lazy rule below) would hold
+        // every chunk back one loaded NVLink round trip per hop.
+        bulk_wait<0>();
+        post(landed);
+      } else if (issued > landed) {
         bulk_wait<1>();  // every store but the newest is complete
         post(landed - 1);
       } else {
@@ -687,7 +735,7 @@ __global__ void __launch_bounds__(kThreads, NL == 1 ? 1 : 3) bcast_kernel(const 
   __syncthreads();
   const auto* hdr = reinterpret_cast<const LaunchParamsT<1>*>(&P);
   if (warp == kWarpsPerCta) {
-    run_publisher(*hdr, &sh);
+    run_publisher(*hdr, &sh, P.ranks[local], cta);
     return;
   }
   Ctx c;

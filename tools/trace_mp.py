@@ -30,14 +30,16 @@ def chk(tag):
     if rank == 0 and not torch.equal(buf, ref):
         bad = int((buf != ref).sum())
         print(f"rank 0 CHECK {tag}: {bad} bad bytes", flush=True)
-for it in range(5):
+ITERS = int(os.environ.get("TRACE_ITERS", 5))
+ktimes = []
+for it in range(ITERS):
     with torch.cuda.stream(s):
         (buf.copy_(ref) if rank == 0 else buf.zero_())
     if it == 0: chk("after copy_")
     with torch.cuda.stream(s):
         tr.zero_()
     if it == 0: chk("after tr.zero_")
-    comm.set_trace(tr if it == 4 else None, cap)
+    comm.set_trace(tr if it == ITERS - 1 else None, cap)
     s.synchronize(); dist.barrier(device_ids=[local])
     if rank == 0 and not torch.equal(buf, ref):
         print(f"rank 0 iter {it}: root buffer differs BEFORE the broadcast", flush=True)
@@ -49,6 +51,7 @@ for it in range(5):
     comm.bcast(buf, m, "uint8", 0, cfg, stream=s)
     ev1.record(s)
     ev1.synchronize()
+    ktimes.append(ev0.elapsed_time(ev1) * 1e3)
     comm.check(s)
     if not torch.equal(buf, ref):
         bad = (buf != ref).nonzero().flatten()
@@ -67,7 +70,7 @@ rec = tr.view(L, cap, 4)[:, :cap - 1].cpu()
 act = life[:, 0] > 0
 t_in = int(life[:, 0][act].min()); t_in_max = int(life[:, 0][act].max()); t_out = int(life[:, 3][act].max())
 land = rec[:, :, 1]; lm = land > 0
-msg = (f"rank {rank}: barrier {evb.elapsed_time(ev0)*1e3:.1f}us kernel(ev0-ev1) {ev0.elapsed_time(ev1)*1e3:.1f}us "
+msg = (f"rank {rank}: median kernel {statistics.median(ktimes[1:]):.1f}us barrier {evb.elapsed_time(ev0)*1e3:.1f}us kernel(ev0-ev1) {ev0.elapsed_time(ev1)*1e3:.1f}us "
        f"lanes enter span {(t_in_max-t_in)/1e3:.1f}us exit at {(t_out-t_in)/1e3:.1f}us")
 if lm.any():
     msg += f" first_land {(int(land[lm].min())-t_in)/1e3:.1f}us last_land {(int(land[lm].max())-t_in)/1e3:.1f}us"
@@ -75,4 +78,31 @@ out = [None] * world
 dist.all_gather_object(out, msg)
 if rank == 0:
     print("\n".join(out))
+# cross-rank milestones on the (driver-synchronised) globaltimer
+def mn(x): return int(x[x > 0].min()) if (x > 0).any() else 0
+def mx(x): return int(x.max())
+ms = dict(enter=t_in, enter_last=t_in_max, first_issue=mn(rec[:, :, 0]), first_land=mn(rec[:, :, 1]),
+          last_land=mx(rec[:, :, 1]), last_store=mx(rec[:, :, 2]), last_post=mx(rec[:, :, 3]), exit=t_out)
+allms = [None] * world
+dist.all_gather_object(allms, ms)
+if rank == 0:
+    base = min(d["enter"] for d in allms)
+    for r, d in enumerate(allms):
+        print(f"rank {r} (us from first enter): " + " ".join(f"{k}={(v - base) / 1e3:.2f}" if v else f"{k}=-"
+                                                            for k, v in d.items()))
+npz = os.environ.get("TRACE_NPZ")
+if npz:
+    import numpy as np
+    np.savez_compressed(npz.replace("RANK", str(rank)), rec=tr.view(L, cap, 4).cpu().numpy(),
+                        plan=np.array(list(comm.plan(cfg, 0, m).values())), ktimes=np.array(ktimes))
+csv_path = os.environ.get("TRACE_CSV")
+if csv_path:
+    from paper_1707_09414_b200.timeline import chain_rows, write_csv
+    plan = comm.plan(cfg, 0, m)
+    rows = chain_rows(tr.cpu().numpy(), L, cap, plan, world, 0, rank)
+    allrows = [None] * world
+    dist.all_gather_object(allrows, rows)
+    if rank == 0:
+        write_csv([r for part in allrows for r in part], csv_path)
+        print("wrote", csv_path, "plan", plan)
 dist.barrier(device_ids=[local]); comm.close(); dist.destroy_process_group()

@@ -31,6 +31,7 @@ ap.add_argument("--max", type=int, default=1 << 30)
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--chunks", default="65536,131072,262144,524288,1048576,2097152,4194304")
 ap.add_argument("--cands", default="direct,knomial,scatter_ring_allgather,chain_pipelined")
+ap.add_argument("--raw", default="", help="also write every measurement (config, n, bytes, seconds) here")
 a = ap.parse_args()
 
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -45,6 +46,7 @@ stream = torch.cuda.Stream(device=dev)
 torch.cuda.synchronize()
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 n_eval = [0]
+raw = []
 
 
 def quantize(t):
@@ -72,7 +74,9 @@ def cost(cfg, n, m):
             times.append(ev0.elapsed_time(ev1) * 1e-3)
     t = torch.tensor(times, dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return quantize(float(statistics.median(t.cpu().tolist())))
+    med = float(statistics.median(t.cpu().tolist()))
+    raw.append((cfg.algorithm.name, cfg.radix_k, cfg.chunk_bytes, n, m, med))
+    return quantize(med)
 
 
 sizes = []
@@ -124,6 +128,11 @@ if push_from is not None:
 if rank == 0:
     os.makedirs(os.path.dirname(os.path.abspath(a.out)), exist_ok=True)
     B.save_table(table, a.out)
+    if a.raw:
+        with open(a.raw, "w") as f:
+            f.write("algorithm,radix,chunk_bytes,n,bytes,seconds\n")
+            for r in raw:
+                f.write(",".join(map(str, r)) + "\n")
     print(f"wrote {a.out}: {len(table.entries)} entries from {n_eval[0]} measurements in {time.time() - t0:.1f}s")
     print(table.text())
 dist.barrier(device_ids=[local])
