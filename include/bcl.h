@@ -177,9 +177,11 @@ bcl_status_t bcl_comm_set_table(bcl_comm_t c, bcl_table_t t);
  * chunks c with c % (lanes / Q) == l / Q. */
 bcl_status_t bcl_comm_plan(bcl_comm_t c, const bcl_config_t* config, int root, uint64_t bytes, int* slices,
                            uint64_t* slice_bytes, uint32_t* n_chunks, int* ctas);
-/* Pipelined-chain transport protocol: 0 auto (the table's measured
+/* Pipelined-chain transport protocol: 0 auto (LL lines up to the group's LL
+ * chain cap, BCL_LL_CHAIN_MAX, default 8 MiB; above it the table's measured
  * "# bcl-push-from" rule), 1 pull (consumers load from the upstream buffer),
- * 2 push (producers store into the downstream buffer). */
+ * 2 push (producers store into the downstream buffer), 3 LL (flagged 16-byte
+ * lines forwarded hop by hop; fails above the cap). */
 bcl_status_t bcl_comm_set_protocol(bcl_comm_t c, int protocol);
 /* The config a NULL-config call would run for this size (select + clamp). */
 bcl_status_t bcl_comm_choose(bcl_comm_t c, uint64_t message_bytes, bcl_config_t* out);

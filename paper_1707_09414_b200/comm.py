@@ -128,8 +128,8 @@ class Comm:
         return {"slices": q.value, "slice_bytes": sb.value, "n_chunks": nc.value, "ctas": ctas.value}
 
     def set_protocol(self, protocol) -> None:
-        """Chain transport: "auto" (table rule), "pull" or "push"."""
-        code = {"auto": 0, "pull": 1, "push": 2}[protocol] if isinstance(protocol, str) else int(protocol)
+        """Chain transport: "auto" (LL up to the LL chain cap, then the table rule), "pull", "push" or "ll"."""
+        code = {"auto": 0, "pull": 1, "push": 2, "ll": 3}[protocol] if isinstance(protocol, str) else int(protocol)
         _check(lib().bcl_comm_set_protocol(self._h, code))
 
     def choose(self, message_bytes: int) -> AlgorithmConfig:

@@ -23,6 +23,8 @@ struct ExportInfo {
   std::int32_t pid;
   std::uint64_t region_bytes;
   std::uint64_t heap_bytes;
+  std::uint64_t ll_max;        // LL landing-area geometry must agree across ranks
+  std::uint64_t ll_chain_max;
   cudaIpcMemHandle_t region;
   cudaIpcMemHandle_t heap;
 };
@@ -77,6 +79,7 @@ GroupOptions GroupOptions::from_env() {
   if (const char* v = std::getenv("BCL_LL")) o.ll = std::atoi(v) != 0;
   if (const char* v = std::getenv("BCL_PROTOCOL")) o.protocol = std::atoi(v);
   if (const char* v = std::getenv("BCL_LL_MAX")) o.ll_max_bytes = std::strtoull(v, nullptr, 10);
+  if (const char* v = std::getenv("BCL_LL_CHAIN_MAX")) o.ll_chain_max_bytes = std::strtoll(v, nullptr, 10);
   if (const char* v = std::getenv("BCL_HOST_PIECE")) o.host_piece = std::max<std::uint64_t>(4096, std::strtoull(v, nullptr, 10));
   if (const char* v = std::getenv("BCL_STAGES")) o.stages = static_cast<std::uint32_t>(std::clamp(std::atoi(v), 2, dev::kMaxStages));
   if (const char* v = std::getenv("BCL_STAGE_BYTES")) o.stage_bytes = static_cast<std::int64_t>(std::strtoul(v, nullptr, 10)) / 16 * 16;
@@ -103,8 +106,8 @@ AggregateRankError::AggregateRankError(std::vector<RankFailure> failures)
 
 void Group::alloc_rank(LocalRank& r, std::size_t heap_bytes) {
   DeviceScope ds(r.device);
-  r.region_bytes = (ll_offset(lanes_alloc_) + static_cast<std::size_t>(n_) * 2 * (ll_max_ / 8) * 2) *
-                   sizeof(std::uint64_t);
+  r.region_bytes = (ll_offset(lanes_alloc_) + ll_words()) * sizeof(std::uint64_t);
+  r.ll_last_to.assign(static_cast<std::size_t>(n_) * 2, 0);
   ck(cudaMalloc(&r.region, r.region_bytes), "cudaMalloc(region)");
   ck(cudaMemset(r.region, 0, r.region_bytes), "cudaMemset(region)");
   ck(cudaMalloc(&r.d_peers, sizeof(dev::PeerTable)), "cudaMalloc(peers)");
@@ -160,6 +163,14 @@ std::uint64_t ll_cap(int n, const GroupOptions& opt) {
   return cap / 16 * 16;
 }
 
+// The chain landing area (one source: the ring predecessor) costs 4 x cap
+// bytes per rank, independent of n.
+std::uint64_t ll_chain_cap(const GroupOptions& opt) {
+  const std::int64_t v = opt.ll_chain_max_bytes < 0 ? static_cast<std::int64_t>(dev::kLLChainMaxBytes)
+                                                   : opt.ll_chain_max_bytes;
+  return static_cast<std::uint64_t>(std::min<std::int64_t>(v, 64ll << 20)) / 16 * 16;
+}
+
 }  // namespace
 
 std::shared_ptr<Group> Group::create_local(const std::vector<int>& devices, const GroupOptions& opt) {
@@ -208,6 +219,7 @@ std::shared_ptr<Group> Group::create_local(const std::vector<int>& devices, cons
   g->lanes_alloc_ = g->lanes_;
   g->single_device_ = g->by_device_.size() == 1;
   g->ll_max_ = ll_cap(n, opt);
+  g->ll_chain_max_ = ll_chain_cap(opt);
   g->local_.resize(static_cast<std::size_t>(n));
   for (int r = 0; r < n; ++r) {
     LocalRank& lr = g->local_[static_cast<std::size_t>(r)];
@@ -246,6 +258,7 @@ std::shared_ptr<Group> Group::create_rank(int n, int rank, int device, std::size
   g->lanes_ = lanes_for(device, 1, opt.max_ctas_per_rank, g->opt_);
   g->lanes_alloc_ = g->lanes_;
   g->ll_max_ = ll_cap(n, opt);
+  g->ll_chain_max_ = ll_chain_cap(opt);
   g->local_.resize(1);
   g->local_[0].rank = rank;
   g->local_[0].device = device;
@@ -267,6 +280,8 @@ std::vector<std::uint8_t> Group::export_info() const {
   info.pid = static_cast<std::int32_t>(getpid());
   info.region_bytes = r.region_bytes;
   info.heap_bytes = r.heap_bytes;
+  info.ll_max = ll_max_;
+  info.ll_chain_max = ll_chain_max_;
   ck(cudaIpcGetMemHandle(&info.region, r.region), "cudaIpcGetMemHandle(region)");
   if (r.heap) ck(cudaIpcGetMemHandle(&info.heap, r.heap), "cudaIpcGetMemHandle(heap)");
   std::vector<std::uint8_t> out(sizeof info);
@@ -285,6 +300,9 @@ void Group::connect(const std::vector<std::vector<std::uint8_t>>& infos) {
     std::memcpy(&all[i], infos[i].data(), sizeof(ExportInfo));
     if (all[i].magic != kInfoMagic || all[i].n != n_ || all[i].rank != static_cast<int>(i)) {
       throw std::invalid_argument("info blobs must be ordered by rank and belong to this group");
+    }
+    if (all[i].ll_max != ll_max_ || all[i].ll_chain_max != ll_chain_max_) {
+      throw std::invalid_argument("ranks disagree on the LL landing areas (BCL_LL_MAX / BCL_LL_CHAIN_MAX)");
     }
     lanes = std::min(lanes, static_cast<int>(all[i].lanes));
   }
@@ -360,7 +378,9 @@ void Group::set_table(const TuningTable& t) {
 void Group::clear_table() { have_table_ = false; }
 
 void Group::set_protocol(int protocol) {
-  if (protocol < 0 || protocol > 2) throw std::invalid_argument("protocol must be 0 (auto), 1 (pull) or 2 (push)");
+  if (protocol < 0 || protocol > 3) {
+    throw std::invalid_argument("protocol must be 0 (auto), 1 (pull), 2 (push) or 3 (ll)");
+  }
   opt_.protocol = protocol;
 }
 
@@ -368,9 +388,25 @@ void Group::set_protocol(int protocol) {
 // table records from which size on it wins.
 bool Group::use_push(const CallPlan& p, std::uint64_t bytes) const {
   if (!p.implicit_chain || n_ < 2) return false;
-  if (opt_.protocol == 1) return false;
+  if (opt_.protocol == 1 || opt_.protocol == 3) return false;
   if (opt_.protocol == 2) return true;
   return select_push(table(), n_, bytes);
+}
+// LL chain: every pipelined chain up to ll_chain_max_ in auto mode (the
+// measured table decides between it and the other schedules), or on request.
+// Provenance / timeline recording need the lane executor.
+bool Group::use_ll_chain(const CallPlan& p, std::uint64_t bytes, const std::vector<int>& locals) const {
+  if (!p.implicit_chain || n_ < 2 || !opt_.ll || bytes == 0) return false;
+  if (opt_.protocol == 1 || opt_.protocol == 2) return false;
+  for (int li : locals) {
+    const LocalRank& r = local_[static_cast<std::size_t>(li)];
+    if (r.prov != nullptr || r.trace != nullptr) return false;
+  }
+  if (bytes > ll_chain_max_) {
+    if (opt_.protocol == 3) throw std::invalid_argument("message exceeds the LL chain landing area");
+    return false;
+  }
+  return true;
 }
 const TuningTable& Group::table() const { return have_table_ ? table_ : builtin_table(); }
 
@@ -498,7 +534,7 @@ void Group::fill_rank_work(dev::RankWork& w, LocalRank& r, const CallPlan& p, vo
 }
 
 void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& bufs, std::uint64_t bytes,
-                      int root, cudaStream_t stream) {
+                      int root, cudaStream_t stream, bool chain) {
   dev::LLParams P{};
   P.n_ranks = n_;
   P.root = root;
@@ -506,6 +542,8 @@ void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& 
   P.bytes = bytes;
   P.lines = static_cast<std::uint32_t>((bytes + 7) / 8);
   P.area_lines = static_cast<std::uint32_t>(ll_max_ / 8);
+  P.chain = chain ? 1 : 0;
+  P.chain_lines = static_cast<std::uint32_t>(ll_chain_max_ / 8);
   // ~4 lines per thread, at most kLLMaxCtas CTAs per rank
   // ~2 lines per thread; ranks sharing a GPU must stay co-resident
   // (cooperative launch): at most 4 LL CTAs per SM in total.
@@ -529,10 +567,20 @@ void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& 
     w.err = r.err_dev;
     w.abort = reinterpret_cast<int*>(r.region + 3 * S + static_cast<std::size_t>(n_));
     const std::uint32_t half = static_cast<std::uint32_t>(e & 1u);
-    if (r.rank == root) {
-      w.need_credit = r.ll_last[half];
-      r.ll_last[half] = e;
-    } else {
+    const int logical = (r.rank - root + n_) % n_;
+    auto target = [&](int t) {  // this call writes lines into t's landing area
+      std::uint64_t& last = r.ll_last_to[static_cast<std::size_t>(t) * 2 + half];
+      w.need[t] = last;
+      last = e;
+    };
+    if (chain) {
+      if (logical + 1 < n_) target((r.rank + 1) % n_);
+    } else if (logical == 0) {
+      for (int t = 0; t < n_; ++t) {
+        if (t != root) target(t);
+      }
+    }
+    if (logical != 0) {
       w.done = reinterpret_cast<unsigned long long*>(r.region + 3 * S + 2 * static_cast<std::size_t>(n_) + 1);
       r.ll_done += static_cast<std::uint64_t>(P.ctas);
       w.done_target = r.ll_done;
@@ -548,7 +596,11 @@ void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& 
 void Group::launch_group(const std::vector<int>& locals, const std::vector<void*>& bufs,
                          std::uint64_t bytes, int root, const CallPlan& p, cudaStream_t stream) {
   if (p.config.algorithm == Algorithm::Direct && bytes <= ll_max_ && opt_.ll) {
-    launch_ll(locals, bufs, bytes, root, stream);
+    launch_ll(locals, bufs, bytes, root, stream, false);
+    return;
+  }
+  if (use_ll_chain(p, bytes, locals)) {
+    launch_ll(locals, bufs, bytes, root, stream, true);
     return;
   }
   dev::LaunchParams P{};

@@ -82,6 +82,7 @@ struct GroupOptions {
   bool ll = true;                                           // LL push protocol for small `direct` calls
   int protocol = 0;                                         // chain: 0 auto (table), 1 pull, 2 push
   std::uint64_t ll_max_bytes = 0;                           // LL threshold (0 = 2 MiB, lowered for many ranks)
+  std::int64_t ll_chain_max_bytes = -1;                     // LL pipelined chain up to this size (-1 = default)
   std::uint64_t host_piece = 4ull << 20;                    // host-buffer calls: H2D/bcast/D2H pipeline piece
   std::int64_t stage_bytes = -1;                            // bulk-copy stage per warp: 0 = vector loads,
                                                             // -1 = auto (8 KiB across GPUs, 0 on one GPU)
@@ -126,7 +127,7 @@ struct LocalRank {
   unsigned long long* trace{};  // optional per-lane event timestamps
   std::uint32_t trace_cap{0};
   std::uint64_t launches{0};
-  std::uint64_t ll_last[2]{0, 0};  // last epoch this rank was an LL root, per half
+  std::vector<std::uint64_t> ll_last_to;  // [target * 2 + half]: last epoch this rank wrote LL lines to target
   std::uint64_t ll_done{0};        // cumulative LL CTA completions expected as a receiver
   std::vector<void*> opened;    // IPC mappings to close
 };
@@ -152,7 +153,7 @@ class Group {
   int local_index_of(int rank) const;
 
   void set_table(const TuningTable& t);
-  void set_protocol(int protocol);  // 0 auto (table's push-from rule), 1 pull, 2 push
+  void set_protocol(int protocol);  // 0 auto (LL chain, then the table's push-from rule), 1 pull, 2 push, 3 LL
   void clear_table();
   const TuningTable& table() const;
   AlgorithmConfig choose(std::uint64_t bytes, const AlgorithmConfig* cfg) const;
@@ -190,15 +191,20 @@ class Group {
   cudaEvent_t event(LocalRank& r, std::size_t i);
   void ensure_scratch(int local_index, std::uint64_t bytes);
   void launch_ll(const std::vector<int>& locals, const std::vector<void*>& bufs, std::uint64_t bytes, int root,
-                 cudaStream_t stream);
+                 cudaStream_t stream, bool chain);
   void raise_errors(const std::vector<int>& locals);
+  bool use_ll_chain(const CallPlan& p, std::uint64_t bytes, const std::vector<int>& locals) const;
   std::size_t region_stride() const { return static_cast<std::size_t>(n_) * lanes_; }
   // Offset (in 8-byte words) of the LL landing area for a flag stride of L lanes.
   std::size_t ll_offset(int lanes) const {
     const std::size_t w = 3 * static_cast<std::size_t>(n_) * lanes + 2 * static_cast<std::size_t>(n_) + 2;
     return (w + 1) / 2 * 2;
   }
-  std::uint64_t ll_max_{dev::kLLMaxBytes};  // LL protocol threshold (bytes)
+  std::uint64_t ll_max_{dev::kLLMaxBytes};  // LL protocol threshold (bytes), direct schedule
+  std::uint64_t ll_chain_max_{0};           // LL pipelined chain up to this size (0 = off)
+  std::size_t ll_words() const {            // 8-byte words of LL landing areas per rank
+    return (static_cast<std::size_t>(n_) * 2 * (ll_max_ / 8) + 2 * (ll_chain_max_ / 8)) * 2;
+  }
 
   int n_{0};
   int lanes_{0};

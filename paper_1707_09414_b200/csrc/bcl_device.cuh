@@ -30,6 +30,7 @@ constexpr int kWarpsPerCta = 8;  // lanes per CTA
 constexpr int kThreads = (kWarpsPerCta + 1) * 32;  // + one publisher warp
 constexpr int kMaxStages = 4;    // bulk-copy stages per copy warp
 constexpr std::uint32_t kLLMaxBytes = 2048 * 1024;      // largest LL message (per-group cap may be lower)
+constexpr std::uint32_t kLLChainMaxBytes = 8u << 20;     // default LL pipelined-chain cap
 constexpr int kLLThreads = 512;
 constexpr int kLLMaxCtas = 64;                          // CTAs per rank for one LL call
 
@@ -134,7 +135,7 @@ struct LLRank {
   const PeerTable* peers;
   ErrorRecord* err;
   int* abort;
-  std::uint64_t need_credit;  // root: receivers must have finished this epoch (same half)
+  std::uint64_t need[kMaxRanks];  // writer: target t must have credited need[t] (0 = not a target / no wait)
   unsigned long long* done;   // receiver: local completion counter (cumulative over calls)
   unsigned long long done_target;  // receiver: value of *done once every CTA of this call finished
 };
@@ -149,7 +150,9 @@ struct LLParamsT {
   std::uint64_t bytes;
   std::uint64_t epoch;
   std::uint32_t half;
-  std::uint32_t area_lines;   // lines per (source, half) landing area
+  std::uint32_t area_lines;   // lines per (source, half) landing area of the direct schedule
+  std::uint32_t chain;        // 1: pipelined chain (rank l forwards every line to l + 1)
+  std::uint32_t chain_lines;  // lines per half of the chain landing area (after the direct areas)
   std::uint64_t timeout_ns;
   LLRank ranks[NL];
 };

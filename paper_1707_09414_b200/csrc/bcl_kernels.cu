@@ -23,6 +23,16 @@
 
 #include "bcl_device.cuh"
 
+// 16-byte loads a lane issues before its stores (bytes in flight per warp =
+// 512 x BCL_LDG_UNROLL), and the co-resident CTAs per SM the shared-GPU
+// kernel is compiled for (register budget).
+#ifndef BCL_LDG_UNROLL
+#define BCL_LDG_UNROLL 8
+#endif
+#ifndef BCL_SHARED_MIN_BLOCKS
+#define BCL_SHARED_MIN_BLOCKS 3
+#endif
+
 namespace bcl {
 namespace dev {
 namespace {
@@ -315,7 +325,7 @@ __device__ void warp_copy(const Ctx& c, const std::uint8_t* src, std::uint8_t* d
   const std::uint64_t nvec = (hi - body_lo) / 16;
   const uint4* vs = reinterpret_cast<const uint4*>(src + body_lo);
   uint4* vd = reinterpret_cast<uint4*>(dst + body_lo);
-  constexpr int U = 8;
+  constexpr int U = BCL_LDG_UNROLL;
   for (std::uint64_t base = 0; base < nvec; base += U * 32) {
     uint4 r[U];
 #pragma unroll
@@ -717,7 +727,7 @@ __device__ void run_events(Ctx& c, int pipe, int q, int ns) {
 // NL = 1: one rank per GPU (full register budget). NL = kMaxLocal: ranks
 // sharing a GPU need several co-resident CTAs per SM, hence the 3-CTA bound.
 template <int NL>
-__global__ void __launch_bounds__(kThreads, NL == 1 ? 1 : 3) bcast_kernel(const __grid_constant__ LaunchParamsT<NL> P) {
+__global__ void __launch_bounds__(kThreads, NL == 1 ? 1 : BCL_SHARED_MIN_BLOCKS) bcast_kernel(const __grid_constant__ LaunchParamsT<NL> P) {
   __shared__ CtaShared sh;
   const int local = NL == 1 ? 0 : static_cast<int>(blockIdx.x) / P.ctas_per_rank;
   const int cta = NL == 1 ? static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x) % P.ctas_per_rank;
@@ -804,6 +814,12 @@ __device__ void ll_fail(const LLRank& R, int peer, std::uint64_t line, std::uint
   }
 }
 
+// LL kernel. direct: the root writes every line into each receiver's
+// landing area for that source. chain (pipelined chain, schedules.cpp:161-187
+// at line granularity): logical rank l polls its chain landing area, copies
+// each line's payload out and forwards the very same line to l + 1, so the
+// hops overlap line by line with no fence and no flag round trip. Writers
+// first wait for their targets' credits for the half they are about to reuse.
 template <int NL>
 __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ LLParamsT<NL> P) {
   const LLRank& R = P.ranks[NL == 1 ? 0 : static_cast<int>(blockIdx.x) / P.ctas];
@@ -811,23 +827,32 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ 
   const std::uint32_t first = cta * blockDim.x + threadIdx.x;
   const std::uint32_t stride = static_cast<std::uint32_t>(P.ctas) * blockDim.x;
   const std::uint32_t flag = static_cast<std::uint32_t>(P.epoch);
-  const std::size_t area = (static_cast<std::size_t>(P.root) * 2 + P.half) * P.area_lines;
-  if (R.rank == P.root) {
-    // The half we are about to overwrite was last used at need_credit: wait
-    // until every receiver is done with it (normally long ago).
-    if (threadIdx.x < static_cast<unsigned>(P.n_ranks) && static_cast<int>(threadIdx.x) != P.root &&
-        R.need_credit > 0) {
-      const std::uint64_t* cr = R.credit + threadIdx.x;
+  const int n = P.n_ranks;
+  const int logical = (R.rank - P.root + n) % n;
+  const int next = (R.rank + 1) % n;
+  const bool chain = P.chain != 0;
+  const bool writer = chain ? logical + 1 < n : logical == 0;
+  const std::size_t area =
+      chain ? static_cast<std::size_t>(n) * 2 * P.area_lines + static_cast<std::size_t>(P.half) * P.chain_lines
+            : (static_cast<std::size_t>(P.root) * 2 + P.half) * P.area_lines;
+  if (writer) {
+    // The half we are about to overwrite was last written for target t in
+    // epoch need[t]: wait until t has read it (normally long ago).
+    const int t = static_cast<int>(threadIdx.x);
+    if (t < n && R.need[t] > 0) {
+      const std::uint64_t* cr = R.credit + t;
       const std::uint64_t t0 = globaltimer();
       std::uint64_t v;
-      while ((v = ld_relaxed_sys(cr)) < R.need_credit) {
+      while ((v = ld_relaxed_sys(cr)) < R.need[t]) {
         if (globaltimer() - t0 > P.timeout_ns) {
-          ll_fail(R, static_cast<int>(threadIdx.x), 0, v, R.need_credit);
+          ll_fail(R, t, 0, v, R.need[t]);
           break;
         }
       }
     }
     __syncthreads();
+  }
+  if (logical == 0) {
     const bool aligned = (reinterpret_cast<std::uintptr_t>(R.buf) & 7u) == 0;
     for (std::uint32_t i = first; i < P.lines; i += stride) {
       const std::uint64_t off = static_cast<std::uint64_t>(i) * 8;
@@ -842,15 +867,21 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ 
           if (b < 4) lo |= byte << (8 * b); else hi |= byte << (8 * (b - 4));
         }
       }
-      for (int d = 0; d < P.n_ranks; ++d) {
-        if (d == P.root) continue;
-        st_volatile_v4(R.peers->ll[d] + area + i, lo, flag, hi, flag);
+      if (chain) {
+        st_volatile_v4(R.peers->ll[next] + area + i, lo, flag, hi, flag);
+      } else {
+        for (int d = 0; d < n; ++d) {
+          if (d == P.root) continue;
+          st_volatile_v4(R.peers->ll[d] + area + i, lo, flag, hi, flag);
+        }
       }
     }
     return;
   }
-  // Receiver: poll our landing lines for this source and copy out.
+  // Receiver: poll our landing lines, forward (chain, not the tail), copy out.
   const uint4* src = R.ll + area;
+  uint4* fwd = chain && writer ? R.peers->ll[next] + area : nullptr;
+  const int source = chain ? (R.rank + n - 1) % n : P.root;
   const bool aligned = (reinterpret_cast<std::uintptr_t>(R.buf) & 7u) == 0;
   bool ok = true;
   for (std::uint32_t i = first; i < P.lines && ok; i += stride) {
@@ -863,7 +894,7 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ 
         if (v.y == flag && v.w == flag) break;
         if ((++spins & 1023u) == 0) {
           if (*(volatile int*)R.abort != 0 || globaltimer() - t0 > P.timeout_ns) {
-            if (*(volatile int*)R.abort == 0) ll_fail(R, P.root, i, v.y, flag);
+            if (*(volatile int*)R.abort == 0) ll_fail(R, source, i, v.y, flag);
             ok = false;
             break;
           }
@@ -871,6 +902,7 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ 
       }
       if (!ok) break;
     }
+    if (fwd != nullptr) st_volatile_v4(fwd + i, v.x, v.y, v.z, v.w);
     const std::uint64_t off = static_cast<std::uint64_t>(i) * 8;
     if (aligned && off + 8 <= P.bytes) {
       *reinterpret_cast<uint2*>(R.buf + off) = make_uint2(v.x, v.z);
@@ -882,9 +914,9 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ 
   }
   __syncthreads();
   if (threadIdx.x == 0 && ok) {
-    // The last CTA to finish tells the root every line of this epoch has
-    // been read, so the root may reuse the half.
-    if (atomicAdd(R.done, 1ull) + 1 == R.done_target) st_relaxed_sys(R.peers->credit[P.root] + R.rank, P.epoch);
+    // The last CTA to finish tells the source every line of this epoch has
+    // been read, so the source may reuse the half.
+    if (atomicAdd(R.done, 1ull) + 1 == R.done_target) st_relaxed_sys(R.peers->credit[source] + R.rank, P.epoch);
   }
 }
 

@@ -57,16 +57,30 @@ def make_bufs(n, m, root, payload, offsets=None):
     return store, views
 
 
-def run_case(algo, n, root, m, chunk=0, radix=0, seed=1, offsets=None):
+def set_protocol(n, protocol):
+    for c in comms_for(n):
+        c.set_protocol(protocol)
+
+
+def run_case(algo, n, root, m, chunk=0, radix=0, seed=1, offsets=None, protocol="auto"):
     payload = O.payload(seed, m)
     expect = [bytearray(m) for _ in range(n)]
     expect[root][:] = payload
     O.bcast(algo, n, root, expect, chunk=chunk, radix=radix)
     _, views = make_bufs(n, m, root, payload, offsets)
-    B.run_bcast(comms_for(n), root, views, m, cfg_of(algo, chunk, radix))
+    set_protocol(n, protocol)
+    try:
+        B.run_bcast(comms_for(n), root, views, m, cfg_of(algo, chunk, radix))
+    finally:
+        set_protocol(n, "auto")
     for r in range(n):
         got = views[r].cpu().numpy().tobytes()
-        assert got == bytes(expect[r]), f"{algo} n={n} root={root} M={m} C={chunk}: rank {r} differs"
+        assert got == bytes(expect[r]), f"{algo}/{protocol} n={n} root={root} M={m} C={chunk}: rank {r} differs"
+
+
+# The pipelined chain runs on two device paths: LL lines forwarded hop by hop
+# (auto up to the LL chain cap) and the lane executor (pull).
+CHAIN_PROTOCOLS = ["auto", "pull"]
 
 
 @pytest.mark.parametrize("idx", range(len(GOLD["bcasts"])))
@@ -83,16 +97,18 @@ def test_reference_trials_bit_exact(idx):
 
 
 @pytest.mark.parametrize("algo", ["direct", "chain", "knomial", "scatter_ring_allgather",
-                                  "chain_pipelined", "knomial_staged"])
+                                  "chain_pipelined", "chain_pipelined/pull", "knomial_staged"])
 @pytest.mark.parametrize("m", [0, 1, 4, 15, 16, 17, 1000, 4096, 65537])
 def test_every_root_small_sizes(algo, m):
+    algo, _, protocol = algo.partition("/")
     for n in (2, 3, 5, 8):
         for root in range(n):
             run_case(algo, n, root, m, chunk=max(1, m // 3 + 1) if m else 7, radix=2 + root % 3,
-                     seed=m * 31 + root)
+                     seed=m * 31 + root, protocol=protocol or "auto")
 
 
-def test_chunk_not_dividing_message_and_tiny_chunks():
+@pytest.mark.parametrize("protocol", CHAIN_PROTOCOLS)
+def test_chunk_not_dividing_message_and_tiny_chunks(protocol):
     # C in [1, M+1] as acceptance.cpp:203-205 draws it.
     rng = random.Random(5)
     for _ in range(20):
@@ -101,20 +117,38 @@ def test_chunk_not_dividing_message_and_tiny_chunks():
         chunk = 1 + rng.randrange(m + 1)
         if (m + chunk - 1) // max(chunk, 1) > 200000:
             chunk = m // 200000 + 1
-        run_case("chain_pipelined", n, rng.randrange(n), m, chunk=chunk, seed=rng.randrange(1 << 30))
+        run_case("chain_pipelined", n, rng.randrange(n), m, chunk=chunk, seed=rng.randrange(1 << 30),
+                 protocol=protocol)
 
 
-def test_misaligned_buffers():
+@pytest.mark.parametrize("protocol", CHAIN_PROTOCOLS)
+def test_misaligned_buffers(protocol):
     """Different byte misalignments per rank (vector and byte paths)."""
     for offs in ([0, 1, 2, 3], [5, 5, 5, 5], [16, 3, 0, 9]):
         for algo in ("chain_pipelined", "knomial", "scatter_ring_allgather"):
-            run_case(algo, 4, 1, 100003, chunk=8191, radix=2, seed=11, offsets=offs)
+            run_case(algo, 4, 1, 100003, chunk=8191, radix=2, seed=11, offsets=offs, protocol=protocol)
 
 
-def test_sixteen_ranks_one_megabyte():
+@pytest.mark.parametrize("protocol", CHAIN_PROTOCOLS)
+def test_sixteen_ranks_one_megabyte(protocol):
     # proj/tests/test_runtime.cpp:224-236 shape.
-    run_case("chain_pipelined", 16, 0, 1 << 20, chunk=65536, seed=99)
+    run_case("chain_pipelined", 16, 0, 1 << 20, chunk=65536, seed=99, protocol=protocol)
     run_case("scatter_ring_allgather", 16, 5, 1 << 20, seed=98)
+
+
+def test_ll_chain_cap_and_interleaving_with_direct():
+    """LL chain at and around its cap (8 MiB), interleaved with LL direct
+    calls from changing roots: the landing halves are shared per writer and
+    target, so credits must track (writer, target, half) exactly."""
+    n = 4
+    cap = 8 << 20
+    sizes = [cap, cap - 8, 3 << 20, cap + 16, 100, 2 << 20]
+    for i, m in enumerate(sizes * 2):
+        root = (i * 3) % n
+        algo = "chain_pipelined" if i % 2 == 0 else "direct"
+        run_case(algo, n, root, m, chunk=262144, seed=i + 7)
+    with pytest.raises(ValueError):
+        run_case("chain_pipelined", n, 0, cap + 16, chunk=262144, protocol="ll")
 
 
 def test_config1_full_size_all_ranks_equal_root():

@@ -51,10 +51,15 @@ def test_one_process_all_gpus_every_algorithm_and_root():
     devices = list(range(min(ngpu(), 8)))
     comms = B.Comm.local(devices, timeout_s=10)
     rng = random.Random(17)
-    for algo in ("chain_pipelined", "knomial", "scatter_ring_allgather", "direct", "chain"):
+    for algo in ("chain_pipelined", "chain_pipelined/pull", "knomial", "scatter_ring_allgather", "direct", "chain"):
+        algo, _, protocol = algo.partition("/")
+        for c in comms:
+            c.set_protocol(protocol or "auto")  # auto: LL lines up to 8 MiB; pull: the lane executor
         for root in range(len(devices)):
-            for m in (0, 4, 4097, 1 << 20, rng.randrange(1, 5 << 20)):
+            for m in (0, 4, 4097, 1 << 20, rng.randrange(1, 5 << 20), (8 << 20) + 5):
                 run_group(comms, devices, algo, root, m, chunk=max(1, m // 5 + 3), seed=m + root)
+    for c in comms:
+        c.set_protocol("auto")
     run_group(comms, devices, "chain_pipelined", 0, 64 << 20, chunk=512 << 10, seed=5)
 
 
@@ -98,7 +103,11 @@ def _ipc_worker(rank, world, port, q):
         ok = True
         for it, (algo, m, root) in enumerate([("chain_pipelined", 64 << 20, 0), ("knomial", 12345, world - 1),
                                               ("scatter_ring_allgather", 3 << 20, 1 % world),
-                                              ("chain_pipelined", 1, 0), ("direct", 777, 0)]):
+                                              ("chain_pipelined", 1, 0), ("direct", 777, 0),
+                                              ("chain_pipelined", (5 << 20) + 3, world - 1),
+                                              ("chain_pipelined", 8 << 20, 1 % world),
+                                              ("direct", 1 << 20, world - 1),
+                                              ("chain_pipelined", (3 << 20) + 1, 0)]):
             payload = O.payload(it, m)
             if rank == root:
                 buf[:m].copy_(torch.frombuffer(bytearray(payload), dtype=torch.uint8))

@@ -22,7 +22,12 @@ HARNESS = os.path.join(ROOT, "oracle", "_ref", "ref_harness")
 
 
 def main():
-    raw = list(csv.DictReader(open(sys.argv[1])))
+    raw, seen = [], set()
+    for r in csv.DictReader(open(sys.argv[1])):  # first measurement of a point = the default protocol
+        key = (r["algorithm"], r["radix"], r["chunk_bytes"], r["n"], r["bytes"])
+        if key not in seen:
+            seen.add(key)
+            raw.append(r)
     chain = [r for r in raw if r["algorithm"] == "chain_pipelined" and int(r["bytes"]) >= 1 << 20]
     rows, y = [], []
     for r in chain:
