@@ -169,6 +169,11 @@ bcl_status_t bcl_comm_export(bcl_comm_t c, void* blob, size_t cap, size_t* len);
 bcl_status_t bcl_comm_connect(bcl_comm_t c, const void* blobs, size_t blob_len);
 bcl_status_t bcl_comm_destroy(bcl_comm_t c);
 bcl_status_t bcl_comm_info(bcl_comm_t c, int* n, int* rank, int* device, int* lanes);
+/* Largest message each line protocol takes on this communicator (bytes; 0 =
+ * unavailable): LL for `direct`, LL and LL128 for the pipelined chain (LL128
+ * needs every rank on its own GPU). New on B200; no reference counterpart. */
+bcl_status_t bcl_comm_protocol_caps(bcl_comm_t c, uint64_t* ll_direct_max, uint64_t* ll_chain_max,
+                                    uint64_t* ll128_max);
 /* Tuning table consulted when a call passes config == NULL; the builtin
  * measured B200 table is used until one is set. The table is copied. */
 bcl_status_t bcl_comm_set_table(bcl_comm_t c, bcl_table_t t);
@@ -177,11 +182,14 @@ bcl_status_t bcl_comm_set_table(bcl_comm_t c, bcl_table_t t);
  * chunks c with c % (lanes / Q) == l / Q. */
 bcl_status_t bcl_comm_plan(bcl_comm_t c, const bcl_config_t* config, int root, uint64_t bytes, int* slices,
                            uint64_t* slice_bytes, uint32_t* n_chunks, int* ctas);
-/* Pipelined-chain transport protocol: 0 auto (LL lines up to the group's LL
- * chain cap, BCL_LL_CHAIN_MAX, default 8 MiB; above it the table's measured
- * "# bcl-push-from" rule), 1 pull (consumers load from the upstream buffer),
- * 2 push (producers store into the downstream buffer), 3 LL (flagged 16-byte
- * lines forwarded hop by hop; fails above the cap). */
+/* Pipelined-chain transport protocol: 0 auto (line protocols up to their
+ * caps -- LL128 when every rank has its own GPU, up to the table's measured
+ * "# bcl-ll128-upto" rule and BCL_LL128_MAX, default 128 MiB, else LL,
+ * BCL_LL_CHAIN_MAX, default 8 MiB -- and above them the table's measured
+ * "# bcl-push-from" rule), 1 pull (consumers load from the
+ * upstream buffer), 2 push (producers store into the downstream buffer),
+ * 3 LL (flagged 16-byte lines forwarded hop by hop), 4 LL128 (128-byte lines,
+ * 120 payload bytes each). 3 and 4 fail above their caps. */
 bcl_status_t bcl_comm_set_protocol(bcl_comm_t c, int protocol);
 /* The config a NULL-config call would run for this size (select + clamp). */
 bcl_status_t bcl_comm_choose(bcl_comm_t c, uint64_t message_bytes, bcl_config_t* out);

@@ -94,6 +94,8 @@ _SIGS = {
     "bcl_comm_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "bcl_comm_connect": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
     "bcl_comm_destroy": (C.c_int, [C.c_void_p]),
+    "bcl_comm_protocol_caps": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                         C.POINTER(C.c_uint64)]),
     "bcl_comm_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
                                 C.POINTER(C.c_int)]),
     "bcl_comm_set_table": (C.c_int, [C.c_void_p, C.c_void_p]),
@@ -377,18 +379,26 @@ def tune(n_list, msg_sizes, candidates, chunk_candidates, startup_s=1e-6, link_B
 def tune_measured(n_list, msg_sizes, candidates, chunk_candidates, cost, provenance="") -> TuningTable:
     """Same brute force with cost(config, n, bytes) -> seconds supplied by a
     measurement (the B200 Measured oracle)."""
+    failure = []
+
     def _cb(cfg_p, n, m, _user):
         try:
             return float(cost(AlgorithmConfig._from(cfg_p.contents), n, m))
-        except Exception:  # noqa: BLE001 - surfaces as BCL_ERR_RUNTIME
+        except Exception as e:  # noqa: BLE001 - surfaces as BCL_ERR_RUNTIME, re-raised below
+            failure.append(e)
             return math.nan
     cb = _COST_FN(_cb)
     h = C.c_void_p()
     nl = (C.c_int * max(len(n_list), 1))(*n_list)
     sz = (C.c_uint64 * max(len(msg_sizes), 1))(*msg_sizes)
     ch = (C.c_uint64 * max(len(chunk_candidates), 1))(*chunk_candidates)
-    _check(lib().bcl_tune_measured(nl, len(n_list), sz, len(msg_sizes), _cands(candidates), len(candidates),
-                                   ch, len(chunk_candidates), cb, None, provenance.encode(), C.byref(h)))
+    try:
+        _check(lib().bcl_tune_measured(nl, len(n_list), sz, len(msg_sizes), _cands(candidates), len(candidates),
+                                       ch, len(chunk_candidates), cb, None, provenance.encode(), C.byref(h)))
+    except BclError as e:
+        if failure:
+            raise failure[0] from e
+        raise
     return TuningTable(h)
 
 

@@ -109,6 +109,12 @@ class Comm:
         _check(lib().bcl_comm_info(self._h, C.byref(n), C.byref(r), C.byref(d), C.byref(l)))
         return {"n": n.value, "rank": r.value, "device": d.value, "lanes": l.value}
 
+    def protocol_caps(self):
+        """Largest message (bytes, 0 = unavailable) per line protocol."""
+        d, c, l128 = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(lib().bcl_comm_protocol_caps(self._h, C.byref(d), C.byref(c), C.byref(l128)))
+        return {"ll_direct": d.value, "ll_chain": c.value, "ll128": l128.value}
+
     @property
     def n_ranks(self) -> int:
         return self.info()["n"]
@@ -128,8 +134,8 @@ class Comm:
         return {"slices": q.value, "slice_bytes": sb.value, "n_chunks": nc.value, "ctas": ctas.value}
 
     def set_protocol(self, protocol) -> None:
-        """Chain transport: "auto" (LL up to the LL chain cap, then the table rule), "pull", "push" or "ll"."""
-        code = {"auto": 0, "pull": 1, "push": 2, "ll": 3}[protocol] if isinstance(protocol, str) else int(protocol)
+        """Chain transport: "auto" (LL128/LL up to their caps, then the table rule), "pull", "push", "ll" or "ll128"."""
+        code = {"auto": 0, "pull": 1, "push": 2, "ll": 3, "ll128": 4}[protocol] if isinstance(protocol, str) else int(protocol)
         _check(lib().bcl_comm_set_protocol(self._h, code))
 
     def choose(self, message_bytes: int) -> AlgorithmConfig:

@@ -397,6 +397,16 @@ bcl_status_t bcl_comm_info(bcl_comm_t c, int* n, int* rank, int* device, int* la
   });
 }
 
+bcl_status_t bcl_comm_protocol_caps(bcl_comm_t c, uint64_t* ll_direct_max, uint64_t* ll_chain_max,
+                                    uint64_t* ll128_max) {
+  return guard([&] {
+    need(c, "comm");
+    if (ll_direct_max) *ll_direct_max = c->g->ll_direct_max();
+    if (ll_chain_max) *ll_chain_max = c->g->ll_chain_max();
+    if (ll128_max) *ll128_max = c->g->ll128_max();
+  });
+}
+
 bcl_status_t bcl_comm_set_table(bcl_comm_t c, bcl_table_t t) {
   return guard([&] {
     need(c, "comm");

@@ -25,6 +25,8 @@ struct ExportInfo {
   std::uint64_t heap_bytes;
   std::uint64_t ll_max;        // LL landing-area geometry must agree across ranks
   std::uint64_t ll_chain_max;
+  std::uint64_t ll128_max;
+  cudaUUID_t uuid;             // physical GPU identity (ordinals differ between processes)
   cudaIpcMemHandle_t region;
   cudaIpcMemHandle_t heap;
 };
@@ -80,6 +82,7 @@ GroupOptions GroupOptions::from_env() {
   if (const char* v = std::getenv("BCL_PROTOCOL")) o.protocol = std::atoi(v);
   if (const char* v = std::getenv("BCL_LL_MAX")) o.ll_max_bytes = std::strtoull(v, nullptr, 10);
   if (const char* v = std::getenv("BCL_LL_CHAIN_MAX")) o.ll_chain_max_bytes = std::strtoll(v, nullptr, 10);
+  if (const char* v = std::getenv("BCL_LL128_MAX")) o.ll128_max_bytes = std::strtoll(v, nullptr, 10);
   if (const char* v = std::getenv("BCL_HOST_PIECE")) o.host_piece = std::max<std::uint64_t>(4096, std::strtoull(v, nullptr, 10));
   if (const char* v = std::getenv("BCL_STAGES")) o.stages = static_cast<std::uint32_t>(std::clamp(std::atoi(v), 2, dev::kMaxStages));
   if (const char* v = std::getenv("BCL_STAGE_BYTES")) o.stage_bytes = static_cast<std::int64_t>(std::strtoul(v, nullptr, 10)) / 16 * 16;
@@ -170,6 +173,11 @@ std::uint64_t ll_chain_cap(const GroupOptions& opt) {
                                                    : opt.ll_chain_max_bytes;
   return static_cast<std::uint64_t>(std::min<std::int64_t>(v, 64ll << 20)) / 16 * 16;
 }
+std::uint64_t ll128_cap(const GroupOptions& opt) {
+  const std::int64_t v = opt.ll128_max_bytes < 0 ? static_cast<std::int64_t>(dev::kLL128MaxBytes)
+                                                 : opt.ll128_max_bytes;
+  return static_cast<std::uint64_t>(std::clamp<std::int64_t>(v, 0, 256ll << 20));
+}
 
 }  // namespace
 
@@ -218,8 +226,10 @@ std::shared_ptr<Group> Group::create_local(const std::vector<int>& devices, cons
   }
   g->lanes_alloc_ = g->lanes_;
   g->single_device_ = g->by_device_.size() == 1;
+  g->ll128_ok_ = n >= 2 && static_cast<int>(g->by_device_.size()) == n;
   g->ll_max_ = ll_cap(n, opt);
   g->ll_chain_max_ = ll_chain_cap(opt);
+  g->ll128_max_ = ll128_cap(opt);
   g->local_.resize(static_cast<std::size_t>(n));
   for (int r = 0; r < n; ++r) {
     LocalRank& lr = g->local_[static_cast<std::size_t>(r)];
@@ -259,6 +269,7 @@ std::shared_ptr<Group> Group::create_rank(int n, int rank, int device, std::size
   g->lanes_alloc_ = g->lanes_;
   g->ll_max_ = ll_cap(n, opt);
   g->ll_chain_max_ = ll_chain_cap(opt);
+  g->ll128_max_ = ll128_cap(opt);
   g->local_.resize(1);
   g->local_[0].rank = rank;
   g->local_[0].device = device;
@@ -282,6 +293,12 @@ std::vector<std::uint8_t> Group::export_info() const {
   info.heap_bytes = r.heap_bytes;
   info.ll_max = ll_max_;
   info.ll_chain_max = ll_chain_max_;
+  info.ll128_max = ll128_max_;
+  {
+    cudaDeviceProp prop{};
+    ck(cudaGetDeviceProperties(&prop, r.device), "cudaGetDeviceProperties");
+    info.uuid = prop.uuid;
+  }
   ck(cudaIpcGetMemHandle(&info.region, r.region), "cudaIpcGetMemHandle(region)");
   if (r.heap) ck(cudaIpcGetMemHandle(&info.heap, r.heap), "cudaIpcGetMemHandle(heap)");
   std::vector<std::uint8_t> out(sizeof info);
@@ -301,12 +318,18 @@ void Group::connect(const std::vector<std::vector<std::uint8_t>>& infos) {
     if (all[i].magic != kInfoMagic || all[i].n != n_ || all[i].rank != static_cast<int>(i)) {
       throw std::invalid_argument("info blobs must be ordered by rank and belong to this group");
     }
-    if (all[i].ll_max != ll_max_ || all[i].ll_chain_max != ll_chain_max_) {
-      throw std::invalid_argument("ranks disagree on the LL landing areas (BCL_LL_MAX / BCL_LL_CHAIN_MAX)");
+    if (all[i].ll_max != ll_max_ || all[i].ll_chain_max != ll_chain_max_ || all[i].ll128_max != ll128_max_) {
+      throw std::invalid_argument("ranks disagree on the LL landing areas (BCL_LL_MAX / _CHAIN_MAX / LL128_MAX)");
     }
     lanes = std::min(lanes, static_cast<int>(all[i].lanes));
   }
   lanes_ = lanes;
+  ll128_ok_ = n_ >= 2;
+  for (std::size_t i = 0; i < all.size(); ++i) {
+    for (std::size_t j = 0; j < i; ++j) {
+      if (std::memcmp(&all[i].uuid, &all[j].uuid, sizeof(cudaUUID_t)) == 0) ll128_ok_ = false;
+    }
+  }
   LocalRank& me = local_[0];
   DeviceScope ds(me.device);
   const std::size_t S = region_stride();
@@ -378,8 +401,8 @@ void Group::set_table(const TuningTable& t) {
 void Group::clear_table() { have_table_ = false; }
 
 void Group::set_protocol(int protocol) {
-  if (protocol < 0 || protocol > 3) {
-    throw std::invalid_argument("protocol must be 0 (auto), 1 (pull), 2 (push) or 3 (ll)");
+  if (protocol < 0 || protocol > 4) {
+    throw std::invalid_argument("protocol must be 0 (auto), 1 (pull), 2 (push), 3 (ll) or 4 (ll128)");
   }
   opt_.protocol = protocol;
 }
@@ -388,25 +411,33 @@ void Group::set_protocol(int protocol) {
 // table records from which size on it wins.
 bool Group::use_push(const CallPlan& p, std::uint64_t bytes) const {
   if (!p.implicit_chain || n_ < 2) return false;
-  if (opt_.protocol == 1 || opt_.protocol == 3) return false;
+  if (opt_.protocol == 1 || opt_.protocol >= 3) return false;
   if (opt_.protocol == 2) return true;
   return select_push(table(), n_, bytes);
 }
-// LL chain: every pipelined chain up to ll_chain_max_ in auto mode (the
-// measured table decides between it and the other schedules), or on request.
-// Provenance / timeline recording need the lane executor.
-bool Group::use_ll_chain(const CallPlan& p, std::uint64_t bytes, const std::vector<int>& locals) const {
-  if (!p.implicit_chain || n_ < 2 || !opt_.ll || bytes == 0) return false;
-  if (opt_.protocol == 1 || opt_.protocol == 2) return false;
+// Line protocols for the pipelined chain in auto mode: LL128 (cross-GPU hops
+// only) up to ll128_max_, else 16-byte LL lines up to ll_chain_max_ (the
+// measured table decides between the chain and the other schedules); above
+// them the lane executor. Provenance / timeline recording need the lane
+// executor. Returns 0 (lane executor), 1 (LL) or 2 (LL128).
+int Group::ll_chain_mode(const CallPlan& p, std::uint64_t bytes, const std::vector<int>& locals) const {
+  if (!p.implicit_chain || n_ < 2 || !opt_.ll || bytes == 0) return 0;
+  if (opt_.protocol == 1 || opt_.protocol == 2) return 0;
   for (int li : locals) {
     const LocalRank& r = local_[static_cast<std::size_t>(li)];
-    if (r.prov != nullptr || r.trace != nullptr) return false;
+    if (r.prov != nullptr || r.trace != nullptr) return 0;
   }
-  if (bytes > ll_chain_max_) {
-    if (opt_.protocol == 3) throw std::invalid_argument("message exceeds the LL chain landing area");
-    return false;
+  if (opt_.protocol == 3) {
+    if (bytes > ll_chain_max_) throw std::invalid_argument("message exceeds the LL chain landing area");
+    return 1;
   }
-  return true;
+  if (opt_.protocol == 4) {
+    if (!ll128_ok_) throw std::invalid_argument("LL128 needs every rank on its own GPU");
+    if (bytes > ll128_max_) throw std::invalid_argument("message exceeds the LL128 chain landing area");
+    return 2;
+  }
+  if (ll128_ok_ && bytes <= ll128_max_ && select_ll128(table(), n_, bytes)) return 2;
+  return bytes <= ll_chain_max_ ? 1 : 0;
 }
 const TuningTable& Group::table() const { return have_table_ ? table_ : builtin_table(); }
 
@@ -534,22 +565,30 @@ void Group::fill_rank_work(dev::RankWork& w, LocalRank& r, const CallPlan& p, vo
 }
 
 void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& bufs, std::uint64_t bytes,
-                      int root, cudaStream_t stream, bool chain) {
+                      int root, cudaStream_t stream, int mode) {
+  const bool chain = mode != 0;
   dev::LLParams P{};
   P.n_ranks = n_;
   P.root = root;
   P.n_local = static_cast<int>(locals.size());
   P.bytes = bytes;
-  P.lines = static_cast<std::uint32_t>((bytes + 7) / 8);
+  P.lines = static_cast<std::uint32_t>(mode == 2 ? (bytes + dev::kLL128Payload - 1) / dev::kLL128Payload
+                                                  : (bytes + 7) / 8);
   P.area_lines = static_cast<std::uint32_t>(ll_max_ / 8);
-  P.chain = chain ? 1 : 0;
+  P.chain = static_cast<std::uint32_t>(mode);
   P.chain_lines = static_cast<std::uint32_t>(ll_chain_max_ / 8);
+  P.chain128_lines = ll128_lines();
+  P.chain128_area = ll128_area();
   // ~4 lines per thread, at most kLLMaxCtas CTAs per rank
   // ~2 lines per thread; ranks sharing a GPU must stay co-resident
   // (cooperative launch): at most 4 LL CTAs per SM in total.
   const int resident = std::max(1, 148 * 4 / std::max<int>(1, P.n_local));
   P.ctas = std::clamp<int>(static_cast<int>((P.lines + 2 * dev::kLLThreads - 1) / (2 * dev::kLLThreads)), 1,
                            std::min(dev::kLLMaxCtas, resident));
+  if (mode == 2) {  // a warp moves 4 lines per step: ~2 steps per warp, up to one CTA per SM
+    const std::uint32_t per_cta = dev::kLLThreads / 32 * 4 * 2;
+    P.ctas = std::clamp<int>(static_cast<int>((P.lines + per_cta - 1) / per_cta), 1, dev::kLL128MaxCtas);
+  }
   P.timeout_ns = opt_.timeout_ns;
   const std::size_t S = region_stride();
   std::uint64_t epoch = 0;
@@ -596,11 +635,11 @@ void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& 
 void Group::launch_group(const std::vector<int>& locals, const std::vector<void*>& bufs,
                          std::uint64_t bytes, int root, const CallPlan& p, cudaStream_t stream) {
   if (p.config.algorithm == Algorithm::Direct && bytes <= ll_max_ && opt_.ll) {
-    launch_ll(locals, bufs, bytes, root, stream, false);
+    launch_ll(locals, bufs, bytes, root, stream, 0);
     return;
   }
-  if (use_ll_chain(p, bytes, locals)) {
-    launch_ll(locals, bufs, bytes, root, stream, true);
+  if (const int mode = ll_chain_mode(p, bytes, locals)) {
+    launch_ll(locals, bufs, bytes, root, stream, mode);
     return;
   }
   dev::LaunchParams P{};
@@ -654,7 +693,9 @@ void Group::bcast(int li, void* buf, std::uint64_t bytes, int root, const Algori
   if (ipc_ && bytes > 0) {
     const auto* b = static_cast<std::uint8_t*>(buf);
     if (b < r.heap || b + bytes > r.heap + r.heap_bytes) {
-      throw std::invalid_argument("per-process ranks need buffers from bcl_mem_alloc");
+      throw std::invalid_argument("per-process ranks need buffers from bcl_mem_alloc (buffer offset " +
+                                  std::to_string(static_cast<long long>(b - r.heap)) + " + " + std::to_string(bytes) +
+                                  " bytes, heap " + std::to_string(r.heap_bytes) + " bytes)");
     }
   }
   const AlgorithmConfig c = choose(bytes, cfg);

@@ -83,6 +83,7 @@ struct GroupOptions {
   int protocol = 0;                                         // chain: 0 auto (table), 1 pull, 2 push
   std::uint64_t ll_max_bytes = 0;                           // LL threshold (0 = 2 MiB, lowered for many ranks)
   std::int64_t ll_chain_max_bytes = -1;                     // LL pipelined chain up to this size (-1 = default)
+  std::int64_t ll128_max_bytes = -1;                        // LL128 pipelined chain up to this size (-1 = default)
   std::uint64_t host_piece = 4ull << 20;                    // host-buffer calls: H2D/bcast/D2H pipeline piece
   std::int64_t stage_bytes = -1;                            // bulk-copy stage per warp: 0 = vector loads,
                                                             // -1 = auto (8 KiB across GPUs, 0 on one GPU)
@@ -147,13 +148,17 @@ class Group {
 
   int n_ranks() const { return n_; }
   int lanes() const { return lanes_; }
+  // Line-protocol landing-area caps (bytes) and whether LL128 is available.
+  std::uint64_t ll_direct_max() const { return opt_.ll ? ll_max_ : 0; }
+  std::uint64_t ll_chain_max() const { return opt_.ll ? ll_chain_max_ : 0; }
+  std::uint64_t ll128_max() const { return opt_.ll && ll128_ok_ ? ll128_max_ : 0; }
   bool ipc() const { return ipc_; }
   int local_count() const { return static_cast<int>(local_.size()); }
   LocalRank& local(int i) { return local_.at(static_cast<std::size_t>(i)); }
   int local_index_of(int rank) const;
 
   void set_table(const TuningTable& t);
-  void set_protocol(int protocol);  // 0 auto (LL chain, then the table's push-from rule), 1 pull, 2 push, 3 LL
+  void set_protocol(int protocol);  // 0 auto (LL128/LL chain, then the table's push-from rule), 1 pull, 2 push, 3 LL, 4 LL128
   void clear_table();
   const TuningTable& table() const;
   AlgorithmConfig choose(std::uint64_t bytes, const AlgorithmConfig* cfg) const;
@@ -191,9 +196,9 @@ class Group {
   cudaEvent_t event(LocalRank& r, std::size_t i);
   void ensure_scratch(int local_index, std::uint64_t bytes);
   void launch_ll(const std::vector<int>& locals, const std::vector<void*>& bufs, std::uint64_t bytes, int root,
-                 cudaStream_t stream, bool chain);
+                 cudaStream_t stream, int mode);
   void raise_errors(const std::vector<int>& locals);
-  bool use_ll_chain(const CallPlan& p, std::uint64_t bytes, const std::vector<int>& locals) const;
+  int ll_chain_mode(const CallPlan& p, std::uint64_t bytes, const std::vector<int>& locals) const;
   std::size_t region_stride() const { return static_cast<std::size_t>(n_) * lanes_; }
   // Offset (in 8-byte words) of the LL landing area for a flag stride of L lanes.
   std::size_t ll_offset(int lanes) const {
@@ -202,8 +207,21 @@ class Group {
   }
   std::uint64_t ll_max_{dev::kLLMaxBytes};  // LL protocol threshold (bytes), direct schedule
   std::uint64_t ll_chain_max_{0};           // LL pipelined chain up to this size (0 = off)
-  std::size_t ll_words() const {            // 8-byte words of LL landing areas per rank
-    return (static_cast<std::size_t>(n_) * 2 * (ll_max_ / 8) + 2 * (ll_chain_max_ / 8)) * 2;
+  std::uint64_t ll128_max_{0};              // LL128 pipelined chain up to this size (0 = off)
+  bool ll128_ok_{false};                    // every rank on its own GPU (LL128 needs NVLink hops)
+  std::uint32_t ll128_lines() const {
+    return static_cast<std::uint32_t>((ll128_max_ + dev::kLL128Payload - 1) / dev::kLL128Payload);
+  }
+  // LL128 area offset from the LL base (16-byte units), 128-byte aligned given
+  // a 256-byte aligned region.
+  std::uint32_t ll128_area() const {
+    const std::size_t units = static_cast<std::size_t>(n_) * 2 * (ll_max_ / 8) + 2 * (ll_chain_max_ / 8);
+    const std::size_t base_bytes = ll_offset(lanes_) * 8 + units * 16;
+    return static_cast<std::uint32_t>(units + ((128 - base_bytes % 128) % 128) / 16);
+  }
+  std::size_t ll_words() const {            // 8-byte words of LL landing areas per rank (+ alignment pad)
+    return (static_cast<std::size_t>(n_) * 2 * (ll_max_ / 8) + 2 * (ll_chain_max_ / 8)) * 2 +
+           static_cast<std::size_t>(2) * ll128_lines() * 16 + 16;
   }
 
   int n_{0};

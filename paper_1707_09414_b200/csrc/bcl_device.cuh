@@ -31,6 +31,9 @@ constexpr int kThreads = (kWarpsPerCta + 1) * 32;  // + one publisher warp
 constexpr int kMaxStages = 4;    // bulk-copy stages per copy warp
 constexpr std::uint32_t kLLMaxBytes = 2048 * 1024;      // largest LL message (per-group cap may be lower)
 constexpr std::uint32_t kLLChainMaxBytes = 8u << 20;     // default LL pipelined-chain cap
+constexpr std::uint32_t kLL128MaxBytes = 128u << 20;     // default LL128 pipelined-chain cap
+constexpr std::uint32_t kLL128Payload = 120;             // payload bytes per 128-byte LL128 line
+constexpr int kLL128MaxCtas = 148;
 constexpr int kLLThreads = 512;
 constexpr int kLLMaxCtas = 64;                          // CTAs per rank for one LL call
 
@@ -151,8 +154,10 @@ struct LLParamsT {
   std::uint64_t epoch;
   std::uint32_t half;
   std::uint32_t area_lines;   // lines per (source, half) landing area of the direct schedule
-  std::uint32_t chain;        // 1: pipelined chain (rank l forwards every line to l + 1)
+  std::uint32_t chain;        // 0 direct, 1 pipelined chain on 16-byte LL lines, 2 chain on 128-byte LL128 lines
   std::uint32_t chain_lines;  // lines per half of the chain landing area (after the direct areas)
+  std::uint32_t chain128_lines;  // 128-byte lines per half of the LL128 chain area
+  std::uint32_t chain128_area;   // its offset from the LL base in 16-byte units (128-byte aligned)
   std::uint64_t timeout_ns;
   LLRank ranks[NL];
 };

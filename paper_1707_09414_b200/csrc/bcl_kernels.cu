@@ -920,6 +920,128 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ 
   }
 }
 
+// LL128 pipelined chain (cross-GPU hops only). A 128-byte line carries 120
+// payload bytes and the epoch in its last 8 bytes; eight threads own one line
+// (16 bytes each) and a warp moves four lines per instruction. Like NCCL's
+// LL128 this relies on NVLink delivering each 128-byte warp-coalesced store
+// as one unit: a reader that sees the new epoch in a line's flag word sees
+// the whole line. Readers vote per warp and reload until all four flags match.
+__device__ __forceinline__ void st_volatile_v2u64(ulonglong2* p, unsigned long long a, unsigned long long b) {
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1,%2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ ulonglong2 ld_volatile_v2u64(const ulonglong2* p) {
+  ulonglong2 v;
+  asm volatile("ld.volatile.global.v2.u64 {%0,%1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+  return v;
+}
+// Bytes [off, off + len) of buf (len <= 8) as a little-endian word; the fast
+// path needs 8-byte alignment of buf + off.
+__device__ __forceinline__ unsigned long long ll128_get(const std::uint8_t* buf, std::uint64_t off, std::uint32_t len,
+                                                        bool aligned) {
+  if (len == 8 && aligned) return *reinterpret_cast<const unsigned long long*>(buf + off);
+  unsigned long long v = 0;
+  for (std::uint32_t b = 0; b < len; ++b) v |= static_cast<unsigned long long>(buf[off + b]) << (8 * b);
+  return v;
+}
+__device__ __forceinline__ void ll128_put(std::uint8_t* buf, std::uint64_t off, std::uint32_t len, bool aligned,
+                                          unsigned long long v) {
+  if (len == 8 && aligned) {
+    *reinterpret_cast<unsigned long long*>(buf + off) = v;
+    return;
+  }
+  for (std::uint32_t b = 0; b < len; ++b) buf[off + b] = static_cast<std::uint8_t>(v >> (8 * b));
+}
+
+__global__ void __launch_bounds__(kLLThreads) ll128_kernel(const __grid_constant__ LLParamsT<1> P) {
+  const LLRank& R = P.ranks[0];
+  const int lane = static_cast<int>(threadIdx.x & 31);
+  const int part = lane & 7;  // 16-byte piece of the line
+  const int sub = lane >> 3;  // line within the warp's group of four
+  const std::uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const std::uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  const unsigned long long flag = P.epoch;
+  const int n = P.n_ranks;
+  const int logical = (R.rank - P.root + n) % n;
+  const int next = (R.rank + 1) % n;
+  const bool writer = logical + 1 < n;
+  const std::size_t area = P.chain128_area + static_cast<std::size_t>(P.half) * P.chain128_lines * 8;
+  if (writer) {
+    const int t = static_cast<int>(threadIdx.x);
+    if (t < n && R.need[t] > 0) {
+      const std::uint64_t t0 = globaltimer();
+      std::uint64_t v;
+      while ((v = ld_relaxed_sys(R.credit + t)) < R.need[t]) {
+        if (globaltimer() - t0 > P.timeout_ns) {
+          ll_fail(R, t, 0, v, R.need[t]);
+          break;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  const bool aligned = (reinterpret_cast<std::uintptr_t>(R.buf) & 7u) == 0;
+  auto piece = [&](std::uint32_t line, std::uint64_t* off, std::uint32_t* len0, std::uint32_t* len1) {
+    // payload bytes of this thread: [off, off + len0) -> word 0, [off + 8, ... + len1) -> word 1
+    *off = static_cast<std::uint64_t>(line) * kLL128Payload + static_cast<std::uint64_t>(part) * 16;
+    const std::uint64_t end = static_cast<std::uint64_t>(line) * kLL128Payload + kLL128Payload;
+    const std::uint64_t lim = end < P.bytes ? end : P.bytes;
+    auto clip = [&](std::uint64_t a) -> std::uint32_t { return a >= lim ? 0u : static_cast<std::uint32_t>(lim - a < 8 ? lim - a : 8); };
+    *len0 = clip(*off);
+    *len1 = part == 7 ? 0u : clip(*off + 8);
+  };
+  uint4* const base_self = R.ll + area;
+  if (logical == 0) {
+    ulonglong2* dst = reinterpret_cast<ulonglong2*>(R.peers->ll[next] + area);
+    for (std::uint32_t g = warp; g * 4 < P.lines; g += warps) {
+      const std::uint32_t line = g * 4 + sub;
+      if (line >= P.lines) continue;
+      std::uint64_t off;
+      std::uint32_t l0, l1;
+      piece(line, &off, &l0, &l1);
+      const unsigned long long a = ll128_get(R.buf, off, l0, aligned);
+      const unsigned long long b = part == 7 ? flag : ll128_get(R.buf, off + 8, l1, aligned);
+      st_volatile_v2u64(dst + static_cast<std::size_t>(line) * 8 + part, a, b);
+    }
+    return;
+  }
+  const ulonglong2* src = reinterpret_cast<const ulonglong2*>(base_self);
+  ulonglong2* fwd = writer ? reinterpret_cast<ulonglong2*>(R.peers->ll[next] + area) : nullptr;
+  const int source = (R.rank + n - 1) % n;
+  bool ok = true;
+  for (std::uint32_t g = warp; g * 4 < P.lines && ok; g += warps) {
+    const std::uint32_t line = g * 4 + sub;
+    const bool active = line < P.lines;
+    ulonglong2 v = make_ulonglong2(0, 0);
+    const std::uint64_t t0 = globaltimer();
+    unsigned spins = 0;
+    while (true) {
+      if (active) v = ld_volatile_v2u64(src + static_cast<std::size_t>(line) * 8 + part);
+      const bool stale = active && part == 7 && v.y != flag;
+      if (!__any_sync(0xffffffffu, stale)) break;
+      if ((++spins & 1023u) == 0) {
+        const int give_up = (*(volatile int*)R.abort != 0 || globaltimer() - t0 > P.timeout_ns) ? 1 : 0;
+        if (__any_sync(0xffffffffu, give_up)) {
+          if (lane == 0 && *(volatile int*)R.abort == 0) ll_fail(R, source, line, 0, flag);
+          ok = false;
+          break;
+        }
+      }
+    }
+    if (!ok) break;
+    if (!active) continue;
+    if (fwd != nullptr) st_volatile_v2u64(fwd + static_cast<std::size_t>(line) * 8 + part, v.x, v.y);
+    std::uint64_t off;
+    std::uint32_t l0, l1;
+    piece(line, &off, &l0, &l1);
+    ll128_put(R.buf, off, l0, aligned, v.x);
+    if (part != 7) ll128_put(R.buf, off + 8, l1, aligned, v.y);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && ok) {
+    if (atomicAdd(R.done, 1ull) + 1 == R.done_target) st_relaxed_sys(R.peers->credit[source] + R.rank, P.epoch);
+  }
+}
+
 // All-ranks barrier: rank r bumps slot [r] in every peer, then waits for
 // every peer's bump in its own slots.
 __global__ void barrier_kernel(const __grid_constant__ BarrierParams B) {
@@ -1003,6 +1125,14 @@ int launch_barrier(const dev::BarrierParams& p, void* stream) {
 }
 
 int launch_ll(const dev::LLParams& p, void* stream) {
+  if (p.chain == 2) {  // LL128: one rank per GPU by construction
+    if (p.n_local != 1) return static_cast<int>(cudaErrorInvalidValue);
+    dev::LLParamsT<1> one;
+    std::memcpy(&one, &p, offsetof(dev::LLParams, ranks));
+    one.ranks[0] = p.ranks[0];
+    dev::ll128_kernel<<<static_cast<unsigned>(p.ctas), dev::kLLThreads, 0, static_cast<cudaStream_t>(stream)>>>(one);
+    return static_cast<int>(cudaGetLastError());
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(p.n_local * p.ctas));
   cfg.blockDim = dim3(dev::kLLThreads);

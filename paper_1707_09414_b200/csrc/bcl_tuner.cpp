@@ -22,6 +22,7 @@ constexpr std::string_view kColumns =
 constexpr std::string_view kPragma = "# oracle:";
 constexpr std::string_view kMeasuredPragma = "# bcl-oracle: measured";
 constexpr std::string_view kPushPragma = "# bcl-push-from:";
+constexpr std::string_view kLL128Pragma = "# bcl-ll128-upto:";
 
 // Rounded geometric mean of two sizes (tuner.cpp:27-31).
 std::uint64_t geo_mid(std::uint64_t a, std::uint64_t b) {
@@ -228,6 +229,18 @@ bool select_push(const TuningTable& t, int n, std::uint64_t m) {
   return best_n >= 0 && m >= from;
 }
 
+bool select_ll128(const TuningTable& t, int n, std::uint64_t m) {
+  int best_n = -1;
+  std::uint64_t upto = 0;
+  for (const auto& [pn, bytes] : t.ll128_upto) {
+    if (pn <= n && pn > best_n) {
+      best_n = pn;
+      upto = bytes;
+    }
+  }
+  return best_n < 0 || m <= upto;  // no rule: up to the group's LL128 cap
+}
+
 TableParseError::TableParseError(std::size_t line, const std::string& what)
     : std::runtime_error("line " + std::to_string(line) + ": " + what), line_(line) {}
 
@@ -242,6 +255,10 @@ std::string save_table_text(const TuningTable& t) {
   s.append("\n");
   for (const auto& [pn, bytes] : t.push_from) {
     s.append(kPushPragma).append(" n=").append(std::to_string(pn)).append(" bytes=").append(std::to_string(bytes));
+    s.append("\n");
+  }
+  for (const auto& [pn, bytes] : t.ll128_upto) {
+    s.append(kLL128Pragma).append(" n=").append(std::to_string(pn)).append(" bytes=").append(std::to_string(bytes));
     s.append("\n");
   }
   s.append(kColumns).append("\n");
@@ -319,6 +336,15 @@ TuningTable load_table(std::istream& in) {
         throw TableParseError(no, "bad push pragma");
       }
       t.push_from.emplace_back(pn, static_cast<std::uint64_t>(bytes));
+      continue;
+    }
+    if (line.rfind(kLL128Pragma, 0) == 0) {
+      int pn = 0;
+      unsigned long long bytes = 0;
+      if (std::sscanf(line.c_str() + kLL128Pragma.size(), " n=%d bytes=%llu", &pn, &bytes) != 2 || pn < 1) {
+        throw TableParseError(no, "bad ll128 pragma");
+      }
+      t.ll128_upto.emplace_back(pn, static_cast<std::uint64_t>(bytes));
       continue;
     }
     if (line.rfind(kMeasuredPragma, 0) == 0) {

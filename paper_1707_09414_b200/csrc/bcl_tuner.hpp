@@ -65,6 +65,10 @@ struct TuningTable {
   // consumers pulling. Stored as "# bcl-push-from: n=<n> bytes=<b>" lines,
   // which the reference load_table skips as comments.
   std::vector<std::pair<int, std::uint64_t>> push_from;
+  // LL128 line protocol for chain_pipelined up to this many bytes at this
+  // rank count ("# bcl-ll128-upto: n=<n> bytes=<b>", also a comment to the
+  // reference loader); without a rule, up to the group's LL128 cap.
+  std::vector<std::pair<int, std::uint64_t>> ll128_upto;
   bool operator==(const TuningTable& o) const {
     return oracle == o.oracle && entries == o.entries;
   }
@@ -96,6 +100,8 @@ AlgorithmConfig select(const TuningTable& table, int n,
                        std::uint64_t message_bytes);
 // Whether a chain_pipelined call of this size should use the push protocol.
 bool select_push(const TuningTable& table, int n, std::uint64_t message_bytes);
+// Whether a chain_pipelined call of this size may use LL128 lines.
+bool select_ll128(const TuningTable& table, int n, std::uint64_t message_bytes);
 
 class TableParseError : public std::runtime_error {
  public:

@@ -167,6 +167,7 @@ def test_measured_tables_load_in_the_reference():
     # the push-protocol rule rides in a comment line the reference skips
     lines = text.splitlines()
     lines.insert(1, "# bcl-push-from: n=4 bytes=268435456")
+    lines.insert(2, "# bcl-ll128-upto: n=2 bytes=33554432")
     text = "\n".join(lines) + "\n"
     t = B.load_table_text(text)
     assert t.text() == text

@@ -51,16 +51,59 @@ def test_one_process_all_gpus_every_algorithm_and_root():
     devices = list(range(min(ngpu(), 8)))
     comms = B.Comm.local(devices, timeout_s=10)
     rng = random.Random(17)
-    for algo in ("chain_pipelined", "chain_pipelined/pull", "knomial", "scatter_ring_allgather", "direct", "chain"):
+    for algo in ("chain_pipelined", "chain_pipelined/ll", "chain_pipelined/pull", "knomial",
+                 "scatter_ring_allgather", "direct", "chain"):
         algo, _, protocol = algo.partition("/")
         for c in comms:
-            c.set_protocol(protocol or "auto")  # auto: LL lines up to 8 MiB; pull: the lane executor
+            c.set_protocol(protocol or "auto")  # auto: LL128 lines up to 32 MiB; pull: the lane executor
         for root in range(len(devices)):
-            for m in (0, 4, 4097, 1 << 20, rng.randrange(1, 5 << 20), (8 << 20) + 5):
+            big = (8 << 20) - 3 if protocol == "ll" else (8 << 20) + 5  # the LL chain cap is 8 MiB
+            for m in (0, 4, 4097, 1 << 20, rng.randrange(1, 5 << 20), big):
                 run_group(comms, devices, algo, root, m, chunk=max(1, m // 5 + 3), seed=m + root)
     for c in comms:
         c.set_protocol("auto")
     run_group(comms, devices, "chain_pipelined", 0, 64 << 20, chunk=512 << 10, seed=5)
+
+
+@needs2
+def test_ll128_chain_back_to_back_stress():
+    """LL128 relies on 128-byte NVLink stores arriving whole: many calls back
+    to back with fresh payloads, every size class, roots rotating, every
+    result checked before the next call reuses the landing halves."""
+    devices = list(range(min(ngpu(), 8)))
+    n = len(devices)
+    old = os.environ.get("BCL_LL128_MAX")
+    os.environ["BCL_LL128_MAX"] = str(32 << 20)
+    try:
+        comms = B.Comm.local(devices, timeout_s=10)
+    finally:
+        if old is None:
+            os.environ.pop("BCL_LL128_MAX")
+        else:
+            os.environ["BCL_LL128_MAX"] = old
+    for c in comms:
+        c.set_protocol("ll128")
+    rng = random.Random(23)
+    cap = 32 << 20
+    bufs = [torch.empty(cap + 64, dtype=torch.uint8, device=f"cuda:{d}") for d in devices]
+    sizes = [1, 119, 120, 121, 4096, 1 << 20, (1 << 20) + 7, 5 << 20, cap - 1, cap]
+    for it in range(60):
+        m = sizes[it % len(sizes)] if it < 2 * len(sizes) else rng.randrange(1, cap + 1)
+        root = it % n
+        src = torch.randint(0, 256, (m,), dtype=torch.uint8, device=f"cuda:{devices[root]}")
+        for r in range(n):
+            if r == root:
+                bufs[r][:m].copy_(src)
+            else:
+                bufs[r][:m].fill_(it & 0xFF)
+        torch.cuda.synchronize(devices[root])
+        B.run_bcast(comms, root, [b[:m] for b in bufs], m, cfg_of("chain_pipelined", 262144))
+        for r in range(n):
+            assert torch.equal(bufs[r][:m].cpu(), src.cpu()), (it, m, root, r)
+    with pytest.raises(ValueError):  # above the LL128 landing area
+        B.run_bcast(comms, 0, [b[:cap + 1] for b in bufs], cap + 1, cfg_of("chain_pipelined", 262144))
+    for c in comms:
+        c.set_protocol("auto")
 
 
 @needs2

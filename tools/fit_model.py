@@ -24,6 +24,8 @@ HARNESS = os.path.join(ROOT, "oracle", "_ref", "ref_harness")
 def main():
     raw, seen = [], set()
     for r in csv.DictReader(open(sys.argv[1])):  # first measurement of a point = the default protocol
+        if r.get("protocol", "auto") != "auto":
+            continue
         key = (r["algorithm"], r["radix"], r["chunk_bytes"], r["n"], r["bytes"])
         if key not in seen:
             seen.add(key)

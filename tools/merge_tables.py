@@ -11,7 +11,7 @@ for p in inputs:
     assert t.oracle == "measured", p
     text = open(p).read().splitlines()
     prov.append(text[0][len("# bcl-oracle: measured "):])
-    push += [l for l in text[1:] if l.startswith("# bcl-push-from:")]
+    push += [l for l in text[1:] if l.startswith(("# bcl-push-from:", "# bcl-ll128-upto:"))]
     rows += [l for l in text[1:] if l.strip() and not l.startswith("#") and not l.startswith("n,")]
 rows.sort(key=lambda l: (int(l.split(",")[0]), int(l.split(",")[1])))
 header = "# bcl-oracle: measured " + " | ".join(prov) + "".join("\n" + l for l in push)

@@ -47,6 +47,12 @@ torch.cuda.synchronize()
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 n_eval = [0]
 raw = []
+proto_now = ["auto"]
+
+
+def set_proto(p):
+    proto_now[0] = p
+    comm.set_protocol(p)
 
 
 def quantize(t):
@@ -67,7 +73,10 @@ def cost(cfg, n, m):
             torch.cuda._sleep(400_000)
         comm.barrier(stream)
         ev0.record(stream)
-        comm.bcast(buf, m, "uint8", 0, cfg, stream=stream)
+        try:
+            comm.bcast(buf, m, "uint8", 0, cfg, stream=stream)
+        except Exception as e:
+            raise RuntimeError(f"bcast {cfg} M={m} protocol={proto_now[0]} failed: {e}") from e
         ev1.record(stream)
         ev1.synchronize()
         if it >= 2:
@@ -75,7 +84,7 @@ def cost(cfg, n, m):
     t = torch.tensor(times, dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     med = float(statistics.median(t.cpu().tolist()))
-    raw.append((cfg.algorithm.name, cfg.radix_k, cfg.chunk_bytes, n, m, med))
+    raw.append((cfg.algorithm.name, cfg.radix_k, cfg.chunk_bytes, n, m, med, proto_now[0]))
     return quantize(med)
 
 
@@ -90,7 +99,7 @@ for name in a.cands.split(","):
 chunks = [int(x) for x in a.chunks.split(",")]
 t0 = time.time()
 table = B.tune_measured([world], sizes, cands, chunks, cost,
-                        provenance=f"B200 x{world}, NVLink P2P pulls, median of {a.iters}-{4 * a.iters} "
+                        provenance=f"B200 x{world}, NVLink (LL128 lines, P2P pulls or pushes per rule), median of {a.iters}-{4 * a.iters} "
                                    f"device-timed runs (max over ranks, 2 significant digits), "
                                    f"{time.strftime('%Y-%m-%d')}")
 comm.check(stream)
@@ -106,11 +115,11 @@ if world >= 3:
         if cfg.algorithm != B.Algorithm.chain_pipelined:
             wins.append((m, False))
             continue
-        comm.set_protocol("pull")
+        set_proto("pull")
         t_pull = cost(cfg, world, m)
-        comm.set_protocol("push")
+        set_proto("push")
         t_push = cost(cfg, world, m)
-        comm.set_protocol("auto")
+        set_proto("auto")
         wins.append((m, t_push < t_pull))
         if rank == 0:
             print(f"protocol {m}: pull {t_pull * 1e6:.1f} us push {t_push * 1e6:.1f} us")
@@ -119,10 +128,43 @@ if world >= 3:
             push_from = m
             break
     comm.check(stream)
+
+# Line protocol for the chain: LL128 (cross-GPU, up to the landing-area cap)
+# against the lane executor (pull, or push past the push-from size) at every
+# swept chain size >= 1 MiB. LL128 is used up to the geometric mean of the
+# last size where it wins and the first where it loses ("# bcl-ll128-upto").
+ll128_upto = None
+ll128_cap = comm.protocol_caps()["ll128"]
+if ll128_cap:
+    last_win = None
+    for m in [x for x in sizes if (1 << 20) <= x <= ll128_cap]:
+        cfg = table.select(world, m)
+        if cfg.algorithm != B.Algorithm.chain_pipelined:
+            continue
+        set_proto("ll128")
+        t_ll = cost(cfg, world, m)
+        set_proto("push" if push_from is not None and m >= push_from else "pull")
+        t_lane = cost(cfg, world, m)
+        set_proto("auto")
+        if rank == 0:
+            print(f"line protocol {m}: ll128 {t_ll * 1e6:.1f} us lane executor {t_lane * 1e6:.1f} us")
+        if t_ll <= t_lane:
+            last_win = m
+        else:
+            ll128_upto = int(math.sqrt(last_win * m)) if last_win else 0
+            break
+    if ll128_upto is None:
+        ll128_upto = ll128_cap
+    comm.check(stream)
 text = table.text()
+extra = []
 if push_from is not None:
+    extra.append(f"# bcl-push-from: n={world} bytes={push_from}")
+if ll128_upto is not None:
+    extra.append(f"# bcl-ll128-upto: n={world} bytes={ll128_upto}")
+if extra:
     lines = text.splitlines()
-    lines.insert(1, f"# bcl-push-from: n={world} bytes={push_from}")
+    lines[1:1] = extra
     text = "\n".join(lines) + "\n"
     table = B.load_table_text(text)
 if rank == 0:
@@ -130,7 +172,7 @@ if rank == 0:
     B.save_table(table, a.out)
     if a.raw:
         with open(a.raw, "w") as f:
-            f.write("algorithm,radix,chunk_bytes,n,bytes,seconds\n")
+            f.write("algorithm,radix,chunk_bytes,n,bytes,seconds,protocol\n")
             for r in raw:
                 f.write(",".join(map(str, r)) + "\n")
     print(f"wrote {a.out}: {len(table.entries)} entries from {n_eval[0]} measurements in {time.time() - t0:.1f}s")
