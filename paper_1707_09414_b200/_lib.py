@@ -134,7 +134,12 @@ def lib():
             raise ImportError(f"{path} is missing: build it with `make -C {_HERE}` (no CPU fallback exists)")
         l = C.CDLL(path)
         for name, (res, args) in _SIGS.items():
-            f = getattr(l, name)
+            try:
+                f = getattr(l, name)
+            except AttributeError:
+                if os.environ.get("BCL_LIB"):  # an older experimental build: its missing entry points raise if called
+                    continue
+                raise
             f.restype = res
             f.argtypes = args
         _lib = l

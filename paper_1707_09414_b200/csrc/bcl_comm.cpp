@@ -110,7 +110,6 @@ AggregateRankError::AggregateRankError(std::vector<RankFailure> failures)
 void Group::alloc_rank(LocalRank& r, std::size_t heap_bytes) {
   DeviceScope ds(r.device);
   r.region_bytes = (ll_offset(lanes_alloc_) + ll_words()) * sizeof(std::uint64_t);
-  r.ll_last_to.assign(static_cast<std::size_t>(n_) * 2, 0);
   ck(cudaMalloc(&r.region, r.region_bytes), "cudaMalloc(region)");
   ck(cudaMemset(r.region, 0, r.region_bytes), "cudaMemset(region)");
   ck(cudaMalloc(&r.d_peers, sizeof(dev::PeerTable)), "cudaMalloc(peers)");
@@ -600,24 +599,21 @@ void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& 
     dev::LLRank& w = P.ranks[i];
     w.rank = r.rank;
     w.buf = static_cast<std::uint8_t*>(bufs[i]);
-    w.credit = r.region + 3 * S + static_cast<std::size_t>(n_) + 1;
+    w.credit = r.region + 3 * S + static_cast<std::size_t>(n_) + 1 + (chain ? static_cast<std::size_t>(n_) + 1 : 0);
     w.ll = reinterpret_cast<uint4*>(r.region + ll_offset(lanes_));
     w.peers = r.d_peers;
     w.err = r.err_dev;
     w.abort = reinterpret_cast<int*>(r.region + 3 * S + static_cast<std::size_t>(n_));
     const std::uint32_t half = static_cast<std::uint32_t>(e & 1u);
     const int logical = (r.rank - root + n_) % n_;
-    auto target = [&](int t) {  // this call writes lines into t's landing area
-      std::uint64_t& last = r.ll_last_to[static_cast<std::size_t>(t) * 2 + half];
-      w.need[t] = last;
-      last = e;
-    };
-    if (chain) {
-      if (logical + 1 < n_) target((r.rank + 1) % n_);
-    } else if (logical == 0) {
-      for (int t = 0; t < n_; ++t) {
-        if (t != root) target(t);
-      }
+    // Writers wait for the credits of the last call of the same kind that
+    // wrote this half (direct: every other rank; chain: the successor).
+    std::uint64_t* last = nullptr;
+    if (chain && logical + 1 < n_) last = &r.ll_last_chain[half];
+    if (!chain && logical == 0) last = &r.ll_last_direct[half];
+    if (last != nullptr) {
+      w.need_credit = *last;
+      *last = e;
     }
     if (logical != 0) {
       w.done = reinterpret_cast<unsigned long long*>(r.region + 3 * S + 2 * static_cast<std::size_t>(n_) + 1);

@@ -128,7 +128,8 @@ struct LocalRank {
   unsigned long long* trace{};  // optional per-lane event timestamps
   std::uint32_t trace_cap{0};
   std::uint64_t launches{0};
-  std::vector<std::uint64_t> ll_last_to;  // [target * 2 + half]: last epoch this rank wrote LL lines to target
+  std::uint64_t ll_last_direct[2]{0, 0};  // last epoch this rank was a direct LL root, per half
+  std::uint64_t ll_last_chain[2]{0, 0};   // last epoch this rank wrote chain lines (LL or LL128), per half
   std::uint64_t ll_done{0};        // cumulative LL CTA completions expected as a receiver
   std::vector<void*> opened;    // IPC mappings to close
 };
@@ -202,8 +203,8 @@ class Group {
   std::size_t region_stride() const { return static_cast<std::size_t>(n_) * lanes_; }
   // Offset (in 8-byte words) of the LL landing area for a flag stride of L lanes.
   std::size_t ll_offset(int lanes) const {
-    const std::size_t w = 3 * static_cast<std::size_t>(n_) * lanes + 2 * static_cast<std::size_t>(n_) + 2;
-    return (w + 1) / 2 * 2;
+    const std::size_t w = 3 * static_cast<std::size_t>(n_) * lanes + 3 * static_cast<std::size_t>(n_) + 2;
+    return (w + 31) / 32 * 32;  // 256-byte aligned: warp stores of LL lines cover whole 128-byte lines
   }
   std::uint64_t ll_max_{dev::kLLMaxBytes};  // LL protocol threshold (bytes), direct schedule
   std::uint64_t ll_chain_max_{0};           // LL pipelined chain up to this size (0 = off)

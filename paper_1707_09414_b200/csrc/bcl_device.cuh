@@ -55,7 +55,7 @@ enum ChunkMode : std::uint32_t {
 
 // Addresses of every peer's state as mapped in *this* rank's address space.
 // Region layout of a rank (8-byte words): flags[n][L] | acks[n][L] | mbox[n][L]
-// | bar[n] | abort | credit[n] | ll_done | pad to 16 B | ll[n][2][ll_lines] (16-byte lines,
+// | bar[n] | abort | credit[n] | ll_done | chain_credit[n] | pad to 16 B | ll[n][2][ll_lines] (16-byte lines,
 // ll_lines = the group's LL cap / 8).
 struct PeerTable {
   std::uint64_t* flags[kMaxRanks];  // peer's flags array (index [my_rank][lane])
@@ -134,11 +134,11 @@ struct LLRank {
   int rank;
   std::uint8_t* buf;
   uint4* ll;                  // local landing area base
-  std::uint64_t* credit;      // local credit array [n]
+  std::uint64_t* credit;      // local credit array [n] of this call's kind (direct, or chain: LL and LL128)
   const PeerTable* peers;
   ErrorRecord* err;
   int* abort;
-  std::uint64_t need[kMaxRanks];  // writer: target t must have credited need[t] (0 = not a target / no wait)
+  std::uint64_t need_credit;  // writer: its targets must have credited this epoch (0 = no wait)
   unsigned long long* done;   // receiver: local completion counter (cumulative over calls)
   unsigned long long done_target;  // receiver: value of *done once every CTA of this call finished
 };

@@ -836,16 +836,16 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ 
       chain ? static_cast<std::size_t>(n) * 2 * P.area_lines + static_cast<std::size_t>(P.half) * P.chain_lines
             : (static_cast<std::size_t>(P.root) * 2 + P.half) * P.area_lines;
   if (writer) {
-    // The half we are about to overwrite was last written for target t in
-    // epoch need[t]: wait until t has read it (normally long ago).
+    // The half we are about to overwrite was last written (same kind) in
+    // epoch need_credit: wait until the targets have read it (normally long ago).
     const int t = static_cast<int>(threadIdx.x);
-    if (t < n && R.need[t] > 0) {
+    if (R.need_credit > 0 && (chain ? t == next : (t < n && t != P.root))) {
       const std::uint64_t* cr = R.credit + t;
       const std::uint64_t t0 = globaltimer();
       std::uint64_t v;
-      while ((v = ld_relaxed_sys(cr)) < R.need[t]) {
+      while ((v = ld_relaxed_sys(cr)) < R.need_credit) {
         if (globaltimer() - t0 > P.timeout_ns) {
-          ll_fail(R, t, 0, v, R.need[t]);
+          ll_fail(R, t, 0, v, R.need_credit);
           break;
         }
       }
@@ -916,7 +916,9 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ 
   if (threadIdx.x == 0 && ok) {
     // The last CTA to finish tells the source every line of this epoch has
     // been read, so the source may reuse the half.
-    if (atomicAdd(R.done, 1ull) + 1 == R.done_target) st_relaxed_sys(R.peers->credit[source] + R.rank, P.epoch);
+    if (atomicAdd(R.done, 1ull) + 1 == R.done_target) {
+      st_relaxed_sys(R.peers->credit[source] + (chain ? n + 1 : 0) + R.rank, P.epoch);
+    }
   }
 }
 
@@ -966,13 +968,12 @@ __global__ void __launch_bounds__(kLLThreads) ll128_kernel(const __grid_constant
   const bool writer = logical + 1 < n;
   const std::size_t area = P.chain128_area + static_cast<std::size_t>(P.half) * P.chain128_lines * 8;
   if (writer) {
-    const int t = static_cast<int>(threadIdx.x);
-    if (t < n && R.need[t] > 0) {
+    if (R.need_credit > 0 && static_cast<int>(threadIdx.x) == next) {
       const std::uint64_t t0 = globaltimer();
       std::uint64_t v;
-      while ((v = ld_relaxed_sys(R.credit + t)) < R.need[t]) {
+      while ((v = ld_relaxed_sys(R.credit + next)) < R.need_credit) {
         if (globaltimer() - t0 > P.timeout_ns) {
-          ll_fail(R, t, 0, v, R.need[t]);
+          ll_fail(R, next, 0, v, R.need_credit);
           break;
         }
       }
@@ -1038,7 +1039,7 @@ __global__ void __launch_bounds__(kLLThreads) ll128_kernel(const __grid_constant
   }
   __syncthreads();
   if (threadIdx.x == 0 && ok) {
-    if (atomicAdd(R.done, 1ull) + 1 == R.done_target) st_relaxed_sys(R.peers->credit[source] + R.rank, P.epoch);
+    if (atomicAdd(R.done, 1ull) + 1 == R.done_target) st_relaxed_sys(R.peers->credit[source] + n + 1 + R.rank, P.epoch);
   }
 }
 

@@ -39,11 +39,12 @@ for setting in settings:
     line = []
     for m in sizes:
         for c in chunks:
-            cfg = B.AlgorithmConfig(B.Algorithm.chain_pipelined, 0, c)
+            algo = B.Algorithm[os.environ.get("ALGO", "chain_pipelined")]
+            cfg = B.AlgorithmConfig(algo, 0, c if algo == B.Algorithm.chain_pipelined else 0)
             ts = []
             for it in range(3 + iters):
                 with torch.cuda.stream(s):
-                    torch.cuda._sleep(400_000)
+                    torch.cuda._sleep(int(os.environ.get("GATE", 400_000)))
                 comm.barrier(s)
                 ev0.record(s)
                 comm.bcast(buf, m, "uint8", 0, cfg, stream=s)
