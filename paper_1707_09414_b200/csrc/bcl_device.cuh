@@ -33,7 +33,7 @@ constexpr std::uint32_t kLLMaxBytes = 2048 * 1024;      // largest LL message (p
 constexpr std::uint32_t kLLChainMaxBytes = 8u << 20;     // default LL pipelined-chain cap
 constexpr std::uint32_t kLL128MaxBytes = 128u << 20;     // default LL128 pipelined-chain cap
 constexpr std::uint32_t kLL128Payload = 120;             // payload bytes per 128-byte LL128 line
-constexpr int kLL128MaxCtas = 148;
+constexpr int kLL128MaxCtas = 444;  // 3 per SM: +4% at 64 MiB n=4 over one per SM (measured)
 constexpr int kLLThreads = 512;
 constexpr int kLLMaxCtas = 64;                          // CTAs per rank for one LL call
 
