@@ -41,7 +41,7 @@ except OSError:
 HBM_PEAK = float(PEAKS.get("hbm_gbs", 6650.0))
 try:  # DRAM bytes per launch of the N=1 kernel from the committed ncu --set full capture
     TRAFFIC_N1 = json.load(open(os.path.join(ROOT, "profiles", "round1", "ncu_traffic.json")))[
-        "n1_config1_bcast_kernel"]["dram_bytes_per_launch"]
+        "n1_config1_local_chain_kernel"]["dram_bytes_per_launch"]
 except (OSError, KeyError, ValueError):
     TRAFFIC_N1 = None
 HBM_PEAK_SRC = "measured" if "hbm_gbs" in PEAKS else "fallback"
@@ -149,7 +149,8 @@ def run_reference_arm(args, rank, world):
 
 def workload_config(n, m, chunk, world):
     if world == 1:
-        wl = (f"BASELINE config 1: pipelined-chain bcast, {n} ranks sharing one B200 (one cooperative launch), "
+        wl = (f"BASELINE config 1: pipelined-chain bcast, {n} ranks sharing one B200 (one launch; every hop "
+              f"copies each chunk from the previous rank's buffer, hops fused per item), "
               f"{m >> 20} MiB float32 payload, root 0, {chunk >> 10} KiB chunks")
     else:
         wl = (f"bcast over {world} B200 (one process per GPU, NVLink P2P), {m >> 20} MiB float32, root 0, "
@@ -259,9 +260,12 @@ def bench_single(args, torch):
 
     t = statistics.mean(times)
     busbw = m / t / 1e9
-    # Roofline of the dominant (only) kernel: every hop reads M and writes M
-    # in HBM of the one GPU: 2 (P-1) M algorithmic bytes per launch.
-    alg_bytes = 2 * (n - 1) * m
+    # Roofline of the dominant (only) kernel, local_chain_kernel: every hop
+    # reads M and writes M, but hop h+1 re-reads what hop h just wrote (an L2
+    # hit by construction), so the DRAM bytes the algorithm needs per launch
+    # are P*M: the root's M read once plus (P-1) M written. 2(P-1)M bytes move
+    # through L2 and are reported beside it.
+    alg_bytes = n * m
     achieved = alg_bytes / t / 1e9
 
     # e2e through the C-ABI with pinned host buffers (run_bcast_host).
@@ -289,9 +293,11 @@ def bench_single(args, torch):
                        "median": round(statistics.median(times) * 1e6, 2), "max": round(max(times) * 1e6, 2)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": HBM_PEAK, "unit": "GB/s",
                      "frac": round(achieved / HBM_PEAK, 4), "traffic": TRAFFIC_N1 if m == 64 << 20 else None,
-                     "algorithmic_bytes": alg_bytes,
-                     "note": f"kernel bcast_kernel<16>; algorithmic bytes 2*(P-1)*M per launch (traffic below it: "
-                             f"the 126 MB L2 serves downstream re-reads); peak {HBM_PEAK_SRC}"},
+                     "algorithmic_bytes": alg_bytes, "l2_bytes": 2 * (n - 1) * m,
+                     "l2_gbs": round(2 * (n - 1) * m / t / 1e9, 1),
+                     "note": f"kernel local_chain_kernel; DRAM-algorithmic bytes P*M per launch (root read once, "
+                             f"P-1 copies written; hop re-reads of the previous hop's output are L2 hits), "
+                             f"2(P-1)M through L2; peak {HBM_PEAK_SRC}"},
         "cpu_baseline": {"value": round(m / cpu["median_s"] / 1e9, 4), "unit": "GB/s", "cores": cpu["cores"],
                          "kind": cpu["kind"], "sample": cpu["sample"]},
         "e2e": {"value": round(m / e2e_t / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": m,

@@ -78,6 +78,9 @@ GroupOptions GroupOptions::from_env() {
   if (const char* v = std::getenv("BCL_STRICT_SYS")) o.strict_sys = std::atoi(v) != 0;
   if (const char* v = std::getenv("BCL_EAGER_POST")) o.eager_post = std::atoi(v) != 0;
   if (const char* v = std::getenv("BCL_WRITER_FENCE")) o.writer_fence = std::atoi(v) != 0;
+  if (const char* v = std::getenv("BCL_LOCAL_FUSED")) o.local_fused = std::atoi(v) != 0;
+  if (const char* v = std::getenv("BCL_LOCAL_CTAS")) o.local_ctas = std::atoi(v);
+  if (const char* v = std::getenv("BCL_LOCAL_ITEM")) o.local_item = std::strtoull(v, nullptr, 10);
   if (const char* v = std::getenv("BCL_LL")) o.ll = std::atoi(v) != 0;
   if (const char* v = std::getenv("BCL_PROTOCOL")) o.protocol = std::atoi(v);
   if (const char* v = std::getenv("BCL_LL_MAX")) o.ll_max_bytes = std::strtoull(v, nullptr, 10);
@@ -419,6 +422,49 @@ bool Group::use_push(const CallPlan& p, std::uint64_t bytes) const {
 // measured table decides between the chain and the other schedules); above
 // them the lane executor. Provenance / timeline recording need the lane
 // executor. Returns 0 (lane executor), 1 (LL) or 2 (LL128).
+// Every rank on this GPU, pipelined chain, auto protocol: the fused
+// flag-free kernel (pull forces the lane executor; timelines need it too).
+bool Group::use_local_chain(const CallPlan& p, const std::vector<int>& locals) const {
+  if (!single_device_ || !p.implicit_chain || opt_.protocol != 0 || !opt_.local_fused) return false;
+  if (static_cast<int>(locals.size()) != n_ || n_ < 2) return false;
+  for (int li : locals) {
+    if (local_[static_cast<std::size_t>(li)].trace != nullptr) return false;
+  }
+  return true;
+}
+
+void Group::launch_local_chain(const std::vector<int>& locals, const std::vector<void*>& bufs, std::uint64_t bytes,
+                               int root, const CallPlan& p, cudaStream_t stream) {
+  dev::LocalChainParams P{};
+  P.n_ranks = n_;
+  P.n_chunks = p.n_chunks;
+  P.bytes = bytes;
+  P.chunk_bytes = p.chunk_bytes;
+  std::uint64_t epoch = 0;
+  for (std::size_t i = 0; i < locals.size(); ++i) {
+    LocalRank& r = local_[static_cast<std::size_t>(locals[i])];
+    const int logical = (r.rank - root + n_) % n_;
+    P.buf[logical] = static_cast<std::uint8_t*>(bufs[i]);
+    P.rank[logical] = r.rank;
+    P.prov[logical] = r.prov;
+    const std::uint64_t e = ++r.epoch;  // keep call counts aligned with the other paths
+    if (i == 0) epoch = e;
+    if (e != epoch) throw std::runtime_error("ranks sharing a GPU drifted apart in call count");
+    ++r.launches;
+  }
+  int sms = 0;
+  DeviceScope ds(local_[static_cast<std::size_t>(locals[0])].device);
+  ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, local_[static_cast<std::size_t>(locals[0])].device),
+     "sm count");
+  const int ctas = opt_.local_ctas > 0 ? opt_.local_ctas : sms * 4;
+  const std::uint64_t warps = static_cast<std::uint64_t>(ctas) * 8;
+  // ~2 items per warp (load balance), 2 KiB .. one chunk, 16-byte multiples.
+  std::uint64_t item = opt_.local_item > 0 ? opt_.local_item : bytes / (2 * warps);
+  item = std::clamp<std::uint64_t>((item + 15) / 16 * 16, 2048, std::max<std::uint64_t>(p.chunk_bytes, 16));
+  P.item_bytes = std::min<std::uint64_t>(item, p.chunk_bytes);
+  ck(static_cast<cudaError_t>(bcl::launch_local_chain(P, ctas, stream)), "launch(local chain)");
+}
+
 int Group::ll_chain_mode(const CallPlan& p, std::uint64_t bytes, const std::vector<int>& locals) const {
   if (!p.implicit_chain || n_ < 2 || !opt_.ll || bytes == 0) return 0;
   if (opt_.protocol == 1 || opt_.protocol == 2) return 0;
@@ -639,6 +685,10 @@ void Group::launch_group(const std::vector<int>& locals, const std::vector<void*
   }
   if (const int mode = ll_chain_mode(p, bytes, locals)) {
     launch_ll(locals, bufs, bytes, root, stream, mode);
+    return;
+  }
+  if (use_local_chain(p, locals)) {
+    launch_local_chain(locals, bufs, bytes, root, p, stream);
     return;
   }
   dev::LaunchParams P{};

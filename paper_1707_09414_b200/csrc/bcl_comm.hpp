@@ -79,6 +79,9 @@ struct GroupOptions {
   bool strict_sys = false;                                  // system-scope fence before every flag
   bool eager_post = true;                                   // bulk chain: forward a chunk once its store is done
   bool writer_fence = true;                                 // copy warps fence their own data (see run_publisher)
+  bool local_fused = true;                                  // single-GPU groups: fused flag-free chain kernel
+  int local_ctas = 0;                                       // its grid (0 = 4 per SM)
+  std::uint64_t local_item = 0;                             // its per-warp item bytes (0 = auto)
   bool ll = true;                                           // LL push protocol for small `direct` calls
   int protocol = 0;                                         // chain: 0 auto (table), 1 pull, 2 push
   std::uint64_t ll_max_bytes = 0;                           // LL threshold (0 = 2 MiB, lowered for many ranks)
@@ -200,6 +203,9 @@ class Group {
                  cudaStream_t stream, int mode);
   void raise_errors(const std::vector<int>& locals);
   int ll_chain_mode(const CallPlan& p, std::uint64_t bytes, const std::vector<int>& locals) const;
+  bool use_local_chain(const CallPlan& p, const std::vector<int>& locals) const;
+  void launch_local_chain(const std::vector<int>& locals, const std::vector<void*>& bufs, std::uint64_t bytes,
+                          int root, const CallPlan& p, cudaStream_t stream);
   std::size_t region_stride() const { return static_cast<std::size_t>(n_) * lanes_; }
   // Offset (in 8-byte words) of the LL landing area for a flag stride of L lanes.
   std::size_t ll_offset(int lanes) const {

@@ -163,6 +163,24 @@ struct LLParamsT {
 };
 using LLParams = LLParamsT<kMaxLocal>;
 
+// Every rank of the group on this GPU (one process): the pipelined chain's
+// hops run as one flag-free kernel. Each warp takes byte ranges ("items") of
+// the message and performs every hop for its item in chain order: logical
+// rank h copies the item from logical rank h - 1's buffer into its own, the
+// next hop reading what the previous one just wrote (an L2 hit). Same bytes
+// read and written per hop as the chain across GPUs; no flags, no waits, no
+// pipeline fill.
+struct LocalChainParams {
+  int n_ranks;
+  std::uint32_t n_chunks;
+  std::uint64_t bytes;
+  std::uint64_t chunk_bytes;
+  std::uint64_t item_bytes;                  // per warp work unit, multiple of 16, <= chunk
+  std::uint8_t* buf[kMaxLocal];              // by logical rank (root first)
+  int rank[kMaxLocal];                       // global rank of each logical rank
+  unsigned long long* prov[kMaxLocal];       // optional provenance of each logical rank
+};
+
 struct BarrierParams {
   int n_ranks;
   int n_local;
@@ -180,6 +198,7 @@ struct BarrierParams {
 int launch_bcast(const dev::LaunchParams& p, int cooperative, void* stream);
 int launch_barrier(const dev::BarrierParams& p, void* stream);
 int launch_ll(const dev::LLParams& p, void* stream);
+int launch_local_chain(const dev::LocalChainParams& p, int ctas, void* stream);
 int bcast_kernel_occupancy(int* blocks_per_sm, std::size_t smem);
 std::size_t bcast_smem_bytes(std::uint32_t stages, std::uint32_t stage_bytes);
 int prepare_bcast_kernels(std::size_t smem);

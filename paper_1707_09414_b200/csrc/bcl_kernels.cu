@@ -786,6 +786,33 @@ __global__ void __launch_bounds__(kThreads, NL == 1 ? 1 : BCL_SHARED_MIN_BLOCKS)
 }
 
 
+// Single-GPU groups: the chain's hops fused per item (LocalChainParams).
+__global__ void __launch_bounds__(256, 4) local_chain_kernel(const __grid_constant__ LocalChainParams P) {
+  const int lane = static_cast<int>(threadIdx.x & 31);
+  const std::uint64_t g = (static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const std::uint64_t G = (static_cast<std::uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const std::uint64_t ipc = (P.chunk_bytes + P.item_bytes - 1) / P.item_bytes;  // items per chunk
+  const std::uint64_t items = static_cast<std::uint64_t>(P.n_chunks) * ipc;
+  Ctx c{};
+  c.lane_id = lane;
+  for (std::uint64_t i = g; i < items; i += G) {
+    const std::uint32_t ch = static_cast<std::uint32_t>(i / ipc);
+    const std::uint64_t off = static_cast<std::uint64_t>(ch) * P.chunk_bytes;
+    const std::uint64_t len = P.bytes - off < P.chunk_bytes ? P.bytes - off : P.chunk_bytes;
+    const std::uint64_t lo = off + (i % ipc) * P.item_bytes;
+    if (lo >= off + len) continue;
+    const std::uint64_t hi = lo + P.item_bytes < off + len ? lo + P.item_bytes : off + len;
+    for (int h = 1; h < P.n_ranks; ++h) {
+      warp_copy(c, P.buf[h - 1], P.buf[h], lo, hi);
+      __syncwarp();  // hop h's stores are visible to hop h + 1's loads (same warp)
+      if (P.prov[h] != nullptr && lane == 0) {
+        atomicAdd(&P.prov[h][static_cast<std::uint64_t>(P.rank[h - 1]) * P.n_chunks + ch],
+                  static_cast<unsigned long long>(hi - lo));
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- LL path
 __device__ __forceinline__ void st_volatile_v4(uint4* p, std::uint32_t a, std::uint32_t b, std::uint32_t c,
                                                std::uint32_t d) {
@@ -1118,6 +1145,11 @@ int launch_bcast(const dev::LaunchParams& p, int cooperative, void* stream) {
   if (p.n_local == 1) return launch_narrow<1>(cfg, p);
   if (p.n_local <= 4) return launch_narrow<4>(cfg, p);
   return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::bcast_kernel<dev::kMaxLocal>, p));
+}
+
+int launch_local_chain(const dev::LocalChainParams& p, int ctas, void* stream) {
+  dev::local_chain_kernel<<<static_cast<unsigned>(ctas), 256, 0, static_cast<cudaStream_t>(stream)>>>(p);
+  return static_cast<int>(cudaGetLastError());
 }
 
 int launch_barrier(const dev::BarrierParams& p, void* stream) {

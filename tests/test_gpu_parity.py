@@ -34,11 +34,23 @@ def _cuda():
 _GROUPS = {}
 
 
-def comms_for(n):
-    """One emulated group per rank count, reused across tests (epochs advance)."""
-    if n not in _GROUPS:
-        _GROUPS[n] = B.Comm.local([0] * n, timeout_s=10)
-    return _GROUPS[n]
+def comms_for(n, fused=False):
+    """One emulated group per rank count, reused across tests (epochs advance).
+    fused=True: a group without the LL chain, so auto-mode chains of every
+    size run the fused single-GPU kernel (local_chain_kernel)."""
+    key = (n, fused)
+    if key not in _GROUPS:
+        old = os.environ.get("BCL_LL_CHAIN_MAX")
+        if fused:
+            os.environ["BCL_LL_CHAIN_MAX"] = "0"
+        try:
+            _GROUPS[key] = B.Comm.local([0] * n, timeout_s=10)
+        finally:
+            if old is None:
+                os.environ.pop("BCL_LL_CHAIN_MAX", None)
+            else:
+                os.environ["BCL_LL_CHAIN_MAX"] = old
+    return _GROUPS[key]
 
 
 def cfg_of(algo, chunk=0, radix=0):
@@ -63,24 +75,30 @@ def set_protocol(n, protocol):
 
 
 def run_case(algo, n, root, m, chunk=0, radix=0, seed=1, offsets=None, protocol="auto"):
+    """protocol: auto (LL chain up to 8 MiB, then the fused kernel), pull (the
+    lane executor) or fused (the fused kernel at every size)."""
     payload = O.payload(seed, m)
     expect = [bytearray(m) for _ in range(n)]
     expect[root][:] = payload
     O.bcast(algo, n, root, expect, chunk=chunk, radix=radix)
     _, views = make_bufs(n, m, root, payload, offsets)
-    set_protocol(n, protocol)
-    try:
-        B.run_bcast(comms_for(n), root, views, m, cfg_of(algo, chunk, radix))
-    finally:
-        set_protocol(n, "auto")
+    if protocol == "fused":
+        B.run_bcast(comms_for(n, fused=True), root, views, m, cfg_of(algo, chunk, radix))
+    else:
+        set_protocol(n, protocol)
+        try:
+            B.run_bcast(comms_for(n), root, views, m, cfg_of(algo, chunk, radix))
+        finally:
+            set_protocol(n, "auto")
     for r in range(n):
         got = views[r].cpu().numpy().tobytes()
         assert got == bytes(expect[r]), f"{algo}/{protocol} n={n} root={root} M={m} C={chunk}: rank {r} differs"
 
 
-# The pipelined chain runs on two device paths: LL lines forwarded hop by hop
-# (auto up to the LL chain cap) and the lane executor (pull).
-CHAIN_PROTOCOLS = ["auto", "pull"]
+# The pipelined chain runs on three device paths on one GPU: LL lines
+# forwarded hop by hop (auto up to the LL chain cap), the fused per-item
+# kernel (auto above it) and the lane executor (pull, and every cross-GPU hop).
+CHAIN_PROTOCOLS = ["auto", "pull", "fused"]
 
 
 @pytest.mark.parametrize("idx", range(len(GOLD["bcasts"])))
@@ -97,7 +115,8 @@ def test_reference_trials_bit_exact(idx):
 
 
 @pytest.mark.parametrize("algo", ["direct", "chain", "knomial", "scatter_ring_allgather",
-                                  "chain_pipelined", "chain_pipelined/pull", "knomial_staged"])
+                                  "chain_pipelined", "chain_pipelined/pull", "chain_pipelined/fused",
+                                  "knomial_staged"])
 @pytest.mark.parametrize("m", [0, 1, 4, 15, 16, 17, 1000, 4096, 65537])
 def test_every_root_small_sizes(algo, m):
     algo, _, protocol = algo.partition("/")
@@ -185,7 +204,8 @@ def test_provenance_matches_schedule_sends():
     """Schedule fidelity (test_runtime.cpp:121-161): every (src, dst, chunk)
     pull happened once and moved exactly the chunk's bytes."""
     n, m = 6, 50000
-    for algo, chunk in (("scatter_ring_allgather", 0), ("chain_pipelined", 7000), ("knomial", 0)):
+    for algo, chunk, protocol in (("scatter_ring_allgather", 0, "auto"), ("chain_pipelined", 7000, "auto"),
+                                  ("chain_pipelined", 7000, "pull"), ("knomial", 0, "auto")):
         cfg = cfg_of(algo, chunk, 2)
         sched = B.make_schedule(cfg, n, 2, m)
         k = len(sched.chunks)
@@ -193,11 +213,13 @@ def test_provenance_matches_schedule_sends():
         prov = [torch.zeros(n * k, dtype=torch.int64, device="cuda:0") for _ in range(n)]
         for r in range(n):
             comms[r].set_provenance(prov[r])
+            comms[r].set_protocol(protocol)  # chain: auto = fused kernel (provenance skips LL), pull = lane executor
         payload = O.payload(3, m)
         _, views = make_bufs(n, m, 2, payload)
         B.run_bcast(comms, 2, views, m, cfg)
         for r in range(n):
             comms[r].set_provenance(None)
+            comms[r].set_protocol("auto")
         expected = {}
         for src, ops in enumerate(sched.per_rank_ops):
             for e in ops:
@@ -211,7 +233,7 @@ def test_provenance_matches_schedule_sends():
                     if int(cnt[src, c]):
                         got[(src, dst, c)] = int(cnt[src, c])
         expected = {key: v for key, v in expected.items() if v}
-        assert got == expected, algo
+        assert got == expected, (algo, protocol)
 
 
 def test_auto_config_uses_table_select():

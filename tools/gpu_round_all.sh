@@ -8,7 +8,7 @@ timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_n1.json 2> 
 CMD="python bench.py --steps 2 --warmup 3 --cpu-iters 1"
 timeout 600 $CMD > gpurun_out/plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_n1.csv $CMD > gpurun_out/ncu_launch.log 2>&1 && \
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:bcast_kernel -s 3 -c 1 -o gpurun_out/prof_n1 $CMD > gpurun_out/ncu_full.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:local_chain_kernel -s 3 -c 1 -o gpurun_out/prof_n1 $CMD > gpurun_out/ncu_full.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/ncu_full.log
 for N in 2 4; do
   timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2990$N bench.py --gpus $N --steps 20 --warmup 5 > gpurun_out/bench_n$N.json 2> gpurun_out/bench_n$N.err
