@@ -482,6 +482,9 @@ int Group::ll_chain_mode(const CallPlan& p, std::uint64_t bytes, const std::vect
     return 2;
   }
   if (ll128_ok_ && bytes <= ll128_max_ && select_ll128(table(), n_, bytes)) return 2;
+  // One GPU: the fused kernel beats LL lines at every size (4 KiB: 8.2 vs
+  // 9.8 us, 8 MiB: 12.4 vs 51.8 us, 4 ranks); LL stays available explicitly.
+  if (use_local_chain(p, locals)) return 0;
   return bytes <= ll_chain_max_ ? 1 : 0;
 }
 const TuningTable& Group::table() const { return have_table_ ? table_ : builtin_table(); }

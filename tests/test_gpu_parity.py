@@ -34,23 +34,11 @@ def _cuda():
 _GROUPS = {}
 
 
-def comms_for(n, fused=False):
-    """One emulated group per rank count, reused across tests (epochs advance).
-    fused=True: a group without the LL chain, so auto-mode chains of every
-    size run the fused single-GPU kernel (local_chain_kernel)."""
-    key = (n, fused)
-    if key not in _GROUPS:
-        old = os.environ.get("BCL_LL_CHAIN_MAX")
-        if fused:
-            os.environ["BCL_LL_CHAIN_MAX"] = "0"
-        try:
-            _GROUPS[key] = B.Comm.local([0] * n, timeout_s=10)
-        finally:
-            if old is None:
-                os.environ.pop("BCL_LL_CHAIN_MAX", None)
-            else:
-                os.environ["BCL_LL_CHAIN_MAX"] = old
-    return _GROUPS[key]
+def comms_for(n):
+    """One emulated group per rank count, reused across tests (epochs advance)."""
+    if n not in _GROUPS:
+        _GROUPS[n] = B.Comm.local([0] * n, timeout_s=10)
+    return _GROUPS[n]
 
 
 def cfg_of(algo, chunk=0, radix=0):
@@ -75,30 +63,27 @@ def set_protocol(n, protocol):
 
 
 def run_case(algo, n, root, m, chunk=0, radix=0, seed=1, offsets=None, protocol="auto"):
-    """protocol: auto (LL chain up to 8 MiB, then the fused kernel), pull (the
-    lane executor) or fused (the fused kernel at every size)."""
+    """protocol (chain): auto (the fused single-GPU kernel), pull (the lane
+    executor) or ll (LL lines forwarded hop by hop, <= 8 MiB)."""
     payload = O.payload(seed, m)
     expect = [bytearray(m) for _ in range(n)]
     expect[root][:] = payload
     O.bcast(algo, n, root, expect, chunk=chunk, radix=radix)
     _, views = make_bufs(n, m, root, payload, offsets)
-    if protocol == "fused":
-        B.run_bcast(comms_for(n, fused=True), root, views, m, cfg_of(algo, chunk, radix))
-    else:
-        set_protocol(n, protocol)
-        try:
-            B.run_bcast(comms_for(n), root, views, m, cfg_of(algo, chunk, radix))
-        finally:
-            set_protocol(n, "auto")
+    set_protocol(n, protocol)
+    try:
+        B.run_bcast(comms_for(n), root, views, m, cfg_of(algo, chunk, radix))
+    finally:
+        set_protocol(n, "auto")
     for r in range(n):
         got = views[r].cpu().numpy().tobytes()
         assert got == bytes(expect[r]), f"{algo}/{protocol} n={n} root={root} M={m} C={chunk}: rank {r} differs"
 
 
-# The pipelined chain runs on three device paths on one GPU: LL lines
-# forwarded hop by hop (auto up to the LL chain cap), the fused per-item
-# kernel (auto above it) and the lane executor (pull, and every cross-GPU hop).
-CHAIN_PROTOCOLS = ["auto", "pull", "fused"]
+# The pipelined chain runs on three device paths on one GPU: the fused
+# per-item kernel (auto), the lane executor (pull; also every cross-GPU pull)
+# and LL lines forwarded hop by hop (ll).
+CHAIN_PROTOCOLS = ["auto", "pull", "ll"]
 
 
 @pytest.mark.parametrize("idx", range(len(GOLD["bcasts"])))
@@ -115,7 +100,7 @@ def test_reference_trials_bit_exact(idx):
 
 
 @pytest.mark.parametrize("algo", ["direct", "chain", "knomial", "scatter_ring_allgather",
-                                  "chain_pipelined", "chain_pipelined/pull", "chain_pipelined/fused",
+                                  "chain_pipelined", "chain_pipelined/pull", "chain_pipelined/ll",
                                   "knomial_staged"])
 @pytest.mark.parametrize("m", [0, 1, 4, 15, 16, 17, 1000, 4096, 65537])
 def test_every_root_small_sizes(algo, m):
@@ -157,15 +142,18 @@ def test_sixteen_ranks_one_megabyte(protocol):
 
 def test_ll_chain_cap_and_interleaving_with_direct():
     """LL chain at and around its cap (8 MiB), interleaved with LL direct
-    calls from changing roots: the landing halves are shared per writer and
-    target, so credits must track (writer, target, half) exactly."""
+    calls from changing roots: direct and chain calls keep separate credits
+    and landing halves; above the cap the auto path takes over."""
     n = 4
     cap = 8 << 20
     sizes = [cap, cap - 8, 3 << 20, cap + 16, 100, 2 << 20]
     for i, m in enumerate(sizes * 2):
         root = (i * 3) % n
-        algo = "chain_pipelined" if i % 2 == 0 else "direct"
-        run_case(algo, n, root, m, chunk=262144, seed=i + 7)
+        if i % 2:
+            run_case("direct", n, root, m, seed=i + 7)
+        else:
+            run_case("chain_pipelined", n, root, m, chunk=262144, seed=i + 7,
+                     protocol="ll" if m <= cap else "auto")
     with pytest.raises(ValueError):
         run_case("chain_pipelined", n, 0, cap + 16, chunk=262144, protocol="ll")
 
