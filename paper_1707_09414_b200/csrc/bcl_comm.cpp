@@ -456,10 +456,13 @@ void Group::launch_local_chain(const std::vector<int>& locals, const std::vector
   DeviceScope ds(local_[static_cast<std::size_t>(locals[0])].device);
   ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, local_[static_cast<std::size_t>(locals[0])].device),
      "sm count");
-  const int ctas = opt_.local_ctas > 0 ? opt_.local_ctas : sms * 4;
+  int occ = 0;
+  ck(static_cast<cudaError_t>(local_chain_occupancy(&occ)), "occupancy(local chain)");
+  const int ctas = opt_.local_ctas > 0 ? opt_.local_ctas : sms * std::max(occ, 1);
   const std::uint64_t warps = static_cast<std::uint64_t>(ctas) * 8;
-  // ~2 items per warp (load balance), 2 KiB .. one chunk, 16-byte multiples.
-  std::uint64_t item = opt_.local_item > 0 ? opt_.local_item : bytes / (2 * warps);
+  // ~4 items per warp (load balance; ~3.5 KiB at 64 MiB: 52 us vs 56 us with
+  // 7 KiB items, profiles/round1/fused_n1_variants.log), 2 KiB .. one chunk.
+  std::uint64_t item = opt_.local_item > 0 ? opt_.local_item : bytes / (4 * warps);
   item = std::clamp<std::uint64_t>((item + 15) / 16 * 16, 2048, std::max<std::uint64_t>(p.chunk_bytes, 16));
   P.item_bytes = std::min<std::uint64_t>(item, p.chunk_bytes);
   ck(static_cast<cudaError_t>(bcl::launch_local_chain(P, ctas, stream)), "launch(local chain)");

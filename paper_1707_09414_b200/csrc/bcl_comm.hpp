@@ -80,7 +80,7 @@ struct GroupOptions {
   bool eager_post = true;                                   // bulk chain: forward a chunk once its store is done
   bool writer_fence = true;                                 // copy warps fence their own data (see run_publisher)
   bool local_fused = true;                                  // single-GPU groups: fused flag-free chain kernel
-  int local_ctas = 0;                                       // its grid (0 = 4 per SM)
+  int local_ctas = 0;                                       // its grid (0 = all resident CTAs)
   std::uint64_t local_item = 0;                             // its per-warp item bytes (0 = auto)
   bool ll = true;                                           // LL push protocol for small `direct` calls
   int protocol = 0;                                         // chain: 0 auto (table), 1 pull, 2 push

@@ -199,6 +199,7 @@ int launch_bcast(const dev::LaunchParams& p, int cooperative, void* stream);
 int launch_barrier(const dev::BarrierParams& p, void* stream);
 int launch_ll(const dev::LLParams& p, void* stream);
 int launch_local_chain(const dev::LocalChainParams& p, int ctas, void* stream);
+int local_chain_occupancy(int* blocks_per_sm);
 int bcast_kernel_occupancy(int* blocks_per_sm, std::size_t smem);
 std::size_t bcast_smem_bytes(std::uint32_t stages, std::uint32_t stage_bytes);
 int prepare_bcast_kernels(std::size_t smem);

@@ -787,7 +787,10 @@ __global__ void __launch_bounds__(kThreads, NL == 1 ? 1 : BCL_SHARED_MIN_BLOCKS)
 
 
 // Single-GPU groups: the chain's hops fused per item (LocalChainParams).
-__global__ void __launch_bounds__(256, 4) local_chain_kernel(const __grid_constant__ LocalChainParams P) {
+#ifndef BCL_LC_MINB
+#define BCL_LC_MINB 4
+#endif
+__global__ void __launch_bounds__(256, BCL_LC_MINB) local_chain_kernel(const __grid_constant__ LocalChainParams P) {
   const int lane = static_cast<int>(threadIdx.x & 31);
   const std::uint64_t g = (static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const std::uint64_t G = (static_cast<std::uint64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -1145,6 +1148,10 @@ int launch_bcast(const dev::LaunchParams& p, int cooperative, void* stream) {
   if (p.n_local == 1) return launch_narrow<1>(cfg, p);
   if (p.n_local <= 4) return launch_narrow<4>(cfg, p);
   return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::bcast_kernel<dev::kMaxLocal>, p));
+}
+
+int local_chain_occupancy(int* blocks_per_sm) {
+  return static_cast<int>(cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, dev::local_chain_kernel, 256, 0));
 }
 
 int launch_local_chain(const dev::LocalChainParams& p, int ctas, void* stream) {
