@@ -639,9 +639,6 @@ void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& 
   if (mode == 2) {  // a warp moves 4 lines per step: ~2 steps per warp, up to one CTA per SM
     const std::uint32_t per_cta = dev::kLLThreads / 32 * 4 * 2;
     P.ctas = std::clamp<int>(static_cast<int>((P.lines + per_cta - 1) / per_cta), 1, dev::kLL128MaxCtas);
-    if (const char* v = std::getenv("BCL_LL128_CTAS")) {  // experiment
-      P.ctas = std::clamp<int>(static_cast<int>((P.lines + per_cta - 1) / per_cta), 1, std::atoi(v));
-    }
   }
   P.timeout_ns = opt_.timeout_ns;
   const std::size_t S = region_stride();

@@ -339,3 +339,19 @@ def test_layerwise_parameter_broadcast(model, bucket):
     for r in range(n):
         for off, size in zip(pb.offsets, pb.sizes):
             assert torch.equal(flats[r][off:off + size], flats[root][off:off + size]), (model, r, off)
+
+
+def test_protocol_caps_and_lane_plan():
+    """bcl_comm_protocol_caps / bcl_comm_plan on a single-GPU group: no LL128
+    (ranks share the GPU), LL caps as configured; the lane plan tiles the
+    lanes (Q divides L) and covers each chunk with Q slices."""
+    comms = comms_for(4)
+    caps = comms[0].protocol_caps()
+    assert caps == {"ll_direct": 2 << 20, "ll_chain": 8 << 20, "ll128": 0}
+    lanes = comms[0].info()["lanes"]
+    for m, chunk in ((64 << 20, 512 << 10), (1 << 20, 65536), (12345, 1000)):
+        p = comms[0].plan(cfg_of("chain_pipelined", chunk), 0, m)
+        assert lanes % p["slices"] == 0
+        assert p["n_chunks"] == -(-m // chunk)
+        assert p["slices"] * p["slice_bytes"] >= min(chunk, m)
+        assert 1 <= p["ctas"] * 8 <= lanes
