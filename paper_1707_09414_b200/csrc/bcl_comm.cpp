@@ -82,7 +82,10 @@ GroupOptions GroupOptions::from_env() {
   if (const char* v = std::getenv("BCL_LOCAL_CTAS")) o.local_ctas = std::atoi(v);
   if (const char* v = std::getenv("BCL_LOCAL_ITEM")) o.local_item = std::strtoull(v, nullptr, 10);
   if (const char* v = std::getenv("BCL_LL")) o.ll = std::atoi(v) != 0;
-  if (const char* v = std::getenv("BCL_PROTOCOL")) o.protocol = std::atoi(v);
+  if (const char* v = std::getenv("BCL_PROTOCOL")) {
+    o.protocol = std::atoi(v);
+    if (o.protocol < 0 || o.protocol > 4) throw std::invalid_argument("BCL_PROTOCOL must be 0..4");
+  }
   if (const char* v = std::getenv("BCL_LL_MAX")) o.ll_max_bytes = std::strtoull(v, nullptr, 10);
   if (const char* v = std::getenv("BCL_LL_CHAIN_MAX")) o.ll_chain_max_bytes = std::strtoll(v, nullptr, 10);
   if (const char* v = std::getenv("BCL_LL128_MAX")) o.ll128_max_bytes = std::strtoll(v, nullptr, 10);
