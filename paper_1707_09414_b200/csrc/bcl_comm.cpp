@@ -249,9 +249,9 @@ std::shared_ptr<Group> Group::create_local(const std::vector<int>& devices, cons
       lr.h_peers.flags[p] = base;
       lr.h_peers.acks[p] = base + S;
       lr.h_peers.mbox[p] = base + 2 * S;
-      lr.h_peers.bar[p] = base + 3 * S;
+      lr.h_peers.bar[p] = base + 4 * S;
       lr.h_peers.addr_base[p] = 0;
-      lr.h_peers.credit[p] = base + 3 * S + n + 1;
+      lr.h_peers.credit[p] = base + 4 * S + n + 1;
       lr.h_peers.ll[p] = reinterpret_cast<uint4*>(base + g->ll_offset(g->lanes_));
     }
     g->upload_peers(lr);
@@ -363,9 +363,9 @@ void Group::connect(const std::vector<std::vector<std::uint8_t>>& infos) {
     me.h_peers.flags[p] = base;
     me.h_peers.acks[p] = base + S;
     me.h_peers.mbox[p] = base + 2 * S;
-    me.h_peers.bar[p] = base + 3 * S;
+    me.h_peers.bar[p] = base + 4 * S;
     me.h_peers.addr_base[p] = heap_base;
-    me.h_peers.credit[p] = base + 3 * S + n_ + 1;
+    me.h_peers.credit[p] = base + 4 * S + n_ + 1;
     me.h_peers.ll[p] = reinterpret_cast<uint4*>(base + ll_offset(lanes_));
   }
   upload_peers(me);
@@ -603,12 +603,13 @@ void Group::fill_rank_work(dev::RankWork& w, LocalRank& r, const CallPlan& p, vo
   w.buf = static_cast<std::uint8_t*>(buf);
   w.pub = ipc_ ? static_cast<std::uint64_t>(static_cast<std::uint8_t*>(buf) - r.heap)
                : reinterpret_cast<std::uint64_t>(buf);
+  if (w.pub >> 48) throw std::runtime_error("buffer address does not fit the 48-bit mailbox field");
   w.flags = r.region;
   w.acks = r.region + S;
   w.mbox = r.region + 2 * S;
   w.peers = r.d_peers;
   w.err = r.err_dev;
-  w.abort = reinterpret_cast<int*>(r.region + 3 * S + static_cast<std::size_t>(n_));
+  w.abort = reinterpret_cast<int*>(r.region + 4 * S + static_cast<std::size_t>(n_));
   w.prov = r.prov;
   w.trace = r.trace;
   w.trace_cap = r.trace_cap;
@@ -654,11 +655,11 @@ void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& 
     dev::LLRank& w = P.ranks[i];
     w.rank = r.rank;
     w.buf = static_cast<std::uint8_t*>(bufs[i]);
-    w.credit = r.region + 3 * S + static_cast<std::size_t>(n_) + 1 + (chain ? static_cast<std::size_t>(n_) + 1 : 0);
+    w.credit = r.region + 4 * S + static_cast<std::size_t>(n_) + 1 + (chain ? static_cast<std::size_t>(n_) + 1 : 0);
     w.ll = reinterpret_cast<uint4*>(r.region + ll_offset(lanes_));
     w.peers = r.d_peers;
     w.err = r.err_dev;
-    w.abort = reinterpret_cast<int*>(r.region + 3 * S + static_cast<std::size_t>(n_));
+    w.abort = reinterpret_cast<int*>(r.region + 4 * S + static_cast<std::size_t>(n_));
     const std::uint32_t half = static_cast<std::uint32_t>(e & 1u);
     const int logical = (r.rank - root + n_) % n_;
     // Writers wait for the credits of the last call of the same kind that
@@ -671,7 +672,7 @@ void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& 
       *last = e;
     }
     if (logical != 0) {
-      w.done = reinterpret_cast<unsigned long long*>(r.region + 3 * S + 2 * static_cast<std::size_t>(n_) + 1);
+      w.done = reinterpret_cast<unsigned long long*>(r.region + 4 * S + 2 * static_cast<std::size_t>(n_) + 1);
       r.ll_done += static_cast<std::uint64_t>(P.ctas);
       w.done_target = r.ll_done;
     }
@@ -982,7 +983,7 @@ void Group::barrier(int li, cudaStream_t stream) {
   B.epoch = ++r.bar_epoch;
   B.timeout_ns = opt_.timeout_ns;
   B.rank[0] = r.rank;
-  B.bar[0] = r.region + 3 * region_stride();
+  B.bar[0] = r.region + 4 * region_stride();
   B.peers[0] = r.d_peers;
   B.err[0] = r.err_dev;
   DeviceScope ds(r.device);
@@ -999,7 +1000,7 @@ void Group::barrier_all(const std::vector<cudaStream_t>& streams) {
       LocalRank& r = local_[static_cast<std::size_t>(kv.second[i])];
       B.epoch = ++r.bar_epoch;
       B.rank[i] = r.rank;
-      B.bar[i] = r.region + 3 * region_stride();
+      B.bar[i] = r.region + 4 * region_stride();
       B.peers[i] = r.d_peers;
       B.err[i] = r.err_dev;
     }

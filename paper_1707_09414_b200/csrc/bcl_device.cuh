@@ -54,13 +54,13 @@ enum ChunkMode : std::uint32_t {
 };
 
 // Addresses of every peer's state as mapped in *this* rank's address space.
-// Region layout of a rank (8-byte words): flags[n][L] | acks[n][L] | mbox[n][L]
+// Region layout of a rank (8-byte words): flags[n][L] | acks[n][L] | mbox[n][L][2]
 // | bar[n] | abort | credit[n] | ll_done | chain_credit[n] | pad to 16 B | ll[n][2][ll_lines] (16-byte lines,
 // ll_lines = the group's LL cap / 8).
 struct PeerTable {
   std::uint64_t* flags[kMaxRanks];  // peer's flags array (index [my_rank][lane])
   std::uint64_t* acks[kMaxRanks];   // peer's acks array  (index [my_rank][lane])
-  std::uint64_t* mbox[kMaxRanks];   // peer's mailbox     (index [my_rank][lane])
+  std::uint64_t* mbox[kMaxRanks];   // peer's mailbox     (16-byte slots, index [my_rank][lane])
   std::uint64_t* bar[kMaxRanks];    // peer's barrier slots (index [my_rank])
   std::uint64_t addr_base[kMaxRanks];  // added to a mailbox value from that peer
   std::uint64_t* credit[kMaxRanks];    // peer's LL credit array (index [my_rank])
@@ -84,7 +84,7 @@ struct RankWork {
   std::uint64_t pub;             // mailbox value naming buf to consumers
   std::uint64_t* flags;          // local flags[n][L]
   std::uint64_t* acks;           // local acks[n][L]
-  std::uint64_t* mbox;           // local mbox[n][L]
+  std::uint64_t* mbox;           // local mbox[n][L] (16-byte slots)
   const PeerTable* peers;        // device-resident
   ErrorRecord* err;              // host-mapped error record of this rank (written once, on failure)
   int* abort;                    // device-memory abort word polled by waiting lanes

@@ -254,6 +254,43 @@ __device__ void publish(Ctx& c, std::uint64_t* addr, std::uint64_t value) {
   __syncwarp();
 }
 
+// Mailboxes are 16-byte slots {epoch16 << 48 | value, epoch}: both halves
+// carry the call's epoch, so a consumer can validate the slot itself and the
+// producer needs no system-scope fence between its mailbox store and its
+// first flag (that fence cost ~4-6 us at lane start, profiles/round1/mbox).
+__device__ __forceinline__ void st_mbox(std::uint64_t* slot, std::uint64_t value, std::uint64_t epoch) {
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1,%2};" ::"l"(slot),
+               "l"(value | ((epoch & 0xFFFFull) << 48)), "l"(epoch)
+               : "memory");
+}
+// Warp-collective: lane 0 polls the mailbox until it carries this call's
+// epoch in both halves; every lane gets the value.
+__device__ std::uint64_t read_mbox(const Ctx& c, const std::uint64_t* slot, int peer) {
+  unsigned long long value = 0;
+  if (c.lane_id == 0) {
+    const std::uint64_t epoch = c.P->epoch;
+    const std::uint64_t hi = (epoch & 0xFFFFull) << 48;
+    const std::uint64_t t0 = globaltimer();
+    unsigned spins = 0;
+    for (;;) {
+      std::uint64_t a, b;
+      asm volatile("ld.volatile.global.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(slot) : "memory");
+      if (b == epoch && (a & 0xFFFF000000000000ull) == hi) {
+        value = a & 0x0000FFFFFFFFFFFFull;
+        break;
+      }
+      if ((++spins & 255u) == 0) {
+        if (*(volatile int*)c.W->abort != 0) break;
+        if (globaltimer() - t0 > c.P->timeout_ns) {
+          fail(c, 1, peer, 0, b, epoch);
+          break;
+        }
+      }
+    }
+  }
+  return __shfl_sync(0xffffffffu, value, 0);
+}
+
 // The publisher warp (lane 0): drain every ring, one fence per batch.
 __device__ void run_publisher(const LaunchParamsT<1>& P, CtaShared* sh, const RankWork& W, int cta) {
   if ((threadIdx.x & 31) != 0) return;
@@ -569,10 +606,7 @@ __device__ void run_chain_push(Ctx& c, int pipe, int q, int ns) {
   const std::size_t slot = static_cast<std::size_t>(me) * L + c.ell;
   const std::uint64_t* arrived = has_prev ? W.flags + static_cast<std::size_t>(prev) * L + c.ell : nullptr;
   if (has_prev) {  // consumer: announce the destination, then "ready"
-    if (c.lane_id == 0) {
-      st_relaxed_sys(W.peers->mbox[prev] + slot, W.pub);
-      fence_acq_rel_sys();
-    }
+    if (c.lane_id == 0) st_mbox(W.peers->mbox[prev] + 2 * slot, W.pub, P.epoch);
     publish(c, W.peers->acks[prev] + slot, P.epoch);
   }
   if (!has_next) {  // tail: wait until every chunk of this lane has landed
@@ -581,7 +615,7 @@ __device__ void run_chain_push(Ctx& c, int pipe, int q, int ns) {
   }
   if (!wait_geq(c, W.acks + static_cast<std::size_t>(next) * L + c.ell, P.epoch, next, 0)) return;
   auto* dst = reinterpret_cast<std::uint8_t*>(
-      W.peers->addr_base[next] + ld_relaxed_sys(W.mbox + static_cast<std::size_t>(next) * L + c.ell));
+      W.peers->addr_base[next] + read_mbox(c, W.mbox + 2 * (static_cast<std::size_t>(next) * L + c.ell), next));
   std::uint64_t* next_flag = W.peers->flags[next] + slot;
   const bool aligned = c.stage != nullptr &&
                        ((reinterpret_cast<std::uintptr_t>(dst) | reinterpret_cast<std::uintptr_t>(W.buf)) & 15u) == 0 &&
@@ -623,10 +657,7 @@ __device__ void run_chain(Ctx& c, int pipe, int q, int ns) {
   const std::uint64_t tag = P.epoch << 32;
   const std::size_t slot = static_cast<std::size_t>(me) * L + c.ell;
 
-  if (has_next && c.lane_id == 0) {
-    st_relaxed_sys(W.peers->mbox[next] + slot, W.pub);
-    if (P.sys_scope) fence_acq_rel_sys();  // remote mailbox lands before any remote flag
-  }
+  if (has_next && c.lane_id == 0) st_mbox(W.peers->mbox[next] + 2 * slot, W.pub, P.epoch);
   if (!has_prev) {
     publish(c, W.peers->flags[next] + slot, tag | mine);  // the head owns every chunk
   } else {
@@ -635,7 +666,7 @@ __device__ void run_chain(Ctx& c, int pipe, int q, int ns) {
     if (c.stage != nullptr) {
       if (!wait_geq(c, ready, tag | 1, prev, pipe)) return;
       src = reinterpret_cast<const std::uint8_t*>(
-          W.peers->addr_base[prev] + ld_relaxed_sys(W.mbox + static_cast<std::size_t>(prev) * L + c.ell));
+          W.peers->addr_base[prev] + read_mbox(c, W.mbox + 2 * (static_cast<std::size_t>(prev) * L + c.ell), prev));
       const bool aligned = ((reinterpret_cast<std::uintptr_t>(src) | reinterpret_cast<std::uintptr_t>(W.buf)) & 15u) == 0 &&
                            (P.chunk_bytes & 15u) == 0 && (P.slice_bytes & 15u) == 0 &&
                            P.slice_bytes <= P.stage_bytes;
@@ -655,7 +686,7 @@ __device__ void run_chain(Ctx& c, int pipe, int q, int ns) {
       const std::uint64_t t_ready = W.trace ? globaltimer() : 0;
       if (k == 0) {
         src = reinterpret_cast<const std::uint8_t*>(
-            W.peers->addr_base[prev] + ld_relaxed_sys(W.mbox + static_cast<std::size_t>(prev) * L + c.ell));
+            W.peers->addr_base[prev] + read_mbox(c, W.mbox + 2 * (static_cast<std::size_t>(prev) * L + c.ell), prev));
       }
       pull_slice(c, pipe + k * ns, q, src, prev);
       if (has_next) publish(c, W.peers->flags[next] + slot, tag | (k + 1));  // forward chunk k
@@ -686,10 +717,9 @@ __device__ void run_events(Ctx& c, int pipe, int q, int ns) {
     const int peer = static_cast<int>((ev >> 24) & 0x7F);
     if (!((sent_mask >> peer) & 1u)) {
       sent_mask |= 1ull << peer;
-      if (c.lane_id == 0) st_relaxed_sys(W.peers->mbox[peer] + slot, W.pub);
+      if (c.lane_id == 0) st_mbox(W.peers->mbox[peer] + 2 * slot, W.pub, P.epoch);
     }
   }
-  if (sent_mask && c.lane_id == 0 && P.sys_scope) fence_acq_rel_sys();  // mailboxes before flags
   const std::uint8_t* src_of[kMaxRanks];
   std::uint32_t k = 0;
   for (int i = 0; i < W.n_events; ++i) {
@@ -707,7 +737,7 @@ __device__ void run_events(Ctx& c, int pipe, int q, int ns) {
       if (!((recv_mask >> peer) & 1u)) {
         recv_mask |= 1ull << peer;
         src_of[peer] = reinterpret_cast<const std::uint8_t*>(
-            W.peers->addr_base[peer] + ld_relaxed_sys(W.mbox + static_cast<std::size_t>(peer) * L + c.ell));
+            W.peers->addr_base[peer] + read_mbox(c, W.mbox + 2 * (static_cast<std::size_t>(peer) * L + c.ell), peer));
       }
       pull_slice(c, ch, q, src_of[peer], peer);
       trace_pull(c, k++, t_wait, t_ready);
