@@ -88,6 +88,14 @@ def cost(cfg, n, m):
     return quantize(med)
 
 
+def raw_cost(cfg, n, m):
+    """Unquantized median: transport rules compare protocols of one schedule,
+    where 2-significant-digit ties (10 us steps above 100 us) would hide
+    real differences."""
+    cost(cfg, n, m)
+    return raw[-1][5]
+
+
 sizes = []
 s = a.min
 while s <= a.max:
@@ -116,9 +124,9 @@ if world >= 3:
             wins.append((m, False))
             continue
         set_proto("pull")
-        t_pull = cost(cfg, world, m)
+        t_pull = raw_cost(cfg, world, m)
         set_proto("push")
-        t_push = cost(cfg, world, m)
+        t_push = raw_cost(cfg, world, m)
         set_proto("auto")
         wins.append((m, t_push < t_pull))
         if rank == 0:
@@ -142,9 +150,9 @@ if ll128_cap:
         if cfg.algorithm != B.Algorithm.chain_pipelined:
             continue
         set_proto("ll128")
-        t_ll = cost(cfg, world, m)
+        t_ll = raw_cost(cfg, world, m)
         set_proto("push" if push_from is not None and m >= push_from else "pull")
-        t_lane = cost(cfg, world, m)
+        t_lane = raw_cost(cfg, world, m)
         set_proto("auto")
         if rank == 0:
             print(f"line protocol {m}: ll128 {t_ll * 1e6:.1f} us lane executor {t_lane * 1e6:.1f} us")
