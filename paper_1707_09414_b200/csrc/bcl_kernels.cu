@@ -1,18 +1,23 @@
-// bcl_kernels.cu — sm_100a broadcast executor (see bcl_device.cuh).
+// bcl_kernels.cu — sm_100a broadcast executors (see bcl_device.cuh).
 //
-// One launch per GPU serves every rank that GPU hosts (normally one). A CTA
-// holds kWarpsPerCta *copy warps* (the lanes) and one *publisher warp*:
-//
+// bcast_kernel — the lane executor. One launch per GPU serves every rank that
+// GPU hosts (normally one). A CTA holds kWarpsPerCta *copy warps* (the lanes)
+// and one *publisher warp*:
 //  * a copy warp owns slice q = lane % Q of the chunks c with
 //    c % (L/Q) == lane / Q and walks its rank's schedule: it waits for the
 //    upstream peer's per-lane counter, pulls the slice straight out of the
-//    peer's buffer with 16-byte vector loads (every load of a batch in
-//    flight), stores it locally, and hands "store value v to flag f" to the
-//    publisher through a shared-memory ring (CTA-scope release);
-//  * the publisher drains the rings of its CTA and issues ONE system-scope
-//    fence per batch before the remote flag stores. Under NVLink load a
-//    fence.acq_rel.sys costs ~10 us (measured), so it must not sit in the copy
-//    warps' per-chunk path.
+//    peer's buffer (TMA bulk copies through shared-memory stages across
+//    GPUs, 16-byte vector loads otherwise), fences its own completed stores
+//    (gpu scope) and hands "store value v to flag f" to the publisher through
+//    a shared-memory ring (CTA-scope release);
+//  * the publisher drains the rings of its CTA and issues the remote flag
+//    stores. It never fences (a fence would wait for its previous remote flag
+//    stores, ~16 us under NVLink load) except in push / strict modes.
+// ll_kernel / ll128_kernel — line protocols (flag travels with the data):
+//   the direct schedule's LL push and the pipelined chain forwarded line by
+//   line (16-byte LL lines, 128-byte LL128 lines across GPUs).
+// local_chain_kernel — every rank on this GPU: the chain's hops fused per item.
+// barrier_kernel — device barrier across ranks.
 //
 // Data never leaves HBM / NVLink: no staging buffers, no cudaMemcpy, no NCCL.
 #include <cuda_runtime.h>
