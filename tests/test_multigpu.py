@@ -101,6 +101,17 @@ def test_ll128_chain_back_to_back_stress():
         B.run_bcast(comms, root, [b[:m] for b in bufs], m, cfg_of("chain_pipelined", 262144))
         for r in range(n):
             assert torch.equal(bufs[r][:m].cpu(), src.cpu()), (it, m, root, r)
+    # misaligned buffers (byte paths of the 120-byte payload pieces)
+    for it, (m, offs) in enumerate([((1 << 20) + 3, [1, 2, 3, 5]), (12345, [7, 0, 4, 1]), (120 * 1000 + 1, [3, 3, 3, 3])]):
+        root = it % n
+        src = torch.randint(0, 256, (m,), dtype=torch.uint8, device=f"cuda:{devices[root]}")
+        views = [bufs[r][offs[r % 4]:offs[r % 4] + m] for r in range(n)]
+        for r in range(n):
+            (views[r].copy_(src) if r == root else views[r].fill_(0xA5))
+        torch.cuda.synchronize(devices[root])
+        B.run_bcast(comms, root, views, m, cfg_of("chain_pipelined", 262144))
+        for r in range(n):
+            assert torch.equal(views[r].cpu(), src.cpu()), ("misaligned", m, offs, r)
     with pytest.raises(ValueError):  # above the LL128 landing area
         B.run_bcast(comms, 0, [b[:cap + 1] for b in bufs], cap + 1, cfg_of("chain_pipelined", 262144))
     for c in comms:
