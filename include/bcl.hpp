@@ -170,6 +170,10 @@ class LocalGroup {
   void set_table(const Table& t) {
     for (bcl_comm_t c : comms_) check(bcl_comm_set_table(c, t.get()));
   }
+  // Chain transport (B200 only): 0 auto, 1 pull, 2 push, 3 LL, 4 LL128.
+  void set_protocol(int protocol) {
+    for (bcl_comm_t c : comms_) check(bcl_comm_set_protocol(c, protocol));
+  }
   // run_bcast (runtime.hpp:140-143) over device buffers; wall seconds.
   double run_bcast(int root, const std::vector<void*>& device_bufs, std::uint64_t bytes,
                    const Config* config = nullptr) {

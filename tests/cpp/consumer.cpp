@@ -73,6 +73,14 @@ int main(int argc, char** argv) {
     for (int r = 0; r < n; ++r) if (r != 1) std::fill(host[r].begin(), host[r].end(), 0);
     (void)g.run_bcast_host(1, ptrs, m);
     for (int r = 0; r < n; ++r) EXPECT(host[r] == host[1]);
+    // every single-GPU transport of the chain: fused (auto), lane executor, LL lines
+    for (int proto : {0, 1, 3}) {
+      g.set_protocol(proto);
+      for (int r = 0; r < n; ++r) if (r != 3) std::fill(host[r].begin(), host[r].end(), 0);
+      (void)g.run_bcast_host(3, ptrs, m, &cfg);
+      for (int r = 0; r < n; ++r) EXPECT(host[r] == host[3]);
+    }
+    g.set_protocol(0);
     std::printf("gpu ok (%.1f us wall)\n", w * 1e6);
   }
   std::printf("consumer ok\n");
