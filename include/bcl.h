@@ -184,7 +184,8 @@ bcl_status_t bcl_comm_plan(bcl_comm_t c, const bcl_config_t* config, int root, u
                            uint64_t* slice_bytes, uint32_t* n_chunks, int* ctas);
 /* Pipelined-chain transport protocol: 0 auto (line protocols up to their
  * caps -- LL128 when every rank has its own GPU, up to the table's measured
- * "# bcl-ll128-upto" rule and BCL_LL128_MAX, default 128 MiB, else LL,
+ * "# bcl-ll128-upto" rule and BCL_LL128_MAX, default 32 MiB at n = 2 and
+ * 512 MiB from n = 3, else LL,
  * BCL_LL_CHAIN_MAX, default 8 MiB -- and above them the table's measured
  * "# bcl-push-from" rule), 1 pull (consumers load from the
  * upstream buffer), 2 push (producers store into the downstream buffer),

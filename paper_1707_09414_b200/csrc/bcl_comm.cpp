@@ -178,10 +178,15 @@ std::uint64_t ll_chain_cap(const GroupOptions& opt) {
                                                    : opt.ll_chain_max_bytes;
   return static_cast<std::uint64_t>(std::min<std::int64_t>(v, 64ll << 20)) / 16 * 16;
 }
-std::uint64_t ll128_cap(const GroupOptions& opt) {
-  const std::int64_t v = opt.ll128_max_bytes < 0 ? static_cast<std::int64_t>(dev::kLL128MaxBytes)
-                                                 : opt.ll128_max_bytes;
-  return static_cast<std::uint64_t>(std::clamp<std::int64_t>(v, 0, 256ll << 20));
+// LL128 landing area: 2 halves x cap x 128/120 bytes per rank. Default cap
+// by rank count: LL128 wins up to the tuner's measured rule, 24 MB at n = 2
+// but beyond 512 MiB at n = 4 (256 MiB: 427 vs 472 us pull; 512 MiB: 841 vs
+// 902 us, profiles/round1/ll128_big/), so 32 MiB for n = 2 (68 MiB per rank)
+// and 512 MiB from n = 3 on (~1.07 GiB per rank of 180 GB).
+std::uint64_t ll128_cap(int n, const GroupOptions& opt) {
+  const std::int64_t dflt = n <= 2 ? (32ll << 20) : static_cast<std::int64_t>(dev::kLL128MaxBytes);
+  const std::int64_t v = opt.ll128_max_bytes < 0 ? dflt : opt.ll128_max_bytes;
+  return static_cast<std::uint64_t>(std::clamp<std::int64_t>(v, 0, 1ll << 30));
 }
 
 }  // namespace
@@ -234,7 +239,7 @@ std::shared_ptr<Group> Group::create_local(const std::vector<int>& devices, cons
   g->ll128_ok_ = n >= 2 && static_cast<int>(g->by_device_.size()) == n;
   g->ll_max_ = ll_cap(n, opt);
   g->ll_chain_max_ = ll_chain_cap(opt);
-  g->ll128_max_ = ll128_cap(opt);
+  g->ll128_max_ = g->ll128_ok_ ? ll128_cap(n, opt) : 0;  // no LL128 area when ranks share a GPU
   g->local_.resize(static_cast<std::size_t>(n));
   for (int r = 0; r < n; ++r) {
     LocalRank& lr = g->local_[static_cast<std::size_t>(r)];
@@ -274,7 +279,7 @@ std::shared_ptr<Group> Group::create_rank(int n, int rank, int device, std::size
   g->lanes_alloc_ = g->lanes_;
   g->ll_max_ = ll_cap(n, opt);
   g->ll_chain_max_ = ll_chain_cap(opt);
-  g->ll128_max_ = ll128_cap(opt);
+  g->ll128_max_ = ll128_cap(n, opt);
   g->local_.resize(1);
   g->local_[0].rank = rank;
   g->local_[0].device = device;

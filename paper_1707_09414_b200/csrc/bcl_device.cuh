@@ -31,7 +31,7 @@ constexpr int kThreads = (kWarpsPerCta + 1) * 32;  // + one publisher warp
 constexpr int kMaxStages = 4;    // bulk-copy stages per copy warp
 constexpr std::uint32_t kLLMaxBytes = 2048 * 1024;      // largest LL message (per-group cap may be lower)
 constexpr std::uint32_t kLLChainMaxBytes = 8u << 20;     // default LL pipelined-chain cap
-constexpr std::uint32_t kLL128MaxBytes = 128u << 20;     // default LL128 pipelined-chain cap
+constexpr std::uint32_t kLL128MaxBytes = 512u << 20;     // default LL128 pipelined-chain cap (n >= 3)
 constexpr std::uint32_t kLL128Payload = 120;             // payload bytes per 128-byte LL128 line
 constexpr int kLL128MaxCtas = 444;  // 3 per SM: +4% at 64 MiB n=4 over one per SM (measured)
 constexpr int kLLThreads = 512;
