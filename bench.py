@@ -297,7 +297,8 @@ def bench_single(args, torch):
                      "l2_gbs": round(2 * (n - 1) * m / t / 1e9, 1),
                      "note": f"kernel local_chain_kernel; DRAM-algorithmic bytes P*M per launch (root read once, "
                              f"P-1 copies written; hop re-reads of the previous hop's output are L2 hits), "
-                             f"2(P-1)M through L2; peak {HBM_PEAK_SRC}"},
+                             f"2(P-1)M through L2; traffic = ncu DRAM bytes per launch, below P*M because the "
+                             f"last writes are still in L2 when the kernel ends; peak {HBM_PEAK_SRC}"},
         "cpu_baseline": {"value": round(m / cpu["median_s"] / 1e9, 4), "unit": "GB/s", "cores": cpu["cores"],
                          "kind": cpu["kind"], "sample": cpu["sample"]},
         "e2e": {"value": round(m / e2e_t / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": m,
