@@ -425,11 +425,6 @@ bool Group::use_push(const CallPlan& p, std::uint64_t bytes) const {
   if (opt_.protocol == 2) return true;
   return select_push(table(), n_, bytes);
 }
-// Line protocols for the pipelined chain in auto mode: LL128 (cross-GPU hops
-// only) up to ll128_max_, else 16-byte LL lines up to ll_chain_max_ (the
-// measured table decides between the chain and the other schedules); above
-// them the lane executor. Provenance / timeline recording need the lane
-// executor. Returns 0 (lane executor), 1 (LL) or 2 (LL128).
 // Every rank on this GPU, pipelined chain, auto protocol: the fused
 // flag-free kernel (pull forces the lane executor; timelines need it too).
 bool Group::use_local_chain(const CallPlan& p, const std::vector<int>& locals) const {
@@ -476,6 +471,11 @@ void Group::launch_local_chain(const std::vector<int>& locals, const std::vector
   ck(static_cast<cudaError_t>(bcl::launch_local_chain(P, ctas, stream)), "launch(local chain)");
 }
 
+// Line protocols for the pipelined chain in auto mode: LL128 (every rank on
+// its own GPU) up to the table's ll128 rule and ll128_max_; on one GPU the
+// fused kernel instead; else 16-byte LL lines up to ll_chain_max_; above them
+// the lane executor. Provenance / timeline recording need the lane executor
+// or the fused kernel. Returns 0 (no line protocol), 1 (LL) or 2 (LL128).
 int Group::ll_chain_mode(const CallPlan& p, std::uint64_t bytes, const std::vector<int>& locals) const {
   if (!p.implicit_chain || n_ < 2 || !opt_.ll || bytes == 0) return 0;
   if (opt_.protocol == 1 || opt_.protocol == 2) return 0;
