@@ -52,8 +52,8 @@ def test_one_process_all_gpus_every_algorithm_and_root():
     comms = B.Comm.local(devices, timeout_s=10)
     assert comms[0].protocol_caps()["ll128"] == (512 << 20 if len(devices) > 2 else 32 << 20)  # own GPU each
     rng = random.Random(17)
-    for algo in ("chain_pipelined", "chain_pipelined/ll", "chain_pipelined/pull", "knomial",
-                 "scatter_ring_allgather", "direct", "chain"):
+    for algo in ("chain_pipelined", "chain_pipelined/ll", "chain_pipelined/pull", "chain_pipelined/push",
+                 "knomial", "scatter_ring_allgather", "direct", "chain"):
         algo, _, protocol = algo.partition("/")
         for c in comms:
             c.set_protocol(protocol or "auto")  # auto: LL128 lines up to 32 MiB; pull: the lane executor
@@ -61,9 +61,10 @@ def test_one_process_all_gpus_every_algorithm_and_root():
             big = (8 << 20) - 3 if protocol == "ll" else (8 << 20) + 5  # the LL chain cap is 8 MiB
             for m in (0, 4, 4097, 1 << 20, rng.randrange(1, 5 << 20), big):
                 run_group(comms, devices, algo, root, m, chunk=max(1, m // 5 + 3), seed=m + root)
-    for c in comms:
-        c.set_protocol("auto")
-    run_group(comms, devices, "chain_pipelined", 0, 64 << 20, chunk=512 << 10, seed=5)
+    for protocol in ("push", "auto"):  # full size on the producer-store path too
+        for c in comms:
+            c.set_protocol(protocol)
+        run_group(comms, devices, "chain_pipelined", 0, 64 << 20, chunk=512 << 10, seed=5)
 
 
 @needs2
