@@ -23,8 +23,11 @@ HARNESS = os.path.join(ROOT, "oracle", "_ref", "ref_harness")
 
 def main():
     raw, seen = [], set()
+    want = os.environ.get("FIT_PROTO")  # e.g. pull: only the lane executor's measurements
     for r in csv.DictReader(open(sys.argv[1])):  # first measurement of a point = the default protocol
-        if r.get("protocol", "auto") != "auto":
+        if want is not None and r.get("protocol", "auto") != want:
+            continue
+        if want is None and r.get("protocol", "auto") != "auto":
             continue
         key = (r["algorithm"], r["radix"], r["chunk_bytes"], r["n"], r["bytes"])
         if key not in seen:
