@@ -205,3 +205,19 @@ def test_builtin_table_is_valid_and_covers_2_4_8():
     for n in (2, 4, 8):
         for m in (4, 4096, 1 << 20, 64 << 20, 1 << 30):
             B.select(t, n, m)
+
+
+def test_builtin_table_is_the_merge_of_the_measured_tables():
+    """paper_1707_09414_b200/tables/b200_default.csv (compiled into the
+    library) is exactly tools/merge_tables.py over the per-n measured tables,
+    and the library's builtin table carries its transport rules."""
+    tdir = os.path.join(ROOT, "paper_1707_09414_b200", "tables")
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "merged.csv")
+        subprocess.run(["python", os.path.join(ROOT, "tools", "merge_tables.py"), out,
+                        os.path.join(tdir, "b200_measured_n2.csv"), os.path.join(tdir, "b200_measured_n4.csv")],
+                       check=True, capture_output=True)
+        assert open(out).read() == open(os.path.join(tdir, "b200_default.csv")).read()
+    text = B.builtin_table().text()
+    assert text == open(os.path.join(tdir, "b200_default.csv")).read()
+    assert "# bcl-ll128-upto: n=4" in text and "# bcl-push-from: n=4" in text

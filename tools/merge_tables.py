@@ -14,6 +14,8 @@ for p in inputs:
     push += [l for l in text[1:] if l.startswith(("# bcl-push-from:", "# bcl-ll128-upto:"))]
     rows += [l for l in text[1:] if l.strip() and not l.startswith("#") and not l.startswith("n,")]
 rows.sort(key=lambda l: (int(l.split(",")[0]), int(l.split(",")[1])))
+# the library's writer order: push rules, then LL128 rules (each by n)
+push.sort(key=lambda l: (not l.startswith("# bcl-push-from:"), int(l.split("n=")[1].split()[0])))
 header = "# bcl-oracle: measured " + " | ".join(prov) + "".join("\n" + l for l in push)
 text = header + "\nn,msg_min_bytes,msg_max_bytes,algorithm,radix,chunk_bytes,predicted_cost_s\n" + "\n".join(rows) + "\n"
 B.load_table_text(text)  # validates ordering / disjoint ranges
