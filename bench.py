@@ -13,10 +13,10 @@ Workloads
   N>1  the same 64 MiB / 512 KiB pipelined chain over N GPUs (one process
        each, buffers in the CUDA-IPC symmetric heap, pulls over NVLink), plus
        the 4 B - 1 GiB sweep with the tuned algorithm per size next to
-       torch.distributed.broadcast (NCCL) on the same buffers.
+       ncclBroadcast (called directly on the same stream and buffers).
 
 Method (osu_bcast as bcastlab bench, proj/tools/bcastlab.cpp:147-206): per
-step non-root buffers are zeroed, L2 is flushed (256 MiB write), ranks meet
+step non-root buffers are zeroed, L2 is flushed (256 MiB read), ranks meet
 at a device barrier, the broadcast is timed with CUDA events on its stream,
 every buffer is verified before the time is kept; per-step latency is the
 max over ranks. One JSON line on rank 0.
@@ -100,9 +100,116 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.sm)}
 
 
+class NvlinkCounters:
+    """NVLink bytes per direction of one GPU from NVML's per-link counters
+    (NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES / _RCV_BYTES, summed over links):
+    the traffic figure of a cross-GPU kernel, read around a run of
+    back-to-back broadcasts (ncu cannot profile kernels that wait on another
+    rank's kernel)."""
+
+    XMIT, RCV, LINKS = 202, 204, 18
+
+    def __init__(self, gpu):
+        self.h = None
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[gpu]) if vis and vis.split(",")[gpu].isdigit() else gpu
+            self.nv, self.h = nv, nv.nvmlDeviceGetHandleByIndex(idx)
+            self.read()
+        except Exception:  # noqa: BLE001 - no NVML / no NVLink counters
+            self.h = None
+
+    def read(self):
+        """(tx_bytes, rx_bytes) summed over links, or None."""
+        if self.h is None:
+            return None
+        ids = [(f, l) for f in (self.XMIT, self.RCV) for l in range(self.LINKS)]
+        vals = self.nv.nvmlDeviceGetFieldValues(self.h, ids)
+        tx = rx = 0
+        for i, v in enumerate(vals):
+            if v.nvmlReturn != 0:
+                continue
+            if i < self.LINKS:
+                tx += v.value.ullVal
+            else:
+                rx += v.value.ullVal
+        return tx, rx
+
+
+class NcclDirect:
+    """ncclBroadcast called directly (nccl-tests style) on our stream and our
+    buffers: the NCCL torch bundles (libnccl.so.2), its own communicator
+    (unique id shared over torch.distributed), no ProcessGroup stream hop."""
+
+    def __init__(self, torch, rank, world):
+        import ctypes as C
+        import torch.distributed as dist
+        path = None
+        try:
+            import nvidia.nccl
+            path = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
+        except ImportError:
+            pass
+        self.C = C
+        self.lib = C.CDLL(path if path and os.path.exists(path) else "libnccl.so.2")
+
+        class UniqueId(C.Structure):
+            _fields_ = [("internal", C.c_char * 128)]
+        uid = UniqueId()
+        if rank == 0:
+            self._ok(self.lib.ncclGetUniqueId(C.byref(uid)))
+        blob = [bytes(uid.internal) if rank == 0 else None]
+        dist.broadcast_object_list(blob, src=0)
+        C.memmove(C.addressof(uid), blob[0], 128)
+        self.comm = C.c_void_p()
+        self._ok(self.lib.ncclCommInitRank(C.byref(self.comm), world, uid, rank))
+        v = C.c_int()
+        self.lib.ncclGetVersion(C.byref(v))
+        self.version = v.value
+        self.lib.ncclBroadcast.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_int, C.c_void_p,
+                                           C.c_void_p]
+
+    def _ok(self, r):
+        if r != 0:
+            raise RuntimeError(f"NCCL error {r}")
+
+    def bcast(self, buf, nbytes, root, stream):
+        p = buf.data_ptr()
+        self._ok(self.lib.ncclBroadcast(p, p, nbytes, 1, root, self.comm, stream.cuda_stream))  # ncclUint8
+
+    def close(self):
+        if self.comm:
+            self.lib.ncclCommDestroy(self.comm)
+            self.comm = None
+
+
+def host_cpu():
+    """Host core count and CPU model of this box (for the CPU baseline)."""
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
+
+
+def verdict(ours, theirs, tie=0.03):
+    """win / tie / loss on medians; within 3% is a tie."""
+    if ours <= theirs * (1 - tie):
+        return "win"
+    if ours >= theirs * (1 + tie):
+        return "loss"
+    return "tie"
+
+
 # ----------------------------------------------------------------- CPU legs
 
-def reference_cpu(n, m, chunk, iters, warmup=1, seed=1):
+def reference_cpu(n, m, chunk, iters, warmup=1, seed=1):  # noqa: C901
     """The reference's own CPU broadcast (oracle/_ref, unmodified bcastlab
     sources) timed with the osu method on this host: n rank threads."""
     harness = os.path.join(ROOT, "oracle", "_ref", "ref_harness")
@@ -156,7 +263,7 @@ def workload_config(n, m, chunk, world):
         wl = (f"bcast over {world} B200 (one process per GPU, NVLink P2P), {m >> 20} MiB float32, root 0, "
               f"tuner-selected algorithm/chunk; sweep 4 B-1 GiB vs NCCL")
     return {"workload": wl, "ranks": n, "bytes": m, "chunk_bytes": chunk, "root": 0,
-            "algorithm": "chain_pipelined", "l2": "flushed between steps (256 MiB write)"}
+            "algorithm": "chain_pipelined", "l2": "flushed between steps (256 MiB read sweep)"}
 
 
 # ----------------------------------------------------------------- GPU legs
@@ -175,6 +282,7 @@ def main():
     ap.add_argument("--workload", default="config1", choices=["config1", "vgg16", "alexnet", "resnet50", "lenet"],
                     help="config1 (default) or a layer-wise parameter broadcast (BASELINE configs 4/5)")
     ap.add_argument("--bucket", type=int, default=0, help="parameter workloads: coalesce tensors into >= this")
+    ap.add_argument("--csv", default=None, help="N>1: write the sweep as the reference bench CSV here")
     ap.add_argument("--fixed-chunk", dest="tuned", action="store_false",
                     help="N>1: pipelined chain with --chunk instead of the tuned selection")
     args = ap.parse_args()
@@ -197,6 +305,13 @@ def main():
 
 
 GATE_CYCLES = 1_000_000  # ~0.5 ms spin: the host enqueues the timed ops behind it
+
+
+def flush_l2(torch, flush):
+    """Evict L2 with a READ sweep of 256 MiB: it writes back the previous
+    step's dirty lines before the timed region and leaves only clean lines
+    (a write sweep left ~126 MB of dirty lines to be written back inside it)."""
+    torch.sum(flush)
 
 
 def time_steps(torch, steps, warmup, prepare, body, verify, stream, align=None):
@@ -236,14 +351,14 @@ def bench_single(args, torch):
     g = torch.Generator(device=dev).manual_seed(1)
     bufs = [torch.zeros(m, dtype=torch.uint8, device=dev) for _ in range(n)]
     bufs[0].copy_(torch.randint(0, 256, (m,), dtype=torch.uint8, device=dev, generator=g))
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = torch.ones(256 << 18, dtype=torch.int32, device=dev)  # 256 MiB > 126 MB L2
     torch.cuda.synchronize()  # setup ran on the default stream; the timed loop uses `stream`
 
     def prepare(it):
         with torch.cuda.stream(stream):
             for r in range(1, n):
                 bufs[r].zero_()
-            flush.fill_(it & 0xFF)
+            flush_l2(torch, flush)
 
     def body(it):
         B.bcast_all(comms, bufs, m, "uint8", 0, cfg, streams=[stream] * n)
@@ -329,10 +444,11 @@ def bench_multi(args, torch, rank, world):
     ref_all = torch.empty(cap, dtype=torch.uint8, device=dev)
     g = torch.Generator(device=dev).manual_seed(1)
     ref_all.copy_(torch.randint(0, 256, (cap,), dtype=torch.uint8, device=dev, generator=g))
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_buf = torch.ones(256 << 18, dtype=torch.int32, device=dev)
+    nccl_direct = NcclDirect(torch, rank, world)
     torch.cuda.synchronize()  # setup ran on the default stream; the timed loop uses `stream`
 
-    def run(size, steps, warmup, ours, cfg=None, flush_l2=True):
+    def run(size, steps, warmup, ours, cfg=None, flush=True):
         buf = buf_all[:size]
         ref = ref_all[:size]
 
@@ -342,8 +458,8 @@ def bench_multi(args, torch, rank, world):
                     buf.copy_(ref)
                 else:
                     buf.zero_()
-                if flush_l2:
-                    flush.fill_(it & 0xFF)
+                if flush:
+                    flush_l2(torch, flush_buf)
             if it == 0:
                 stream.synchronize()
                 dist.barrier(device_ids=[local])
@@ -352,8 +468,7 @@ def bench_multi(args, torch, rank, world):
             if ours:
                 comm.bcast(buf, size, "uint8", 0, cfg, stream=stream)
             else:
-                with torch.cuda.stream(stream):
-                    dist.broadcast(buf, src=0)
+                nccl_direct.bcast(buf, size, 0, stream)
 
         def verify(it):
             return torch.equal(buf, ref)
@@ -375,6 +490,29 @@ def bench_multi(args, torch, rank, world):
         times = run(m, args.steps, args.warmup, True, cfg)
     launches = comm.launches - launches0 - args.warmup
     nccl = run(m, args.steps, args.warmup, False)
+
+    # NVLink bytes per broadcast from NVML counters over a run of
+    # back-to-back calls (device time by CUDA events on the stream).
+    counters = NvlinkCounters(local)
+    reps = 50
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    dist.barrier(device_ids=[local])
+    time.sleep(0.2)
+    c0 = counters.read()
+    ev0.record(stream)
+    for _ in range(reps):
+        comm.bcast(buf_all[:m], m, "uint8", 0, cfg, stream=stream)
+    ev1.record(stream)
+    ev1.synchronize()
+    time.sleep(0.2)
+    c1 = counters.read()
+    loop_t = ev0.elapsed_time(ev1) * 1e-3 / reps
+    nv = torch.tensor([(c1[0] - c0[0]) / reps, (c1[1] - c0[1]) / reps, loop_t] if c0 and c1 else [-1.0, -1.0, loop_t],
+                      dtype=torch.float64, device=dev)
+    nv_all = [torch.zeros_like(nv) for _ in range(world)]
+    dist.all_gather(nv_all, nv)
+    nv_all = [x.cpu().tolist() for x in nv_all]
 
     # e2e through the C-ABI with pinned host buffers (bcl_bcast_host)
     host = torch.empty(m, dtype=torch.uint8, pin_memory=True)
@@ -405,19 +543,41 @@ def bench_multi(args, torch, rank, world):
         while size <= sweep_max:
             steps = 20 if size <= (16 << 20) else 8
             c = comm.choose(size)
-            ours = run(size, steps, 3, True, None, flush_l2=False)
-            theirs = run(size, steps, 3, False, None, flush_l2=False)
+            ours = run(size, steps, 3, True, None, flush=False)
+            theirs = run(size, steps, 3, False, None, flush=False)
             to, tn = statistics.median(ours), statistics.median(theirs)
+            ch = c.chunk_bytes if c.algorithm == B.Algorithm.chain_pipelined else size
+            t_roof = size / LINK_BW + (world - 1) * min(max(ch, 1), size) / LINK_BW
             sweep.append({"bytes": size, "algorithm": c.algorithm.name, "chunk": c.chunk_bytes,
-                          "ours_us": round(to * 1e6, 2), "nccl_us": round(tn * 1e6, 2),
-                          "ours_busbw": round(size / to / 1e9, 2), "nccl_busbw": round(size / tn / 1e9, 2)})
+                          "ours_us": {"min": round(min(ours) * 1e6, 2), "median": round(to * 1e6, 2),
+                                      "max": round(max(ours) * 1e6, 2)},
+                          "nccl_us": {"min": round(min(theirs) * 1e6, 2), "median": round(tn * 1e6, 2),
+                                      "max": round(max(theirs) * 1e6, 2)},
+                          "ours_busbw": round(size / to / 1e9, 2), "nccl_busbw": round(size / tn / 1e9, 2),
+                          "frac_of_chain_roofline": round(t_roof / to, 4) if size >= (1 << 20) else None,
+                          "vs_nccl": verdict(to, tn), "iterations": steps,
+                          "ours_mean_us": round(statistics.mean(ours) * 1e6, 2)})
             size *= 2
+
+    cpu = None
+    if rank == 0:
+        cpu = reference_cpu(world, m, cfg.chunk_bytes if cfg.algorithm == B.Algorithm.chain_pipelined else chunk,
+                            max(3, args.cpu_iters // 2))
+    dist.barrier(device_ids=[local])
 
     if rank == 0:
         t = statistics.mean(times)
         t_nccl = statistics.mean(nccl)
         busbw = m / t / 1e9
         t_roof = m / LINK_BW + (world - 1) * max(cfg.chunk_bytes, 1) / LINK_BW
+        rx = [x[1] for x in nv_all]
+        tx = [x[0] for x in nv_all]
+        have_nv = all(v >= 0 for v in rx + tx)
+        link = {"per_rank": [{"rank": r, "tx_bytes_per_call": round(x[0]), "rx_bytes_per_call": round(x[1]),
+                              "call_us": round(x[2] * 1e6, 2),
+                              "tx_gbs": round(x[0] / x[2] / 1e9, 1), "rx_gbs": round(x[1] / x[2] / 1e9, 1)}
+                             for r, x in enumerate(nv_all)] if have_nv else None,
+                "source": "NVML NVLink per-link XMIT/RCV byte counters over %d back-to-back calls" % reps}
         line = {
             "metric": METRIC, "value": round(busbw, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t * 1e3, 4), "higher_is_better": True, "scaling": "weak",
@@ -425,13 +585,21 @@ def bench_multi(args, torch, rank, world):
             "config": dict(workload_config(world, m, cfg.chunk_bytes, world), algorithm=cfg.algorithm.name,
                            selection="tuned (builtin measured table)" if args.tuned else "fixed"),
             "latency_us": {"mean": round(t * 1e6, 2), "min": round(min(times) * 1e6, 2),
-                           "median": round(statistics.median(times) * 1e6, 2)},
+                           "median": round(statistics.median(times) * 1e6, 2), "max": round(max(times) * 1e6, 2)},
             "nccl": {"busbw": round(m / t_nccl / 1e9, 2), "latency_us": round(t_nccl * 1e6, 2),
-                     "impl": "torch.distributed.broadcast (NCCL %s)" % ".".join(map(str, torch.cuda.nccl.version()))},
+                     "median_us": round(statistics.median(nccl) * 1e6, 2), "vs_ours": verdict(t, t_nccl),
+                     "impl": "ncclBroadcast called directly on the same stream and buffers (NCCL %d)"
+                             % nccl_direct.version},
             "roofline": {"bound": "nvlink", "achieved": round(busbw, 1), "peak": LINK_BW / 1e9, "unit": "GB/s",
-                         "frac": round(busbw / (LINK_BW / 1e9), 4), "traffic": None,
+                         "frac": round(busbw / (LINK_BW / 1e9), 4),
+                         "traffic": round(max(rx)) if have_nv else None,
+                         "traffic_note": "max over ranks of NVLink bytes received per call (NVML counters); "
+                                         "algorithmic: M = %d per receiving GPU" % m,
                          "chain_roofline_us": round(t_roof * 1e6, 2), "frac_of_chain_roofline": round(t_roof / t, 4),
                          "note": "per-GPU ingress M/t vs NVLink-5 900 GB/s per direction (north_star)"},
+            "nvlink": link,
+            "cpu_baseline": {"value": round(m / cpu["median_s"] / 1e9, 4), "unit": "GB/s", "cores": cpu["cores"],
+                             "kind": cpu["kind"], "sample": cpu["sample"], "host": host_cpu()},
             "e2e": {"value": round(m / statistics.mean(e2e) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": m,
                     "d2h_bytes_per_step": (world - 1) * m, "latency_ms": round(statistics.mean(e2e) * 1e3, 3),
                     "path": "bcl_bcast_host (C-ABI) per rank, pinned host buffers"},
@@ -439,10 +607,27 @@ def bench_multi(args, torch, rank, world):
             "clocks": clk.summary(),
             "sweep": sweep,
         }
+        if sweep:
+            line["sweep_vs_nccl"] = {k: sum(1 for e in sweep if e["vs_nccl"] == k) for k in ("win", "tie", "loss")}
+            csv_path = args.csv or (os.path.join("gpurun_out", f"bench_sweep_n{world}.csv")
+                                    if os.path.isdir("gpurun_out") else None)
+            if csv_path:
+                write_bench_csv(csv_path, sweep)
         print(json.dumps(line), flush=True)
     dist.barrier(device_ids=[local])
+    nccl_direct.close()
     comm.close()
     dist.destroy_process_group()
+
+
+def write_bench_csv(path, sweep):
+    """The reference bench's CSV (proj/tools/bcastlab.cpp:284-303):
+    size_bytes,algorithm,chunk_bytes,avg_us,min_us,max_us,iterations."""
+    with open(path, "w") as f:
+        f.write("size_bytes,algorithm,chunk_bytes,avg_us,min_us,max_us,iterations\n")
+        for e in sweep:
+            f.write("%d,%s,%d,%.3f,%.3f,%.3f,%d\n" % (e["bytes"], e["algorithm"], e["chunk"], e["ours_mean_us"],
+                                                     e["ours_us"]["min"], e["ours_us"]["max"], e["iterations"]))
 
 
 def bench_params(args, torch, rank, world):
@@ -465,6 +650,7 @@ def bench_params(args, torch, rank, world):
     ref = torch.randint(0, 256, (pb.total_bytes,), dtype=torch.uint8, device=dev, generator=g)
     views = [flat[o:o + n] for o, n in pb.msgs]
     stream = torch.cuda.Stream(device=dev)
+    nccl_direct = NcclDirect(torch, rank, world)
     torch.cuda.synchronize()
     roots = [0] if args.workload == "vgg16" else [world - 1, world // 2]
     results = {}
@@ -484,9 +670,8 @@ def bench_params(args, torch, rank, world):
                 if impl == "ours":
                     pb.bcast(comm, flat, root, stream)
                 else:
-                    with torch.cuda.stream(stream):
-                        for v in views:
-                            dist.broadcast(v, src=root)
+                    for v in views:
+                        nccl_direct.bcast(v, v.numel(), root, stream)
 
             def verify(it):
                 return all(torch.equal(flat[o:o + n], ref[o:o + n]) for o, n in zip(pb.offsets, pb.sizes))
@@ -514,6 +699,7 @@ def bench_params(args, torch, rank, world):
                 "gpu_launches": len(pb.msgs) * args.steps}
         print(json.dumps(line), flush=True)
     dist.barrier(device_ids=[local])
+    nccl_direct.close()
     comm.close()
     dist.destroy_process_group()
 

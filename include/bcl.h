@@ -165,6 +165,25 @@ bcl_status_t bcl_comm_init_all(int n, const int* devices, double timeout_s,
  * bcl_mem_alloc serves broadcast buffers (peers map it via CUDA IPC). */
 bcl_status_t bcl_comm_init_rank(int n, int rank, int device, size_t heap_bytes,
                                 double timeout_s, bcl_comm_t* out);
+/* The same with communicator options, "key=value" pairs separated by ','
+ * (the BCL_* environment variables in lower case without the prefix, which
+ * they override), e.g. "timeout_s=10,stage_bytes=8192,sys_scope=1":
+ *   timeout_s      device wait bound (s)
+ *   protocol       chain transport, as bcl_comm_set_protocol
+ *   stage_bytes    TMA bulk-copy stage per copy warp (0 = 16-byte vector loads;
+ *                  default 8192 across GPUs, 0 when every rank shares one GPU)
+ *   sys_scope      1: system-scope flag polls and fences even when every rank
+ *                  shares one GPU (the cross-GPU code path on one device)
+ *   strict_sys     1: system-scope fence in the publisher before every flag
+ *   writer_fence   0 publisher fences, 1 gpu scope, 2 the call's scope (default)
+ *   ll128          -1 auto (ranks on distinct GPUs), 0 off, 1 also between
+ *                  ranks sharing a GPU;  ll128_max, ll_chain_max, ll_max caps
+ *   window_bytes, min_slice, max_ctas, stages, poll_ns, host_piece, ll,
+ *   eager_post, local_fused, local_ctas, local_item  (tuning knobs)
+ * Unknown keys fail with BCL_ERR_INVALID_ARGUMENT. New on B200. */
+bcl_status_t bcl_comm_init_all_opts(int n, const int* devices, const char* options, bcl_comm_t* out);
+bcl_status_t bcl_comm_init_rank_opts(int n, int rank, int device, size_t heap_bytes, const char* options,
+                                     bcl_comm_t* out);
 bcl_status_t bcl_comm_export(bcl_comm_t c, void* blob, size_t cap, size_t* len);
 bcl_status_t bcl_comm_connect(bcl_comm_t c, const void* blobs, size_t blob_len);
 bcl_status_t bcl_comm_destroy(bcl_comm_t c);

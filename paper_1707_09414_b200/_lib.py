@@ -91,6 +91,8 @@ _SIGS = {
     "bcl_table_select": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.POINTER(_Config)]),
     "bcl_comm_init_all": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.c_double, C.POINTER(C.c_void_p)]),
     "bcl_comm_init_rank": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_size_t, C.c_double, C.POINTER(C.c_void_p)]),
+    "bcl_comm_init_all_opts": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.c_char_p, C.POINTER(C.c_void_p)]),
+    "bcl_comm_init_rank_opts": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_size_t, C.c_char_p, C.POINTER(C.c_void_p)]),
     "bcl_comm_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "bcl_comm_connect": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
     "bcl_comm_destroy": (C.c_int, [C.c_void_p]),

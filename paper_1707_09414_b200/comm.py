@@ -37,6 +37,13 @@ def _dtype(d) -> int:
     return DTYPES[str(d).replace("torch.", "")]
 
 
+def _options(timeout_s, options) -> bytes:
+    items = dict(options)
+    if timeout_s and timeout_s > 0:
+        items.setdefault("timeout_s", timeout_s)
+    return ",".join(f"{k}={int(v) if isinstance(v, bool) else v}" for k, v in items.items()).encode()
+
+
 def _cfg(config: Optional[AlgorithmConfig]):
     return C.byref(config._c()) if config is not None else None
 
@@ -61,26 +68,35 @@ class Comm:
 
     # ------------------------------------------------------------ creation
     @staticmethod
-    def local(devices: Sequence[int], timeout_s: float = 0.0) -> List["Comm"]:
-        """One process drives len(devices) ranks (rank r on devices[r])."""
+    def local(devices: Sequence[int], timeout_s: float = 0.0, **options) -> List["Comm"]:
+        """One process drives len(devices) ranks (rank r on devices[r]).
+        options: communicator options of bcl_comm_init_all_opts (include/bcl.h),
+        e.g. stage_bytes=8192, sys_scope=1, ll128=1."""
         n = len(devices)
         out = (C.c_void_p * n)()
         devs = (C.c_int * n)(*devices)
-        _check(lib().bcl_comm_init_all(n, devs, timeout_s, out))
+        if options:
+            _check(lib().bcl_comm_init_all_opts(n, devs, _options(timeout_s, options), out))
+        else:
+            _check(lib().bcl_comm_init_all(n, devs, timeout_s, out))
         return [Comm(C.c_void_p(out[i])) for i in range(n)]
 
     @staticmethod
-    def rank(n: int, rank: int, device: int, heap_bytes: int = 0, timeout_s: float = 0.0) -> "Comm":
+    def rank(n: int, rank: int, device: int, heap_bytes: int = 0, timeout_s: float = 0.0, **options) -> "Comm":
         """One process per GPU; call export()/connect() (or use connect_torch)."""
         h = C.c_void_p()
-        _check(lib().bcl_comm_init_rank(n, rank, device, heap_bytes, timeout_s, C.byref(h)))
+        if options:
+            _check(lib().bcl_comm_init_rank_opts(n, rank, device, heap_bytes, _options(timeout_s, options),
+                                                 C.byref(h)))
+        else:
+            _check(lib().bcl_comm_init_rank(n, rank, device, heap_bytes, timeout_s, C.byref(h)))
         return Comm(h)
 
     @staticmethod
     def connect_torch(n: int, rank: int, device: int, heap_bytes: int = 0, timeout_s: float = 0.0,
-                      group=None) -> "Comm":
+                      group=None, **options) -> "Comm":
         """init_rank + an all_gather of the IPC blobs over torch.distributed."""
-        c = Comm.rank(n, rank, device, heap_bytes, timeout_s)
+        c = Comm.rank(n, rank, device, heap_bytes, timeout_s, **options)
         c.connect(exchange_blobs(c.export(), group))
         return c
 

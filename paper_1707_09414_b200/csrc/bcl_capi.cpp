@@ -362,6 +362,28 @@ bcl_status_t bcl_comm_init_rank(int n, int rank, int device, size_t heap_bytes, 
   });
 }
 
+bcl_status_t bcl_comm_init_all_opts(int n, const int* devices, const char* options, bcl_comm_t* out) {
+  return guard([&] {
+    need(devices, "devices");
+    need(out, "out");
+    if (n < 1) throw std::invalid_argument("rank count must be >= 1");
+    bcl::GroupOptions opt = bcl::GroupOptions::from_env();
+    if (options) opt.apply(options);
+    auto g = bcl::Group::create_local(std::vector<int>(devices, devices + n), opt);
+    for (int r = 0; r < n; ++r) out[r] = new bcl_comm_s{g, r};
+  });
+}
+
+bcl_status_t bcl_comm_init_rank_opts(int n, int rank, int device, size_t heap_bytes, const char* options,
+                                     bcl_comm_t* out) {
+  return guard([&] {
+    need(out, "out");
+    bcl::GroupOptions opt = bcl::GroupOptions::from_env();
+    if (options) opt.apply(options);
+    *out = new bcl_comm_s{bcl::Group::create_rank(n, rank, device, heap_bytes, opt), 0};
+  });
+}
+
 bcl_status_t bcl_comm_export(bcl_comm_t c, void* blob, size_t cap, size_t* len) {
   return guard([&] {
     need(c, "comm");

@@ -2,6 +2,7 @@
 #include "bcl_comm.hpp"
 
 #include <algorithm>
+#include <cctype>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -69,30 +70,73 @@ std::string format_failures(const std::vector<RankFailure>& f) {
 
 }  // namespace
 
+namespace {
+
+// One setter per option, shared by the BCL_* environment variables and the
+// options string of bcl_comm_init_*_opts (key = the variable name without
+// the BCL_ prefix, lower case).
+void set_option(GroupOptions& o, const std::string& key, const std::string& v) {
+  const char* s = v.c_str();
+  auto u64 = [&] { return std::strtoull(s, nullptr, 10); };
+  auto i64 = [&] { return std::strtoll(s, nullptr, 10); };
+  auto i32 = [&] { return std::atoi(s); };
+  if (key == "poll_ns") o.poll_ns = static_cast<std::uint32_t>(u64());
+  else if (key == "window_bytes") o.window_bytes = std::max<std::uint64_t>(16, u64());
+  else if (key == "min_slice") o.min_slice = std::max<std::uint64_t>(16, u64());
+  else if (key == "max_ctas") o.max_ctas_per_rank = i32();
+  else if (key == "strict_sys") o.strict_sys = i32() != 0;
+  else if (key == "sys_scope") o.sys_scope = i32();
+  else if (key == "eager_post") o.eager_post = i32() != 0;
+  else if (key == "writer_fence") {
+    o.writer_fence = i32();
+    if (o.writer_fence < 0 || o.writer_fence > 2) throw std::invalid_argument("writer_fence must be 0, 1 or 2");
+  } else if (key == "local_fused") o.local_fused = i32() != 0;
+  else if (key == "local_ctas") o.local_ctas = i32();
+  else if (key == "local_item") o.local_item = u64();
+  else if (key == "ll") o.ll = i32() != 0;
+  else if (key == "ll128") o.ll128 = i32();
+  else if (key == "protocol") {
+    o.protocol = i32();
+    if (o.protocol < 0 || o.protocol > 4) throw std::invalid_argument("protocol must be 0..4");
+  } else if (key == "ll_max") o.ll_max_bytes = u64();
+  else if (key == "ll_chain_max") o.ll_chain_max_bytes = i64();
+  else if (key == "ll128_max") o.ll128_max_bytes = i64();
+  else if (key == "host_piece") o.host_piece = std::max<std::uint64_t>(4096, u64());
+  else if (key == "stages") o.stages = static_cast<std::uint32_t>(std::clamp(i32(), 2, dev::kMaxStages));
+  else if (key == "stage_bytes") o.stage_bytes = i64() < 0 ? -1 : i64() / 16 * 16;
+  else if (key == "timeout_s") o.timeout_ns = static_cast<std::uint64_t>(std::strtod(s, nullptr) * 1e9);
+  else throw std::invalid_argument("unknown communicator option '" + key + "'");
+}
+
+constexpr const char* kOptionNames[] = {
+    "poll_ns", "window_bytes", "min_slice", "max_ctas", "strict_sys", "sys_scope", "eager_post", "writer_fence",
+    "local_fused", "local_ctas", "local_item", "ll", "ll128", "protocol", "ll_max", "ll_chain_max", "ll128_max",
+    "host_piece", "stages", "stage_bytes"};
+
+}  // namespace
+
 GroupOptions GroupOptions::from_env() {
   GroupOptions o;
-  if (const char* v = std::getenv("BCL_POLL_NS")) o.poll_ns = static_cast<std::uint32_t>(std::strtoul(v, nullptr, 10));
-  if (const char* v = std::getenv("BCL_WINDOW_BYTES")) o.window_bytes = std::max<std::uint64_t>(16, std::strtoull(v, nullptr, 10));
-  if (const char* v = std::getenv("BCL_MIN_SLICE")) o.min_slice = std::max<std::uint64_t>(16, std::strtoull(v, nullptr, 10));
-  if (const char* v = std::getenv("BCL_MAX_CTAS")) o.max_ctas_per_rank = std::atoi(v);
-  if (const char* v = std::getenv("BCL_STRICT_SYS")) o.strict_sys = std::atoi(v) != 0;
-  if (const char* v = std::getenv("BCL_EAGER_POST")) o.eager_post = std::atoi(v) != 0;
-  if (const char* v = std::getenv("BCL_WRITER_FENCE")) o.writer_fence = std::atoi(v) != 0;
-  if (const char* v = std::getenv("BCL_LOCAL_FUSED")) o.local_fused = std::atoi(v) != 0;
-  if (const char* v = std::getenv("BCL_LOCAL_CTAS")) o.local_ctas = std::atoi(v);
-  if (const char* v = std::getenv("BCL_LOCAL_ITEM")) o.local_item = std::strtoull(v, nullptr, 10);
-  if (const char* v = std::getenv("BCL_LL")) o.ll = std::atoi(v) != 0;
-  if (const char* v = std::getenv("BCL_PROTOCOL")) {
-    o.protocol = std::atoi(v);
-    if (o.protocol < 0 || o.protocol > 4) throw std::invalid_argument("BCL_PROTOCOL must be 0..4");
+  for (const char* name : kOptionNames) {
+    std::string env = "BCL_";
+    for (const char* c = name; *c; ++c) env += static_cast<char>(std::toupper(static_cast<unsigned char>(*c)));
+    if (const char* v = std::getenv(env.c_str())) set_option(o, name, v);
   }
-  if (const char* v = std::getenv("BCL_LL_MAX")) o.ll_max_bytes = std::strtoull(v, nullptr, 10);
-  if (const char* v = std::getenv("BCL_LL_CHAIN_MAX")) o.ll_chain_max_bytes = std::strtoll(v, nullptr, 10);
-  if (const char* v = std::getenv("BCL_LL128_MAX")) o.ll128_max_bytes = std::strtoll(v, nullptr, 10);
-  if (const char* v = std::getenv("BCL_HOST_PIECE")) o.host_piece = std::max<std::uint64_t>(4096, std::strtoull(v, nullptr, 10));
-  if (const char* v = std::getenv("BCL_STAGES")) o.stages = static_cast<std::uint32_t>(std::clamp(std::atoi(v), 2, dev::kMaxStages));
-  if (const char* v = std::getenv("BCL_STAGE_BYTES")) o.stage_bytes = static_cast<std::int64_t>(std::strtoul(v, nullptr, 10)) / 16 * 16;
   return o;
+}
+
+void GroupOptions::apply(const std::string& options) {
+  std::size_t at = 0;
+  while (at < options.size()) {
+    std::size_t end = options.find_first_of(",; ", at);
+    if (end == std::string::npos) end = options.size();
+    const std::string item = options.substr(at, end - at);
+    at = end + 1;
+    if (item.empty()) continue;
+    const std::size_t eq = item.find('=');
+    if (eq == std::string::npos || eq == 0) throw std::invalid_argument("option '" + item + "' is not key=value");
+    set_option(*this, item.substr(0, eq), item.substr(eq + 1));
+  }
 }
 
 std::size_t dtype_size(DataType t) {
@@ -134,6 +178,12 @@ void Group::alloc_rank(LocalRank& r, std::size_t heap_bytes) {
     r.heap_bytes = heap_bytes;
   }
   ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+}
+
+void Group::cache_device_limits(int device) {
+  DeviceScope ds(device);
+  ck(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device), "sm count");
+  ck(static_cast<cudaError_t>(local_chain_occupancy(&local_chain_occ_)), "occupancy(local chain)");
 }
 
 void Group::upload_peers(LocalRank& r) {
@@ -236,10 +286,14 @@ std::shared_ptr<Group> Group::create_local(const std::vector<int>& devices, cons
   }
   g->lanes_alloc_ = g->lanes_;
   g->single_device_ = g->by_device_.size() == 1;
-  g->ll128_ok_ = n >= 2 && static_cast<int>(g->by_device_.size()) == n;
+  g->sys_ = !g->single_device_ || opt.sys_scope == 1;
+  // LL128 lines cross NVLink when every rank owns its GPU; opt.ll128 = 1 also
+  // runs them through L2 between ranks sharing a GPU (one cooperative launch).
+  g->ll128_ok_ = n >= 2 && opt.ll128 != 0 && (static_cast<int>(g->by_device_.size()) == n || opt.ll128 == 1);
   g->ll_max_ = ll_cap(n, opt);
   g->ll_chain_max_ = ll_chain_cap(opt);
-  g->ll128_max_ = g->ll128_ok_ ? ll128_cap(n, opt) : 0;  // no LL128 area when ranks share a GPU
+  g->ll128_max_ = g->ll128_ok_ ? ll128_cap(n, opt) : 0;  // no LL128 area without LL128
+  g->cache_device_limits(devices[0]);
   g->local_.resize(static_cast<std::size_t>(n));
   for (int r = 0; r < n; ++r) {
     LocalRank& lr = g->local_[static_cast<std::size_t>(r)];
@@ -277,9 +331,11 @@ std::shared_ptr<Group> Group::create_rank(int n, int rank, int device, std::size
   if (g->opt_.window_bytes == 0) g->opt_.window_bytes = 4ull << 20;
   g->lanes_ = lanes_for(device, 1, opt.max_ctas_per_rank, g->opt_);
   g->lanes_alloc_ = g->lanes_;
+  g->sys_ = n > 1 || opt.sys_scope == 1;
   g->ll_max_ = ll_cap(n, opt);
   g->ll_chain_max_ = ll_chain_cap(opt);
-  g->ll128_max_ = ll128_cap(n, opt);
+  g->ll128_max_ = opt.ll128 != 0 ? ll128_cap(n, opt) : 0;
+  g->cache_device_limits(device);
   g->local_.resize(1);
   g->local_[0].rank = rank;
   g->local_[0].device = device;
@@ -334,7 +390,15 @@ void Group::connect(const std::vector<std::vector<std::uint8_t>>& infos) {
     lanes = std::min(lanes, static_cast<int>(all[i].lanes));
   }
   lanes_ = lanes;
-  ll128_ok_ = n_ >= 2;
+  {
+    // Plans computed before connect (bcl_comm_plan) used this rank's own lane
+    // count; every rank must plan with the group minimum.
+    std::lock_guard<std::mutex> lock(plan_mu_);
+    plans_.clear();
+  }
+  // Processes sharing a GPU run separate launches that wait on one another:
+  // no LL128 (and no guarantee of co-residency either).
+  ll128_ok_ = n_ >= 2 && ll128_max_ > 0;
   for (std::size_t i = 0; i < all.size(); ++i) {
     for (std::size_t j = 0; j < i; ++j) {
       if (std::memcmp(&all[i].uuid, &all[j].uuid, sizeof(cudaUUID_t)) == 0) ll128_ok_ = false;
@@ -427,11 +491,13 @@ bool Group::use_push(const CallPlan& p, std::uint64_t bytes) const {
 }
 // Every rank on this GPU, pipelined chain, auto protocol: the fused
 // flag-free kernel (pull forces the lane executor; timelines need it too).
+// (The timeline hook needs the lane executor: single-process groups only, so
+// every rank takes the same decision.)
 bool Group::use_local_chain(const CallPlan& p, const std::vector<int>& locals) const {
   if (!single_device_ || !p.implicit_chain || opt_.protocol != 0 || !opt_.local_fused) return false;
   if (static_cast<int>(locals.size()) != n_ || n_ < 2) return false;
-  for (int li : locals) {
-    if (local_[static_cast<std::size_t>(li)].trace != nullptr) return false;
+  for (const LocalRank& r : local_) {
+    if (r.trace != nullptr) return false;
   }
   return true;
 }
@@ -455,18 +521,14 @@ void Group::launch_local_chain(const std::vector<int>& locals, const std::vector
     if (e != epoch) throw std::runtime_error("ranks sharing a GPU drifted apart in call count");
     ++r.launches;
   }
-  int sms = 0;
   DeviceScope ds(local_[static_cast<std::size_t>(locals[0])].device);
-  ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, local_[static_cast<std::size_t>(locals[0])].device),
-     "sm count");
-  int occ = 0;
-  ck(static_cast<cudaError_t>(local_chain_occupancy(&occ)), "occupancy(local chain)");
-  const int ctas = opt_.local_ctas > 0 ? opt_.local_ctas : sms * std::max(occ, 1);
+  const int ctas = opt_.local_ctas > 0 ? opt_.local_ctas : sms_ * std::max(local_chain_occ_, 1);
   const std::uint64_t warps = static_cast<std::uint64_t>(ctas) * 8;
   // ~4 items per warp (load balance; ~3.5 KiB at 64 MiB: 52 us vs 56 us with
   // 7 KiB items, profiles/round1/fused_n1_variants.log), 2 KiB .. one chunk.
   std::uint64_t item = opt_.local_item > 0 ? opt_.local_item : bytes / (4 * warps);
-  item = std::clamp<std::uint64_t>((item + 15) / 16 * 16, 2048, std::max<std::uint64_t>(p.chunk_bytes, 16));
+  const std::uint64_t hi = std::max<std::uint64_t>(p.chunk_bytes, 16);
+  item = std::clamp<std::uint64_t>((item + 15) / 16 * 16, std::min<std::uint64_t>(2048, hi), hi);
   P.item_bytes = std::min<std::uint64_t>(item, p.chunk_bytes);
   ck(static_cast<cudaError_t>(bcl::launch_local_chain(P, ctas, stream)), "launch(local chain)");
 }
@@ -474,25 +536,23 @@ void Group::launch_local_chain(const std::vector<int>& locals, const std::vector
 // Line protocols for the pipelined chain in auto mode: LL128 (every rank on
 // its own GPU) up to the table's ll128 rule and ll128_max_; on one GPU the
 // fused kernel instead; else 16-byte LL lines up to ll_chain_max_; above them
-// the lane executor. Provenance / timeline recording need the lane executor
-// or the fused kernel. Returns 0 (no line protocol), 1 (LL) or 2 (LL128).
+// the lane executor. Returns 0 (no line protocol), 1 (LL) or 2 (LL128).
+// The choice depends only on state every rank shares (options, table, size):
+// diagnostic hooks (provenance, timeline) never change the transport — line
+// protocols simply record nothing — so ranks cannot disagree and deadlock.
 int Group::ll_chain_mode(const CallPlan& p, std::uint64_t bytes, const std::vector<int>& locals) const {
   if (!p.implicit_chain || n_ < 2 || !opt_.ll || bytes == 0) return 0;
   if (opt_.protocol == 1 || opt_.protocol == 2) return 0;
-  for (int li : locals) {
-    const LocalRank& r = local_[static_cast<std::size_t>(li)];
-    if (r.prov != nullptr || r.trace != nullptr) return 0;
-  }
   if (opt_.protocol == 3) {
     if (bytes > ll_chain_max_) throw std::invalid_argument("message exceeds the LL chain landing area");
     return 1;
   }
   if (opt_.protocol == 4) {
-    if (!ll128_ok_) throw std::invalid_argument("LL128 needs every rank on its own GPU");
+    if (!ll128_ok_) throw std::invalid_argument("LL128 needs every rank on its own GPU (or the ll128=1 option)");
     if (bytes > ll128_max_) throw std::invalid_argument("message exceeds the LL128 chain landing area");
     return 2;
   }
-  if (ll128_ok_ && bytes <= ll128_max_ && select_ll128(table(), n_, bytes)) return 2;
+  if (ll128_ok_ && !single_device_ && bytes <= ll128_max_ && select_ll128(table(), n_, bytes)) return 2;
   // One GPU: the fused kernel beats LL lines at every size (4 KiB: 8.2 vs
   // 9.8 us, 8 MiB: 12.4 vs 51.8 us, 4 ranks); LL stays available explicitly.
   if (use_local_chain(p, locals)) return 0;
@@ -642,12 +702,13 @@ void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& 
   // ~4 lines per thread, at most kLLMaxCtas CTAs per rank
   // ~2 lines per thread; ranks sharing a GPU must stay co-resident
   // (cooperative launch): at most 4 LL CTAs per SM in total.
-  const int resident = std::max(1, 148 * 4 / std::max<int>(1, P.n_local));
+  const int resident = std::max(1, sms_ * 4 / std::max<int>(1, P.n_local));
   P.ctas = std::clamp<int>(static_cast<int>((P.lines + 2 * dev::kLLThreads - 1) / (2 * dev::kLLThreads)), 1,
                            std::min(dev::kLLMaxCtas, resident));
-  if (mode == 2) {  // a warp moves 4 lines per step: ~2 steps per warp, up to one CTA per SM
+  if (mode == 2) {  // a warp moves 4 lines per step: ~2 steps per warp, up to 3 CTAs per SM
     const std::uint32_t per_cta = dev::kLLThreads / 32 * 4 * 2;
-    P.ctas = std::clamp<int>(static_cast<int>((P.lines + per_cta - 1) / per_cta), 1, dev::kLL128MaxCtas);
+    const int cap = P.n_local > 1 ? std::max(1, sms_ * 2 / P.n_local) : dev::kLL128MaxCtas;  // co-resident
+    P.ctas = std::clamp<int>(static_cast<int>((P.lines + per_cta - 1) / per_cta), 1, cap);
   }
   P.timeout_ns = opt_.timeout_ns;
   const std::size_t S = region_stride();
@@ -717,8 +778,8 @@ void Group::launch_group(const std::vector<int>& locals, const std::vector<void*
   P.slice_bytes = p.slice_bytes;
   P.timeout_ns = opt_.timeout_ns;
   P.poll_ns = opt_.poll_ns;
-  P.sys_scope = single_device_ ? 0 : 1;
-  P.strict_sys = (opt_.strict_sys && !single_device_) ? 1 : 0;
+  P.sys_scope = sys_ ? 1 : 0;
+  P.strict_sys = (opt_.strict_sys && sys_) ? 1 : 0;
   P.stage_bytes = static_cast<std::uint32_t>(std::max<std::int64_t>(opt_.stage_bytes, 0));
   P.stages = opt_.stages;
   P.push = use_push(p, bytes) ? 1 : 0;
@@ -726,7 +787,7 @@ void Group::launch_group(const std::vector<int>& locals, const std::vector<void*
   // Push publishes data that lives in the peer's memory: its sys-scope fence
   // must wait for the remote stores anyway, so the publisher keeps it (a
   // writer-side sys fence halves push bandwidth: 3.39 vs 1.73 ms, 1 GiB n=4).
-  P.writer_fence = (opt_.writer_fence && !P.strict_sys && !P.push) ? 1 : 0;
+  P.writer_fence = (P.strict_sys || P.push) ? 0 : (sys_ ? opt_.writer_fence : std::min(opt_.writer_fence, 1));
   std::uint64_t epoch = 0;
   for (std::size_t i = 0; i < locals.size(); ++i) {
     LocalRank& r = local_[static_cast<std::size_t>(locals[i])];

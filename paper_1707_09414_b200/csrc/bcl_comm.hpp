@@ -77,8 +77,14 @@ struct GroupOptions {
   int max_ctas_per_rank = 0;                                // 0 = SM count
   std::uint32_t poll_ns = 64;                               // back-off between flag polls (ns)
   bool strict_sys = false;                                  // system-scope fence before every flag
+  int sys_scope = -1;                                       // flag polls/fences at system scope: -1 auto (ranks
+                                                            // span GPUs), 1 always (runs the cross-GPU code on one GPU)
   bool eager_post = true;                                   // bulk chain: forward a chunk once its store is done
-  bool writer_fence = true;                                 // copy warps fence their own data (see run_publisher)
+  int writer_fence = 2;                                     // copy warps fence their own data before the hand-off:
+                                                            // 0 no (the publisher fences), 1 gpu scope, 2 the call's
+                                                            // scope (system across GPUs)
+  int ll128 = -1;                                           // LL128 chain lines: -1 auto (every rank on its own
+                                                            // GPU), 0 off, 1 also for ranks sharing a GPU
   bool local_fused = true;                                  // single-GPU groups: fused flag-free chain kernel
   int local_ctas = 0;                                       // its grid (0 = all resident CTAs)
   std::uint64_t local_item = 0;                             // its per-warp item bytes (0 = auto)
@@ -92,6 +98,9 @@ struct GroupOptions {
                                                             // -1 = auto (8 KiB across GPUs, 0 on one GPU)
   std::uint32_t stages = 2;                                 // bulk-copy stages per copy warp
   static GroupOptions from_env();                           // BCL_* overrides (tuning runs)
+  // "key=value,key=value" with the BCL_* names in lower case (e.g.
+  // "stage_bytes=8192,sys_scope=1,protocol=2"); applied over *this.
+  void apply(const std::string& options);
 };
 
 // What one call does on the device, derived identically on every rank.
@@ -193,6 +202,7 @@ class Group {
   Group() = default;
   void alloc_rank(LocalRank& r, std::size_t heap_bytes);
   void upload_peers(LocalRank& r);
+  void cache_device_limits(int device);
   void fill_rank_work(dev::RankWork& w, LocalRank& r, const CallPlan& p, void* buf);
   void launch_group(const std::vector<int>& locals, const std::vector<void*>& bufs,
                     std::uint64_t bytes, int root, const CallPlan& p, cudaStream_t stream);
@@ -236,6 +246,7 @@ class Group {
   int lanes_alloc_{0};
   bool ipc_{false};
   bool single_device_{false};  // every rank on one GPU: gpu-scope ordering suffices
+  bool sys_{false};            // system-scope flags (ranks span GPUs, or the sys_scope=1 option)
   bool connected_{false};
   bool broken_{false};
   GroupOptions opt_;
@@ -243,6 +254,8 @@ class Group {
   std::map<int, std::vector<int>> by_device_;
   TuningTable table_;
   bool have_table_{false};
+  int sms_{0};                  // SM count of the first device
+  int local_chain_occ_{0};      // resident local_chain_kernel CTAs per SM
   std::mutex plan_mu_;
   std::map<std::tuple<int, int, std::uint64_t, int, std::uint64_t>, std::shared_ptr<CallPlan>> plans_;
 };

@@ -25,6 +25,9 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <algorithm>
 
 #include "bcl_device.cuh"
 
@@ -35,7 +38,7 @@
 #define BCL_LDG_UNROLL 8
 #endif
 #ifndef BCL_SHARED_MIN_BLOCKS
-#define BCL_SHARED_MIN_BLOCKS 3
+#define BCL_SHARED_MIN_BLOCKS 2
 #endif
 
 namespace bcl {
@@ -238,8 +241,16 @@ __device__ bool wait_geq(const Ctx& c, const std::uint64_t* p, std::uint64_t tar
 // batch's remote flag stores, whose acknowledgements queue behind loaded
 // NVLink traffic (measured ~16 us per batch at n = 4, 64 MiB); the copy warp
 // has only its own, already completed, data writes outstanding.
+// writer_fence = 2 (the default across GPUs) fences at system scope: the
+// copy warp has no remote stores outstanding at that point (its data went to
+// its own HBM and its remote flags are stored by the publisher), so the fence
+// only waits for its local, completed writes.
 __device__ __forceinline__ void writer_fence(const LaunchParamsT<1>& P) {
-  if (P.writer_fence) fence_acq_rel_gpu();
+  if (P.writer_fence == 2) {
+    fence_acq_rel_sys();
+  } else if (P.writer_fence == 1) {
+    fence_acq_rel_gpu();
+  }
 }
 
 // Queue "*addr = value" behind this warp's preceding stores. The warp
@@ -771,7 +782,8 @@ __device__ void run_events(Ctx& c, int pipe, int q, int ns) {
 }
 
 // NL = 1: one rank per GPU (full register budget). NL = kMaxLocal: ranks
-// sharing a GPU need several co-resident CTAs per SM, hence the 3-CTA bound.
+// sharing a GPU need several co-resident CTAs per SM: 2 per SM (112 registers,
+// no spills; the 3-CTA bound spilled 224 bytes).
 template <int NL>
 __global__ void __launch_bounds__(kThreads, NL == 1 ? 1 : BCL_SHARED_MIN_BLOCKS) bcast_kernel(const __grid_constant__ LaunchParamsT<NL> P) {
   __shared__ CtaShared sh;
@@ -1030,13 +1042,18 @@ __device__ __forceinline__ void ll128_put(std::uint8_t* buf, std::uint64_t off, 
   for (std::uint32_t b = 0; b < len; ++b) buf[off + b] = static_cast<std::uint8_t>(v >> (8 * b));
 }
 
-__global__ void __launch_bounds__(kLLThreads) ll128_kernel(const __grid_constant__ LLParamsT<1> P) {
-  const LLRank& R = P.ranks[0];
+// NL > 1: ranks sharing one GPU (cooperative launch, P.ctas CTAs per rank) —
+// the same line protocol through L2 instead of NVLink, so the cross-GPU
+// kernel is parity-tested on a single B200.
+template <int NL>
+__global__ void __launch_bounds__(kLLThreads) ll128_kernel(const __grid_constant__ LLParamsT<NL> P) {
+  const LLRank& R = P.ranks[NL == 1 ? 0 : static_cast<int>(blockIdx.x) / P.ctas];
+  const std::uint32_t cta = NL == 1 ? blockIdx.x : blockIdx.x % P.ctas;
   const int lane = static_cast<int>(threadIdx.x & 31);
   const int part = lane & 7;  // 16-byte piece of the line
   const int sub = lane >> 3;  // line within the warp's group of four
-  const std::uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const std::uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  const std::uint32_t warp = (cta * blockDim.x + threadIdx.x) >> 5;
+  const std::uint32_t warps = (static_cast<std::uint32_t>(P.ctas) * blockDim.x) >> 5;
   const unsigned long long flag = P.epoch;
   const int n = P.n_ranks;
   const int logical = (R.rank - P.root + n) % n;
@@ -1159,14 +1176,26 @@ std::size_t bcast_smem_bytes(std::uint32_t stages, std::uint32_t stage_bytes) {
   return static_cast<std::size_t>(dev::kWarpsPerCta) * stages * stage_bytes;
 }
 
+// The dynamic shared-memory limit is a per-function, per-device attribute:
+// raise it to the largest stage budget any group on the device asked for
+// (a later group with fewer stages must not lower it under an earlier one).
 int prepare_bcast_kernels(std::size_t smem) {
-  cudaError_t e = cudaFuncSetAttribute(dev::bcast_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  static std::mutex mu;
+  static std::map<int, std::size_t> raised;  // device -> attribute value set
+  int device = 0;
+  cudaError_t e = cudaGetDevice(&device);
   if (e != cudaSuccess) return static_cast<int>(e);
-  e = cudaFuncSetAttribute(dev::bcast_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  std::lock_guard<std::mutex> lock(mu);
+  std::size_t& cur = raised[device];
+  if (smem <= cur && cur != 0) return 0;
+  cur = std::max(cur, smem);
+  const int v = static_cast<int>(cur);
+  e = cudaFuncSetAttribute(dev::bcast_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
   if (e != cudaSuccess) return static_cast<int>(e);
-  return static_cast<int>(cudaFuncSetAttribute(dev::bcast_kernel<dev::kMaxLocal>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  e = cudaFuncSetAttribute(dev::bcast_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  return static_cast<int>(
+      cudaFuncSetAttribute(dev::bcast_kernel<dev::kMaxLocal>, cudaFuncAttributeMaxDynamicSharedMemorySize, v));
 }
 
 template <int NL>
@@ -1219,14 +1248,6 @@ int launch_barrier(const dev::BarrierParams& p, void* stream) {
 }
 
 int launch_ll(const dev::LLParams& p, void* stream) {
-  if (p.chain == 2) {  // LL128: one rank per GPU by construction
-    if (p.n_local != 1) return static_cast<int>(cudaErrorInvalidValue);
-    dev::LLParamsT<1> one;
-    std::memcpy(&one, &p, offsetof(dev::LLParams, ranks));
-    one.ranks[0] = p.ranks[0];
-    dev::ll128_kernel<<<static_cast<unsigned>(p.ctas), dev::kLLThreads, 0, static_cast<cudaStream_t>(stream)>>>(one);
-    return static_cast<int>(cudaGetLastError());
-  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(p.n_local * p.ctas));
   cfg.blockDim = dim3(dev::kLLThreads);
@@ -1240,8 +1261,10 @@ int launch_ll(const dev::LLParams& p, void* stream) {
     dev::LLParamsT<1> one;
     std::memcpy(&one, &p, offsetof(dev::LLParams, ranks));
     one.ranks[0] = p.ranks[0];
+    if (p.chain == 2) return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::ll128_kernel<1>, one));
     return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::ll_kernel<1>, one));
   }
+  if (p.chain == 2) return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::ll128_kernel<dev::kMaxLocal>, p));
   return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::ll_kernel<dev::kMaxLocal>, p));
 }
 

@@ -1,8 +1,11 @@
 """GPU parity: the device broadcast vs the CPU oracle, bit-exact.
 
-All ranks share cuda:0 here (one cooperative launch serves them), so the same
-flag protocol, lane plan and copy code as the multi-GPU path run on one B200;
-tests/test_multigpu.py repeats the key cases across real GPUs. Cases follow
+All ranks share cuda:0 here (one cooperative launch serves them). Communicator
+options force the cross-GPU device paths onto this one GPU, so every one of
+them is checked here (VARIANTS): TMA-bulk pulls with system-scope flags and
+writer fences (the default across GPUs), the strict fence mode, producer
+pushes, and LL128 lines; tests/test_multigpu.py repeats the key cases across
+real GPUs. Cases follow
 the reference's own tests: acceptance criterion 4's random trials
 (proj/tests/acceptance.cpp:190-233) via the committed golden list, the
 runtime tests (proj/tests/test_runtime.cpp:99-254) and edge cases (empty,
@@ -33,12 +36,36 @@ def _cuda():
 
 _GROUPS = {}
 
+# Device paths of the pipelined chain, as (group options, protocol):
+#   auto       the fused per-item kernel auto mode picks on one GPU
+#   pull       the lane executor with 16-byte vector loads, gpu-scope flags
+#   ll         16-byte LL lines forwarded hop by hop
+#   push       producers store into the downstream buffer
+#   xpull      what runs across GPUs: TMA bulk pulls through shared-memory
+#              stages, system-scope polls and writer fences (chain_pull_bulk)
+#   xstrict    the same with the publisher's system-scope fence per flag batch
+#   xpush      TMA bulk pushes with system-scope publication
+#   ll128      128-byte LL128 lines (the cross-GPU kernel, here through L2)
+XGPU = {"stage_bytes": 8192, "sys_scope": 1}
+VARIANTS = {
+    "auto": ({}, "auto"),
+    "pull": ({}, "pull"),
+    "ll": ({}, "ll"),
+    "push": ({}, "push"),
+    "xpull": (XGPU, "pull"),
+    "xstrict": (dict(XGPU, strict_sys=1), "pull"),
+    "xpush": (XGPU, "push"),
+    "ll128": ({"ll128": 1, "ll128_max": 32 << 20, "sys_scope": 1}, "ll128"),
+}
+CHAIN_PROTOCOLS = list(VARIANTS)
 
-def comms_for(n):
-    """One emulated group per rank count, reused across tests (epochs advance)."""
-    if n not in _GROUPS:
-        _GROUPS[n] = B.Comm.local([0] * n, timeout_s=10)
-    return _GROUPS[n]
+
+def comms_for(n, options=None):
+    """One emulated group per (rank count, options), reused across tests (epochs advance)."""
+    key = (n, tuple(sorted((options or {}).items())))
+    if key not in _GROUPS:
+        _GROUPS[key] = B.Comm.local([0] * n, timeout_s=10, **(options or {}))
+    return _GROUPS[key]
 
 
 def cfg_of(algo, chunk=0, radix=0):
@@ -57,33 +84,26 @@ def make_bufs(n, m, root, payload, offsets=None):
     return store, views
 
 
-def set_protocol(n, protocol):
-    for c in comms_for(n):
-        c.set_protocol(protocol)
-
-
 def run_case(algo, n, root, m, chunk=0, radix=0, seed=1, offsets=None, protocol="auto"):
-    """protocol (chain): auto (the fused single-GPU kernel), pull (the lane
-    executor) or ll (LL lines forwarded hop by hop, <= 8 MiB)."""
+    """protocol: a key of VARIANTS (the chain's device path; other schedules
+    run on the lane executor with the variant's options)."""
+    options, proto = VARIANTS[protocol]
     payload = O.payload(seed, m)
     expect = [bytearray(m) for _ in range(n)]
     expect[root][:] = payload
     O.bcast(algo, n, root, expect, chunk=chunk, radix=radix)
     _, views = make_bufs(n, m, root, payload, offsets)
-    set_protocol(n, protocol)
+    comms = comms_for(n, options)
+    for c in comms:
+        c.set_protocol(proto if algo == "chain_pipelined" else "auto")
     try:
-        B.run_bcast(comms_for(n), root, views, m, cfg_of(algo, chunk, radix))
+        B.run_bcast(comms, root, views, m, cfg_of(algo, chunk, radix))
     finally:
-        set_protocol(n, "auto")
+        for c in comms:
+            c.set_protocol("auto")
     for r in range(n):
         got = views[r].cpu().numpy().tobytes()
         assert got == bytes(expect[r]), f"{algo}/{protocol} n={n} root={root} M={m} C={chunk}: rank {r} differs"
-
-
-# The pipelined chain runs on three device paths on one GPU: the fused
-# per-item kernel (auto), the lane executor (pull; also every cross-GPU pull)
-# and LL lines forwarded hop by hop (ll).
-CHAIN_PROTOCOLS = ["auto", "pull", "ll"]
 
 
 @pytest.mark.parametrize("idx", range(len(GOLD["bcasts"])))
@@ -99,9 +119,9 @@ def test_reference_trials_bit_exact(idx):
     assert got == GOLD["bcasts"][idx]["rank_fnv"]
 
 
-@pytest.mark.parametrize("algo", ["direct", "chain", "knomial", "scatter_ring_allgather",
-                                  "chain_pipelined", "chain_pipelined/pull", "chain_pipelined/ll",
-                                  "knomial_staged"])
+@pytest.mark.parametrize("algo", ["direct", "chain", "knomial", "scatter_ring_allgather", "knomial_staged",
+                                  "direct/xpull", "knomial/xpull", "scatter_ring_allgather/xpull"]
+                         + ["chain_pipelined/" + v for v in VARIANTS])
 @pytest.mark.parametrize("m", [0, 1, 4, 15, 16, 17, 1000, 4096, 65537])
 def test_every_root_small_sizes(algo, m):
     algo, _, protocol = algo.partition("/")
@@ -169,39 +189,50 @@ def test_config1_full_size_all_ranks_equal_root():
         assert torch.equal(bufs[r], bufs[0])
 
 
-def test_back_to_back_calls_change_payload_and_root():
-    """Epoch stress: buffers reused immediately, roots and payloads vary."""
+@pytest.mark.parametrize("variant", ["auto", "xpull", "xpush", "ll128"])
+def test_back_to_back_calls_change_payload_and_root(variant):
+    """Epoch stress: buffers reused immediately, roots and payloads vary; the
+    chain calls run on the variant's device path."""
     n, m = 4, 3 << 20
-    comms = comms_for(n)
+    options, proto = VARIANTS[variant]
+    comms = comms_for(n, options)
     bufs = [torch.zeros(m, dtype=torch.uint8, device="cuda:0") for _ in range(n)]
-    for it in range(40):
-        root = it % n
-        bufs[root].fill_(it + 1)
-        algo = ["chain_pipelined", "knomial", "scatter_ring_allgather", "direct"][it % 4]
-        B.bcast_all(comms, bufs, m, "uint8", root, cfg_of(algo, 262144 + it, 2))
-        if it % 7 == 6:
-            torch.cuda.synchronize()
-            for r in range(n):
-                assert int(bufs[r].min()) == it + 1 == int(bufs[r].max()), (it, r)
-    torch.cuda.synchronize()
-    for c in comms:
-        c.check()
+    try:
+        for it in range(40):
+            root = it % n
+            bufs[root].fill_(it + 1)
+            algo = ["chain_pipelined", "knomial", "scatter_ring_allgather", "direct"][it % 4]
+            for c in comms:
+                c.set_protocol(proto if algo == "chain_pipelined" else "auto")
+            B.bcast_all(comms, bufs, m, "uint8", root, cfg_of(algo, 262144 + it, 2))
+            if it % 7 == 6:
+                torch.cuda.synchronize()
+                for r in range(n):
+                    assert int(bufs[r].min()) == it + 1 == int(bufs[r].max()), (it, r)
+        torch.cuda.synchronize()
+        for c in comms:
+            c.check()
+    finally:
+        for c in comms:
+            c.set_protocol("auto")
 
 
 def test_provenance_matches_schedule_sends():
     """Schedule fidelity (test_runtime.cpp:121-161): every (src, dst, chunk)
     pull happened once and moved exactly the chunk's bytes."""
     n, m = 6, 50000
-    for algo, chunk, protocol in (("scatter_ring_allgather", 0, "auto"), ("chain_pipelined", 7000, "auto"),
-                                  ("chain_pipelined", 7000, "pull"), ("knomial", 0, "auto")):
+    for algo, chunk, variant in (("scatter_ring_allgather", 0, "auto"), ("chain_pipelined", 7000, "auto"),
+                                 ("chain_pipelined", 7000, "pull"), ("chain_pipelined", 8192, "xpull"),
+                                 ("chain_pipelined", 7000, "xpull"), ("knomial", 0, "auto")):
         cfg = cfg_of(algo, chunk, 2)
         sched = B.make_schedule(cfg, n, 2, m)
         k = len(sched.chunks)
-        comms = comms_for(n)
+        options, protocol = VARIANTS[variant]
+        comms = comms_for(n, options)
         prov = [torch.zeros(n * k, dtype=torch.int64, device="cuda:0") for _ in range(n)]
         for r in range(n):
             comms[r].set_provenance(prov[r])
-            comms[r].set_protocol(protocol)  # chain: auto = fused kernel (provenance skips LL), pull = lane executor
+            comms[r].set_protocol(protocol)  # chain: auto = the fused kernel, pull = the lane executor
         payload = O.payload(3, m)
         _, views = make_bufs(n, m, 2, payload)
         B.run_bcast(comms, 2, views, m, cfg)
@@ -221,7 +252,7 @@ def test_provenance_matches_schedule_sends():
                     if int(cnt[src, c]):
                         got[(src, dst, c)] = int(cnt[src, c])
         expected = {key: v for key, v in expected.items() if v}
-        assert got == expected, (algo, protocol)
+        assert got == expected, (algo, variant)
 
 
 def test_auto_config_uses_table_select():
@@ -278,6 +309,21 @@ def test_host_buffer_run_bcast():
     assert wall > 0
     for r in range(n):
         assert bytes(hosts[r]) == payload
+
+
+def test_options_are_validated():
+    with pytest.raises(ValueError):
+        B.Comm.local([0, 0], bogus_knob=1)
+    comms = comms_for(2)  # ranks sharing a GPU: LL128 only with the ll128=1 option
+    bufs = [torch.zeros(16, dtype=torch.uint8, device="cuda:0") for _ in comms]
+    for c in comms:
+        c.set_protocol("ll128")
+    try:
+        with pytest.raises(ValueError):
+            B.bcast_all(comms, bufs, 16, "uint8", 0, cfg_of("chain_pipelined", 4))
+    finally:
+        for c in comms:
+            c.set_protocol("auto")
 
 
 def test_contract_errors():
@@ -348,6 +394,7 @@ def test_protocol_caps_and_lane_plan():
     comms = comms_for(4)
     caps = comms[0].protocol_caps()
     assert caps == {"ll_direct": 2 << 20, "ll_chain": 8 << 20, "ll128": 0}
+    assert comms_for(4, VARIANTS["ll128"][0])[0].protocol_caps()["ll128"] == 32 << 20
     lanes = comms[0].info()["lanes"]
     for m, chunk in ((64 << 20, 512 << 10), (1 << 20, 65536), (12345, 1000)):
         p = comms[0].plan(cfg_of("chain_pipelined", chunk), 0, m)
