@@ -186,6 +186,17 @@ bcl_status_t bcl_comm_init_rank_opts(int n, int rank, int device, size_t heap_by
                                      bcl_comm_t* out);
 bcl_status_t bcl_comm_export(bcl_comm_t c, void* blob, size_t cap, size_t* len);
 bcl_status_t bcl_comm_connect(bcl_comm_t c, const void* blobs, size_t blob_len);
+/* Buffer registration (one process per GPU; collective: every rank, same
+ * order, NCCL-style). The device allocation (cudaMalloc / caching allocator
+ * segment) holding [ptr, ptr + bytes) is exported with CUDA IPC: pass every
+ * rank's blob, ordered by rank, to bcl_comm_register_connect. Afterwards
+ * bcl_bcast works zero-copy on any buffer inside the registered allocations,
+ * not only on bcl_mem_alloc buffers (the line protocols need neither). blob
+ * == NULL only returns the blob size in *len. Up to
+ * 255 registrations per communicator. One-process groups (bcl_comm_init_all)
+ * need none: export returns *len = 0 and connect does nothing. */
+bcl_status_t bcl_comm_register_export(bcl_comm_t c, void* ptr, size_t bytes, void* blob, size_t cap, size_t* len);
+bcl_status_t bcl_comm_register_connect(bcl_comm_t c, const void* blobs, size_t blob_len);
 bcl_status_t bcl_comm_destroy(bcl_comm_t c);
 bcl_status_t bcl_comm_info(bcl_comm_t c, int* n, int* rank, int* device, int* lanes);
 /* Largest message each line protocol takes on this communicator (bytes; 0 =
@@ -201,15 +212,17 @@ bcl_status_t bcl_comm_set_table(bcl_comm_t c, bcl_table_t t);
  * chunks c with c % (lanes / Q) == l / Q. */
 bcl_status_t bcl_comm_plan(bcl_comm_t c, const bcl_config_t* config, int root, uint64_t bytes, int* slices,
                            uint64_t* slice_bytes, uint32_t* n_chunks, int* ctas);
-/* Pipelined-chain transport protocol: 0 auto (line protocols up to their
- * caps -- LL128 when every rank has its own GPU, up to the table's measured
- * "# bcl-ll128-upto" rule and BCL_LL128_MAX, default 32 MiB at n = 2 and
- * 512 MiB from n = 3, else LL,
- * BCL_LL_CHAIN_MAX, default 8 MiB -- and above them the table's measured
- * "# bcl-push-from" rule), 1 pull (consumers load from the
- * upstream buffer), 2 push (producers store into the downstream buffer),
- * 3 LL (flagged 16-byte lines forwarded hop by hop), 4 LL128 (128-byte lines,
- * 120 payload bytes each). 3 and 4 fail above their caps. */
+/* Pipelined-chain transport protocol: 0 auto (line protocols where the
+ * tuning table's rules pick them -- LL128 when every rank has its own GPU, up
+ * to the table's measured "# bcl-ll128-upto" rule (and the ll128_max option,
+ * no limit by default: LL128 lines land in a bounded per-rank ring of 58 MB
+ * with per-warp credits), else 16-byte LL lines up to ll_chain_max (default
+ * 8 MiB) -- and above them the table's measured "# bcl-push-from" rule),
+ * 1 pull (consumers load from the upstream buffer), 2 push (producers store
+ * into the downstream buffer), 3 LL (flagged 16-byte lines forwarded hop by
+ * hop), 4 LL128 (128-byte lines, 120 payload bytes each). 3 fails above
+ * ll_chain_max, 4 above ll128_max or when ranks share a GPU without the
+ * ll128=1 option. */
 bcl_status_t bcl_comm_set_protocol(bcl_comm_t c, int protocol);
 /* The config a NULL-config call would run for this size (select + clamp). */
 bcl_status_t bcl_comm_choose(bcl_comm_t c, uint64_t message_bytes, bcl_config_t* out);

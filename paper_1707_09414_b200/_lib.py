@@ -96,6 +96,9 @@ _SIGS = {
     "bcl_comm_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "bcl_comm_connect": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
     "bcl_comm_destroy": (C.c_int, [C.c_void_p]),
+    "bcl_comm_register_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t,
+                                           C.POINTER(C.c_size_t)]),
+    "bcl_comm_register_connect": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
     "bcl_comm_protocol_caps": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                          C.POINTER(C.c_uint64)]),
     "bcl_comm_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),

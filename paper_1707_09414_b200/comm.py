@@ -114,6 +114,21 @@ class Comm:
         joined = b"".join(blobs)
         _check(lib().bcl_comm_connect(self._h, C.c_char_p(joined), size))
 
+    def register(self, buf, nbytes: Optional[int] = None, group=None) -> None:
+        """Collective (per-process ranks): register the device allocation
+        holding `buf` so broadcasts on buffers inside it are zero-copy; the
+        blobs are exchanged over torch.distributed. No-op for one-process groups."""
+        nbytes = nbytes if nbytes is not None else (buf.numel() * buf.element_size() if hasattr(buf, "numel") else 0)
+        ln = C.c_size_t()
+        _check(lib().bcl_comm_register_export(self._h, C.c_void_p(_ptr(buf)), nbytes, None, 0, C.byref(ln)))
+        if ln.value == 0:
+            return
+        blob = C.create_string_buffer(ln.value)
+        _check(lib().bcl_comm_register_export(self._h, C.c_void_p(_ptr(buf)), nbytes, blob, ln.value, C.byref(ln)))
+        blobs = exchange_blobs(blob.raw[:ln.value], group)
+        joined = b"".join(blobs)
+        _check(lib().bcl_comm_register_connect(self._h, C.c_char_p(joined), ln.value))
+
     def close(self) -> None:
         if self._h is not None and self._h.value:
             lib().bcl_comm_destroy(self._h)

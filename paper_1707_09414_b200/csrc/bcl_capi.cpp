@@ -404,6 +404,31 @@ bcl_status_t bcl_comm_connect(bcl_comm_t c, const void* blobs, size_t blob_len) 
   });
 }
 
+bcl_status_t bcl_comm_register_export(bcl_comm_t c, void* ptr, size_t bytes, void* blob, size_t cap,
+                                      size_t* len) {
+  return guard([&] {
+    need(c, "comm");
+    const std::size_t need_bytes = c->g->register_blob_bytes();
+    if (len) *len = need_bytes;
+    if (blob == nullptr || need_bytes == 0) return;  // size query (no registration happens)
+    if (cap < need_bytes) throw std::invalid_argument("blob buffer too small");
+    const auto v = c->g->register_export(ptr, bytes);
+    std::memcpy(blob, v.data(), v.size());
+  });
+}
+
+bcl_status_t bcl_comm_register_connect(bcl_comm_t c, const void* blobs, size_t blob_len) {
+  return guard([&] {
+    need(c, "comm");
+    if (!c->g->ipc()) return;
+    need(blobs, "blobs");
+    std::vector<std::vector<std::uint8_t>> v;
+    const auto* p = static_cast<const std::uint8_t*>(blobs);
+    for (int r = 0; r < c->g->n_ranks(); ++r) v.emplace_back(p + r * blob_len, p + (r + 1) * blob_len);
+    c->g->register_connect(v);
+  });
+}
+
 bcl_status_t bcl_comm_destroy(bcl_comm_t c) {
   delete c;
   return BCL_OK;

@@ -184,6 +184,7 @@ void Group::cache_device_limits(int device) {
   DeviceScope ds(device);
   ck(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device), "sm count");
   ck(static_cast<cudaError_t>(local_chain_occupancy(&local_chain_occ_)), "occupancy(local chain)");
+  ck(static_cast<cudaError_t>(ll128_occupancy(&ll128_occ_)), "occupancy(ll128)");
 }
 
 void Group::upload_peers(LocalRank& r) {
@@ -228,15 +229,12 @@ std::uint64_t ll_chain_cap(const GroupOptions& opt) {
                                                    : opt.ll_chain_max_bytes;
   return static_cast<std::uint64_t>(std::min<std::int64_t>(v, 64ll << 20)) / 16 * 16;
 }
-// LL128 landing area: 2 halves x cap x 128/120 bytes per rank. Default cap
-// by rank count: LL128 wins up to the tuner's measured rule, 24 MB at n = 2
-// but beyond 512 MiB at n = 4 (256 MiB: 427 vs 472 us pull; 512 MiB: 841 vs
-// 902 us, profiles/round1/ll128_big/), so 32 MiB for n = 2 (68 MiB per rank)
-// and 512 MiB from n = 3 on (~1.07 GiB per rank of 180 GB).
-std::uint64_t ll128_cap(int n, const GroupOptions& opt) {
-  const std::int64_t dflt = n <= 2 ? (32ll << 20) : static_cast<std::int64_t>(dev::kLL128MaxBytes);
-  const std::int64_t v = opt.ll128_max_bytes < 0 ? dflt : opt.ll128_max_bytes;
-  return static_cast<std::uint64_t>(std::clamp<std::int64_t>(v, 0, 1ll << 30));
+// LL128 size limit: the landing ring is bounded (kLL128RingLines, 58 MB per
+// rank) whatever the message size, so by default only the table's measured
+// rule limits LL128; ll128_max caps it further (0 turns LL128 off).
+constexpr std::uint64_t kNoLimit = 1ull << 62;
+std::uint64_t ll128_cap(const GroupOptions& opt) {
+  return opt.ll128_max_bytes < 0 ? kNoLimit : static_cast<std::uint64_t>(opt.ll128_max_bytes);
 }
 
 }  // namespace
@@ -292,7 +290,8 @@ std::shared_ptr<Group> Group::create_local(const std::vector<int>& devices, cons
   g->ll128_ok_ = n >= 2 && opt.ll128 != 0 && (static_cast<int>(g->by_device_.size()) == n || opt.ll128 == 1);
   g->ll_max_ = ll_cap(n, opt);
   g->ll_chain_max_ = ll_chain_cap(opt);
-  g->ll128_max_ = g->ll128_ok_ ? ll128_cap(n, opt) : 0;  // no LL128 area without LL128
+  g->ll128_max_ = g->ll128_ok_ ? ll128_cap(opt) : 0;  // no LL128 ring without LL128
+  g->ll128_ok_ = g->ll128_ok_ && g->ll128_max_ > 0;
   g->cache_device_limits(devices[0]);
   g->local_.resize(static_cast<std::size_t>(n));
   for (int r = 0; r < n; ++r) {
@@ -311,6 +310,7 @@ std::shared_ptr<Group> Group::create_local(const std::vector<int>& devices, cons
       lr.h_peers.bar[p] = base + 4 * S;
       lr.h_peers.addr_base[p] = 0;
       lr.h_peers.credit[p] = base + 4 * S + n + 1;
+      lr.h_peers.wcredit[p] = base + 4 * S + 3 * n + 2;
       lr.h_peers.ll[p] = reinterpret_cast<uint4*>(base + g->ll_offset(g->lanes_));
     }
     g->upload_peers(lr);
@@ -334,7 +334,7 @@ std::shared_ptr<Group> Group::create_rank(int n, int rank, int device, std::size
   g->sys_ = n > 1 || opt.sys_scope == 1;
   g->ll_max_ = ll_cap(n, opt);
   g->ll_chain_max_ = ll_chain_cap(opt);
-  g->ll128_max_ = opt.ll128 != 0 ? ll128_cap(n, opt) : 0;
+  g->ll128_max_ = opt.ll128 != 0 ? ll128_cap(opt) : 0;
   g->cache_device_limits(device);
   g->local_.resize(1);
   g->local_[0].rank = rank;
@@ -370,6 +370,100 @@ std::vector<std::uint8_t> Group::export_info() const {
   std::vector<std::uint8_t> out(sizeof info);
   std::memcpy(out.data(), &info, sizeof info);
   return out;
+}
+
+namespace {
+
+constexpr std::uint32_t kRegMagic = 0xB200BC58u;
+struct RegInfo {
+  std::uint32_t magic;
+  std::int32_t rank;
+  std::int32_t id;
+  std::int32_t pad;
+  std::uint64_t size;
+  cudaIpcMemHandle_t handle;
+};
+
+// [base, base + size) of the device allocation holding p (driver API through
+// the runtime's entry-point lookup: no libcuda link dependency).
+void allocation_range(const void* p, std::uint8_t** base, std::size_t* size) {
+  using Fn = int (*)(unsigned long long*, std::size_t*, unsigned long long);
+  static Fn fn = nullptr;
+  if (fn == nullptr) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    ck(cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q), "cudaGetDriverEntryPoint");
+    if (f == nullptr || q != cudaDriverEntryPointSuccess) throw std::runtime_error("cuMemGetAddressRange unavailable");
+    fn = reinterpret_cast<Fn>(f);
+  }
+  unsigned long long b = 0;
+  if (fn(&b, size, reinterpret_cast<unsigned long long>(p)) != 0) {
+    throw std::invalid_argument("buffer is not device memory from cudaMalloc");
+  }
+  *base = reinterpret_cast<std::uint8_t*>(b);
+}
+
+}  // namespace
+
+std::size_t Group::register_blob_bytes() const { return ipc_ ? sizeof(RegInfo) : 0; }
+
+std::vector<std::uint8_t> Group::register_export(void* ptr, std::size_t bytes) {
+  if (!ipc_) return {};
+  if (!connected_) throw std::invalid_argument("communicator is not connected");
+  if (ptr == nullptr || bytes == 0) throw std::invalid_argument("nothing to register");
+  LocalRank& r = local_[0];
+  if (r.regs.size() >= static_cast<std::size_t>(dev::kMaxRegs)) throw std::invalid_argument("too many registrations");
+  DeviceScope ds(r.device);
+  std::uint8_t* base = nullptr;
+  std::size_t size = 0;
+  allocation_range(ptr, &base, &size);
+  if (static_cast<std::uint8_t*>(ptr) + bytes > base + size) {
+    throw std::invalid_argument("registered range spans several allocations");
+  }
+  if (size >= (1ull << 40)) throw std::invalid_argument("allocation larger than 1 TiB");
+  RegInfo info{};
+  info.magic = kRegMagic;
+  info.rank = r.rank;
+  info.id = static_cast<std::int32_t>(r.regs.size());
+  info.size = size;
+  ck(cudaIpcGetMemHandle(&info.handle, base), "cudaIpcGetMemHandle(buffer)");
+  r.regs.push_back(LocalRank::Registration{base, size});  // completed by register_connect
+  std::vector<std::uint8_t> out(sizeof info);
+  std::memcpy(out.data(), &info, sizeof info);
+  return out;
+}
+
+void Group::register_connect(const std::vector<std::vector<std::uint8_t>>& blobs) {
+  if (!ipc_) return;
+  LocalRank& me = local_[0];
+  if (static_cast<int>(blobs.size()) != n_) throw std::invalid_argument("one registration blob per rank required");
+  if (me.regs.empty()) throw std::invalid_argument("register_export first");
+  const int id = static_cast<int>(me.regs.size()) - 1;
+  DeviceScope ds(me.device);
+  if (me.d_regs == nullptr) {
+    me.h_regs.assign(static_cast<std::size_t>(n_) * dev::kMaxRegs, 0);
+    ck(cudaMalloc(&me.d_regs, me.h_regs.size() * sizeof(std::uint64_t)), "cudaMalloc(regs)");
+  }
+  for (int p = 0; p < n_; ++p) {
+    RegInfo info{};
+    if (blobs[static_cast<std::size_t>(p)].size() < sizeof info) throw std::invalid_argument("truncated registration blob");
+    std::memcpy(&info, blobs[static_cast<std::size_t>(p)].data(), sizeof info);
+    if (info.magic != kRegMagic || info.rank != p || info.id != id) {
+      throw std::invalid_argument("registration blobs must be ordered by rank and belong to the same registration");
+    }
+    std::uint64_t mapped = reinterpret_cast<std::uint64_t>(me.regs.back().base);
+    if (p != me.rank) {
+      void* q = nullptr;
+      ck(cudaIpcOpenMemHandle(&q, info.handle, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle(buffer)");
+      me.opened.push_back(q);
+      mapped = reinterpret_cast<std::uint64_t>(q);
+    }
+    me.h_regs[static_cast<std::size_t>(p) * dev::kMaxRegs + static_cast<std::size_t>(id)] = mapped;
+  }
+  ck(cudaMemcpy(me.d_regs, me.h_regs.data(), me.h_regs.size() * sizeof(std::uint64_t), cudaMemcpyHostToDevice),
+     "cudaMemcpy(regs)");
+  me.h_peers.regs = me.d_regs;
+  upload_peers(me);
 }
 
 void Group::connect(const std::vector<std::vector<std::uint8_t>>& infos) {
@@ -435,6 +529,7 @@ void Group::connect(const std::vector<std::vector<std::uint8_t>>& infos) {
     me.h_peers.bar[p] = base + 4 * S;
     me.h_peers.addr_base[p] = heap_base;
     me.h_peers.credit[p] = base + 4 * S + n_ + 1;
+    me.h_peers.wcredit[p] = base + 4 * S + 3 * static_cast<std::size_t>(n_) + 2;
     me.h_peers.ll[p] = reinterpret_cast<uint4*>(base + ll_offset(lanes_));
   }
   upload_peers(me);
@@ -448,6 +543,7 @@ Group::~Group() {
     for (void* p : r.opened) cudaIpcCloseMemHandle(p);
     if (r.region) cudaFree(r.region);
     if (r.d_peers) cudaFree(r.d_peers);
+    if (r.d_regs) cudaFree(r.d_regs);
     if (r.heap) cudaFree(r.heap);
     if (r.scratch && !ipc_) cudaFree(r.scratch);
     if (r.err_host) cudaFreeHost(r.err_host);
@@ -549,7 +645,7 @@ int Group::ll_chain_mode(const CallPlan& p, std::uint64_t bytes, const std::vect
   }
   if (opt_.protocol == 4) {
     if (!ll128_ok_) throw std::invalid_argument("LL128 needs every rank on its own GPU (or the ll128=1 option)");
-    if (bytes > ll128_max_) throw std::invalid_argument("message exceeds the LL128 chain landing area");
+    if (bytes > ll128_max_) throw std::invalid_argument("message exceeds the communicator's LL128 limit (ll128_max)");
     return 2;
   }
   if (ll128_ok_ && !single_device_ && bytes <= ll128_max_ && select_ll128(table(), n_, bytes)) return 2;
@@ -661,12 +757,29 @@ CallPlan Group::plan(const AlgorithmConfig& cfg, int root, std::uint64_t bytes) 
 
 // ---------------------------------------------------------------- launches
 
-void Group::fill_rank_work(dev::RankWork& w, LocalRank& r, const CallPlan& p, void* buf) {
+// Per-process ranks name their buffer to peers as a symmetric-heap offset or
+// as (registration id + 1) << 40 | offset into a registered allocation.
+std::uint64_t Group::ipc_mailbox_value(const LocalRank& r, const std::uint8_t* b, std::uint64_t bytes) const {
+  if (bytes == 0) return 0;  // nothing is read
+  if (b >= r.heap && b + bytes <= r.heap + r.heap_bytes) return static_cast<std::uint64_t>(b - r.heap);
+  for (std::size_t i = 0; i < r.regs.size(); ++i) {
+    const auto& g = r.regs[i];
+    if (r.d_regs != nullptr && b >= g.base && b + bytes <= g.base + g.size && i < r.regs.size()) {
+      return ((i + 1) << 40) | static_cast<std::uint64_t>(b - g.base);
+    }
+  }
+  throw std::invalid_argument(
+      "per-process ranks pull peers' buffers directly: use buffers from bcl_mem_alloc or register their allocation "
+      "with bcl_comm_register_export/connect (buffer offset " +
+      std::to_string(static_cast<long long>(b - r.heap)) + " + " + std::to_string(bytes) + " bytes)");
+}
+
+void Group::fill_rank_work(dev::RankWork& w, LocalRank& r, const CallPlan& p, void* buf, std::uint64_t bytes) {
   const std::size_t S = region_stride();
   w.rank = r.rank;
   w.n_events = p.implicit_chain ? -1 : static_cast<int>(p.events[static_cast<std::size_t>(r.rank)].size());
   w.buf = static_cast<std::uint8_t*>(buf);
-  w.pub = ipc_ ? static_cast<std::uint64_t>(static_cast<std::uint8_t*>(buf) - r.heap)
+  w.pub = ipc_ ? ipc_mailbox_value(r, static_cast<std::uint8_t*>(buf), bytes)
                : reinterpret_cast<std::uint64_t>(buf);
   if (w.pub >> 48) throw std::runtime_error("buffer address does not fit the 48-bit mailbox field");
   w.flags = r.region;
@@ -707,7 +820,8 @@ void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& 
                            std::min(dev::kLLMaxCtas, resident));
   if (mode == 2) {  // a warp moves 4 lines per step: ~2 steps per warp, up to 3 CTAs per SM
     const std::uint32_t per_cta = dev::kLLThreads / 32 * 4 * 2;
-    const int cap = P.n_local > 1 ? std::max(1, sms_ * 2 / P.n_local) : dev::kLL128MaxCtas;  // co-resident
+    // every CTA of every rank co-resident (writers wait on ring credits)
+    const int cap = std::max(1, std::min(dev::kLL128MaxCtas, sms_ * std::max(ll128_occ_, 1)) / P.n_local);
     P.ctas = std::clamp<int>(static_cast<int>((P.lines + per_cta - 1) / per_cta), 1, cap);
   }
   P.timeout_ns = opt_.timeout_ns;
@@ -722,6 +836,7 @@ void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& 
     w.rank = r.rank;
     w.buf = static_cast<std::uint8_t*>(bufs[i]);
     w.credit = r.region + 4 * S + static_cast<std::size_t>(n_) + 1 + (chain ? static_cast<std::size_t>(n_) + 1 : 0);
+    w.wcredit = r.region + 4 * S + 3 * static_cast<std::size_t>(n_) + 2;
     w.ll = reinterpret_cast<uint4*>(r.region + ll_offset(lanes_));
     w.peers = r.d_peers;
     w.err = r.err_dev;
@@ -731,7 +846,8 @@ void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& 
     // Writers wait for the credits of the last call of the same kind that
     // wrote this half (direct: every other rank; chain: the successor).
     std::uint64_t* last = nullptr;
-    if (chain && logical + 1 < n_) last = &r.ll_last_chain[half];
+    if (mode == 1 && logical + 1 < n_) last = &r.ll_last_chain[half];
+    if (mode == 2 && logical + 1 < n_) last = &r.ll_last_ring;
     if (!chain && logical == 0) last = &r.ll_last_direct[half];
     if (last != nullptr) {
       w.need_credit = *last;
@@ -794,7 +910,7 @@ void Group::launch_group(const std::vector<int>& locals, const std::vector<void*
     const std::uint64_t e = ++r.epoch;
     if (i == 0) epoch = e;
     if (e != epoch) throw std::runtime_error("ranks sharing a GPU drifted apart in call count");
-    fill_rank_work(P.ranks[i], r, p, bufs[i]);
+    fill_rank_work(P.ranks[i], r, p, bufs[i], bytes);
     ++r.launches;
   }
   P.epoch = epoch;
@@ -812,14 +928,8 @@ void Group::bcast(int li, void* buf, std::uint64_t bytes, int root, const Algori
     throw std::invalid_argument("ranks sharing a GPU must be driven together (bcast_all)");
   }
   if (bytes > 0 && buf == nullptr) throw std::invalid_argument("null buffer");
-  if (ipc_ && bytes > 0) {
-    const auto* b = static_cast<std::uint8_t*>(buf);
-    if (b < r.heap || b + bytes > r.heap + r.heap_bytes) {
-      throw std::invalid_argument("per-process ranks need buffers from bcl_mem_alloc (buffer offset " +
-                                  std::to_string(static_cast<long long>(b - r.heap)) + " + " + std::to_string(bytes) +
-                                  " bytes, heap " + std::to_string(r.heap_bytes) + " bytes)");
-    }
-  }
+  // (Per-process ranks: line protocols take any device buffer; the lane
+  // executor needs heap or registered buffers, checked in fill_rank_work.)
   const AlgorithmConfig c = choose(bytes, cfg);
   const CallPlan p = plan(c, root, bytes);
   if (n_ == 1) return;  // nothing moves (reference: n = 1 leaves the buffer untouched)
@@ -883,7 +993,14 @@ void Group::ensure_scratch(int li, std::uint64_t bytes) {
   if (bytes <= r.scratch_bytes) return;
   DeviceScope ds(r.device);
   if (ipc_) {
-    r.scratch = static_cast<std::uint8_t*>(mem_alloc(li, bytes));
+    // Peers read the scratch, so it lives in the symmetric heap. Grow the
+    // previous scratch in place when it is the heap's last allocation.
+    if (r.scratch != nullptr && r.scratch + r.scratch_bytes == r.heap + r.heap_used &&
+        static_cast<std::size_t>(r.scratch - r.heap) + bytes <= r.heap_bytes) {
+      r.heap_used = static_cast<std::size_t>(r.scratch - r.heap) + bytes;
+    } else {
+      r.scratch = static_cast<std::uint8_t*>(mem_alloc(li, bytes));
+    }
   } else {
     if (r.scratch) ck(cudaFree(r.scratch), "cudaFree(scratch)");
     ck(cudaMalloc(&r.scratch, bytes), "cudaMalloc(scratch)");

@@ -92,7 +92,8 @@ struct GroupOptions {
   int protocol = 0;                                         // chain: 0 auto (table), 1 pull, 2 push
   std::uint64_t ll_max_bytes = 0;                           // LL threshold (0 = 2 MiB, lowered for many ranks)
   std::int64_t ll_chain_max_bytes = -1;                     // LL pipelined chain up to this size (-1 = default)
-  std::int64_t ll128_max_bytes = -1;                        // LL128 pipelined chain up to this size (-1 = default)
+  std::int64_t ll128_max_bytes = -1;                        // LL128 pipelined chain up to this size (-1 = no limit
+                                                            // beyond the table's rule; 0 = off)
   std::uint64_t host_piece = 4ull << 20;                    // host-buffer calls: H2D/bcast/D2H pipeline piece
   std::int64_t stage_bytes = -1;                            // bulk-copy stage per warp: 0 = vector loads,
                                                             // -1 = auto (8 KiB across GPUs, 0 on one GPU)
@@ -141,9 +142,19 @@ struct LocalRank {
   std::uint32_t trace_cap{0};
   std::uint64_t launches{0};
   std::uint64_t ll_last_direct[2]{0, 0};  // last epoch this rank was a direct LL root, per half
-  std::uint64_t ll_last_chain[2]{0, 0};   // last epoch this rank wrote chain lines (LL or LL128), per half
+  std::uint64_t ll_last_chain[2]{0, 0};   // last epoch this rank wrote LL chain lines, per half
+  std::uint64_t ll_last_ring{0};          // last epoch this rank wrote into its successor's LL128 ring
   std::uint64_t ll_done{0};        // cumulative LL CTA completions expected as a receiver
   std::vector<void*> opened;    // IPC mappings to close
+  // Per-process mode: allocations registered for zero-copy broadcasts
+  // (bcl_comm_register_*), id = index; peers' bases as mapped here.
+  struct Registration {
+    std::uint8_t* base{};
+    std::size_t size{};
+  };
+  std::vector<Registration> regs;
+  std::vector<std::uint64_t> h_regs;  // [peer][kMaxRegs]
+  std::uint64_t* d_regs{};
 };
 
 class Group {
@@ -158,6 +169,15 @@ class Group {
   // Multi-process wiring (create_rank only).
   std::vector<std::uint8_t> export_info() const;
   void connect(const std::vector<std::vector<std::uint8_t>>& infos);
+  // Buffer registration (per-process ranks; collective, same order on every
+  // rank): the device allocation holding [ptr, ptr + bytes) is exported with
+  // CUDA IPC; after register_connect with every rank's blob, broadcasts on
+  // buffers inside it read and write peers' memory directly (zero copy).
+  // One-process groups need no registration (UVA): export returns an empty
+  // blob and connect is a no-op.
+  std::vector<std::uint8_t> register_export(void* ptr, std::size_t bytes);
+  void register_connect(const std::vector<std::vector<std::uint8_t>>& blobs);
+  std::size_t register_blob_bytes() const;  // 0 for one-process groups
 
   int n_ranks() const { return n_; }
   int lanes() const { return lanes_; }
@@ -203,7 +223,8 @@ class Group {
   void alloc_rank(LocalRank& r, std::size_t heap_bytes);
   void upload_peers(LocalRank& r);
   void cache_device_limits(int device);
-  void fill_rank_work(dev::RankWork& w, LocalRank& r, const CallPlan& p, void* buf);
+  void fill_rank_work(dev::RankWork& w, LocalRank& r, const CallPlan& p, void* buf, std::uint64_t bytes);
+  std::uint64_t ipc_mailbox_value(const LocalRank& r, const std::uint8_t* b, std::uint64_t bytes) const;
   void launch_group(const std::vector<int>& locals, const std::vector<void*>& bufs,
                     std::uint64_t bytes, int root, const CallPlan& p, cudaStream_t stream);
   bool use_push(const CallPlan& p, std::uint64_t bytes) const;
@@ -219,16 +240,15 @@ class Group {
   std::size_t region_stride() const { return static_cast<std::size_t>(n_) * lanes_; }
   // Offset (in 8-byte words) of the LL landing area for a flag stride of L lanes.
   std::size_t ll_offset(int lanes) const {
-    const std::size_t w = 4 * static_cast<std::size_t>(n_) * lanes + 3 * static_cast<std::size_t>(n_) + 2;
+    const std::size_t w = 4 * static_cast<std::size_t>(n_) * lanes + 3 * static_cast<std::size_t>(n_) + 2 +
+                          static_cast<std::size_t>(dev::kLL128WarpsMax);
     return (w + 31) / 32 * 32;  // 256-byte aligned: warp stores of LL lines cover whole 128-byte lines
   }
   std::uint64_t ll_max_{dev::kLLMaxBytes};  // LL protocol threshold (bytes), direct schedule
   std::uint64_t ll_chain_max_{0};           // LL pipelined chain up to this size (0 = off)
-  std::uint64_t ll128_max_{0};              // LL128 pipelined chain up to this size (0 = off)
+  std::uint64_t ll128_max_{0};              // LL128 pipelined chain up to this size (0 = off; the ring is bounded)
   bool ll128_ok_{false};                    // every rank on its own GPU (LL128 needs NVLink hops)
-  std::uint32_t ll128_lines() const {
-    return static_cast<std::uint32_t>((ll128_max_ + dev::kLL128Payload - 1) / dev::kLL128Payload);
-  }
+  std::uint32_t ll128_lines() const { return ll128_max_ > 0 ? dev::kLL128RingLines : 0; }
   // LL128 area offset from the LL base (16-byte units), 128-byte aligned given
   // a 256-byte aligned region.
   std::uint32_t ll128_area() const {
@@ -238,7 +258,7 @@ class Group {
   }
   std::size_t ll_words() const {            // 8-byte words of LL landing areas per rank (+ alignment pad)
     return (static_cast<std::size_t>(n_) * 2 * (ll_max_ / 8) + 2 * (ll_chain_max_ / 8)) * 2 +
-           static_cast<std::size_t>(2) * ll128_lines() * 16 + 16;
+           static_cast<std::size_t>(ll128_lines()) * 16 + 16;
   }
 
   int n_{0};
@@ -256,6 +276,7 @@ class Group {
   bool have_table_{false};
   int sms_{0};                  // SM count of the first device
   int local_chain_occ_{0};      // resident local_chain_kernel CTAs per SM
+  int ll128_occ_{0};            // resident ll128_kernel CTAs per SM
   std::mutex plan_mu_;
   std::map<std::tuple<int, int, std::uint64_t, int, std::uint64_t>, std::shared_ptr<CallPlan>> plans_;
 };

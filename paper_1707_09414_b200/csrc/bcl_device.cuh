@@ -26,15 +26,22 @@ namespace dev {
 constexpr int kMaxLocal = 16;    // ranks served by one launch (ranks sharing a GPU)
 constexpr int kMaxEvents = 64;   // explicit per-rank event list (trees, SRA)
 constexpr int kMaxRanks = 64;    // communicator size limit
+constexpr int kMaxRegs = 255;    // registered allocations per rank (per-process mode; 8-bit id in the mailbox)
 constexpr int kWarpsPerCta = 8;  // lanes per CTA
 constexpr int kThreads = (kWarpsPerCta + 1) * 32;  // + one publisher warp
 constexpr int kMaxStages = 4;    // bulk-copy stages per copy warp
 constexpr std::uint32_t kLLMaxBytes = 2048 * 1024;      // largest LL message (per-group cap may be lower)
 constexpr std::uint32_t kLLChainMaxBytes = 8u << 20;     // default LL pipelined-chain cap
-constexpr std::uint32_t kLL128MaxBytes = 512u << 20;     // default LL128 pipelined-chain cap (n >= 3)
 constexpr std::uint32_t kLL128Payload = 120;             // payload bytes per 128-byte LL128 line
 constexpr int kLL128MaxCtas = 444;  // 3 per SM: +4% at 64 MiB n=4 over one per SM (measured)
 constexpr int kLLThreads = 512;
+// LL128 landing ring: every warp of the (identical) grid on each rank owns a
+// private sub-ring of kLL128Depth groups of 4 lines; the reader returns
+// per-warp credits every kLL128Depth / 2 groups. Bounded memory for any
+// message size: 7104 warps x 16 x 4 lines x 128 B = 58 MB per rank.
+constexpr int kLL128Depth = 16;
+constexpr int kLL128WarpsMax = kLL128MaxCtas * (kLLThreads / 32);
+constexpr std::uint32_t kLL128RingLines = static_cast<std::uint32_t>(kLL128WarpsMax) * kLL128Depth * 4;
 constexpr int kLLMaxCtas = 64;                          // CTAs per rank for one LL call
 
 // Explicit event word: chunk (bits 0-23) | peer (24-30) | recv (31) |
@@ -55,8 +62,9 @@ enum ChunkMode : std::uint32_t {
 
 // Addresses of every peer's state as mapped in *this* rank's address space.
 // Region layout of a rank (8-byte words): flags[n][L] | acks[n][L] | mbox[n][L][2]
-// | bar[n] | abort | credit[n] | ll_done | chain_credit[n] | pad to 16 B | ll[n][2][ll_lines] (16-byte lines,
-// ll_lines = the group's LL cap / 8).
+// | bar[n] | abort | credit[n] | ll_done | chain_credit[n] | wcredit[kLL128WarpsMax] | pad to 256 B
+// | ll[n][2][ll_lines] (16-byte lines, ll_lines = the group's LL cap / 8) | chain LL [2][chain_lines]
+// | LL128 ring [kLL128RingLines] (128-byte lines).
 struct PeerTable {
   std::uint64_t* flags[kMaxRanks];  // peer's flags array (index [my_rank][lane])
   std::uint64_t* acks[kMaxRanks];   // peer's acks array  (index [my_rank][lane])
@@ -65,6 +73,9 @@ struct PeerTable {
   std::uint64_t addr_base[kMaxRanks];  // added to a mailbox value from that peer
   std::uint64_t* credit[kMaxRanks];    // peer's LL credit array (index [my_rank])
   uint4* ll[kMaxRanks];                // peer's LL landing area (index [my_rank][half][line])
+  std::uint64_t* wcredit[kMaxRanks];   // peer's LL128 per-warp ring credits (written by its successor)
+  const std::uint64_t* regs;           // per-process mode: [peer][kMaxRegs] registered allocation bases as mapped
+                                       // here (device array), else null
 };
 
 struct ErrorRecord {  // host-mapped, written by the first failing lane
@@ -135,6 +146,7 @@ struct LLRank {
   std::uint8_t* buf;
   uint4* ll;                  // local landing area base
   std::uint64_t* credit;      // local credit array [n] of this call's kind (direct, or chain: LL and LL128)
+  std::uint64_t* wcredit;     // local LL128 per-warp ring credits [kLL128WarpsMax] (written by the successor)
   const PeerTable* peers;
   ErrorRecord* err;
   int* abort;
@@ -156,7 +168,7 @@ struct LLParamsT {
   std::uint32_t area_lines;   // lines per (source, half) landing area of the direct schedule
   std::uint32_t chain;        // 0 direct, 1 pipelined chain on 16-byte LL lines, 2 chain on 128-byte LL128 lines
   std::uint32_t chain_lines;  // lines per half of the chain landing area (after the direct areas)
-  std::uint32_t chain128_lines;  // 128-byte lines per half of the LL128 chain area
+  std::uint32_t chain128_lines;  // 128-byte lines of the LL128 ring (kLL128RingLines)
   std::uint32_t chain128_area;   // its offset from the LL base in 16-byte units (128-byte aligned)
   std::uint64_t timeout_ns;
   LLRank ranks[NL];
@@ -200,6 +212,7 @@ int launch_barrier(const dev::BarrierParams& p, void* stream);
 int launch_ll(const dev::LLParams& p, void* stream);
 int launch_local_chain(const dev::LocalChainParams& p, int ctas, void* stream);
 int local_chain_occupancy(int* blocks_per_sm);
+int ll128_occupancy(int* blocks_per_sm);
 int bcast_kernel_occupancy(int* blocks_per_sm, std::size_t smem);
 std::size_t bcast_smem_bytes(std::uint32_t stages, std::uint32_t stage_bytes);
 int prepare_bcast_kernels(std::size_t smem);

@@ -307,6 +307,18 @@ __device__ std::uint64_t read_mbox(const Ctx& c, const std::uint64_t* slot, int 
   return __shfl_sync(0xffffffffu, value, 0);
 }
 
+// A peer buffer address from its mailbox value: a raw pointer (one process,
+// UVA), a symmetric-heap offset (per-process ranks), or, with the registration
+// id in bits 40-47, an offset into a registered allocation of that peer as
+// mapped here (bcl_comm_register_*).
+__device__ __forceinline__ std::uint64_t peer_addr(const RankWork& W, int peer, std::uint64_t v) {
+  const std::uint64_t id = v >> 40;
+  if (W.peers->regs != nullptr && id != 0) {
+    return W.peers->regs[static_cast<std::size_t>(peer) * kMaxRegs + id - 1] + (v & ((1ull << 40) - 1));
+  }
+  return W.peers->addr_base[peer] + v;
+}
+
 // A remote store straight from the copy warp, for hand-offs that need no
 // fence: the head's "every chunk ready" (its data was written by earlier
 // stream work) and a consumer's final ack (its reads have completed). Safe to
@@ -642,7 +654,7 @@ __device__ void run_chain_push(Ctx& c, int pipe, int q, int ns) {
   }
   if (!wait_geq(c, W.acks + static_cast<std::size_t>(next) * L + c.ell, P.epoch, next, 0)) return;
   auto* dst = reinterpret_cast<std::uint8_t*>(
-      W.peers->addr_base[next] + read_mbox(c, W.mbox + 2 * (static_cast<std::size_t>(next) * L + c.ell), next));
+      peer_addr(W, next, read_mbox(c, W.mbox + 2 * (static_cast<std::size_t>(next) * L + c.ell), next)));
   std::uint64_t* next_flag = W.peers->flags[next] + slot;
   const bool aligned = c.stage != nullptr &&
                        ((reinterpret_cast<std::uintptr_t>(dst) | reinterpret_cast<std::uintptr_t>(W.buf)) & 15u) == 0 &&
@@ -693,7 +705,7 @@ __device__ void run_chain(Ctx& c, int pipe, int q, int ns) {
     if (c.stage != nullptr) {
       if (!wait_geq(c, ready, tag | 1, prev, pipe)) return;
       src = reinterpret_cast<const std::uint8_t*>(
-          W.peers->addr_base[prev] + read_mbox(c, W.mbox + 2 * (static_cast<std::size_t>(prev) * L + c.ell), prev));
+          peer_addr(W, prev, read_mbox(c, W.mbox + 2 * (static_cast<std::size_t>(prev) * L + c.ell), prev)));
       const bool aligned = ((reinterpret_cast<std::uintptr_t>(src) | reinterpret_cast<std::uintptr_t>(W.buf)) & 15u) == 0 &&
                            (P.chunk_bytes & 15u) == 0 && (P.slice_bytes & 15u) == 0 &&
                            P.slice_bytes <= P.stage_bytes;
@@ -713,7 +725,7 @@ __device__ void run_chain(Ctx& c, int pipe, int q, int ns) {
       const std::uint64_t t_ready = W.trace ? globaltimer() : 0;
       if (k == 0) {
         src = reinterpret_cast<const std::uint8_t*>(
-            W.peers->addr_base[prev] + read_mbox(c, W.mbox + 2 * (static_cast<std::size_t>(prev) * L + c.ell), prev));
+            peer_addr(W, prev, read_mbox(c, W.mbox + 2 * (static_cast<std::size_t>(prev) * L + c.ell), prev)));
       }
       pull_slice(c, pipe + k * ns, q, src, prev);
       if (has_next) publish(c, W.peers->flags[next] + slot, tag | (k + 1));  // forward chunk k
@@ -764,7 +776,7 @@ __device__ void run_events(Ctx& c, int pipe, int q, int ns) {
       if (!((recv_mask >> peer) & 1u)) {
         recv_mask |= 1ull << peer;
         src_of[peer] = reinterpret_cast<const std::uint8_t*>(
-            W.peers->addr_base[peer] + read_mbox(c, W.mbox + 2 * (static_cast<std::size_t>(peer) * L + c.ell), peer));
+            peer_addr(W, peer, read_mbox(c, W.mbox + 2 * (static_cast<std::size_t>(peer) * L + c.ell), peer)));
       }
       pull_slice(c, ch, q, src_of[peer], peer);
       trace_pull(c, k++, t_wait, t_ready);
@@ -1010,14 +1022,23 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ 
   }
 }
 
-// LL128 pipelined chain (cross-GPU hops only). A 128-byte line carries 120
-// payload bytes and the epoch in its last 8 bytes; eight threads own one line
-// (16 bytes each) and a warp moves four lines per instruction. Like NCCL's
-// LL128 this relies on NVLink delivering each 128-byte warp-coalesced store
-// as one unit: a reader that sees the new epoch in a line's flag word sees
-// the whole line. Readers vote per warp and reload until all four flags match.
+// LL128 pipelined chain. A 128-byte line carries 120 payload bytes and a flag
+// in its last 8 bytes; eight threads own one line (16 bytes each) and a warp
+// moves four lines (a "group") per instruction. Like NCCL's LL128 this relies
+// on a 128-byte warp-coalesced store arriving as one unit (over NVLink, and
+// through L2 between ranks sharing a GPU): a reader that sees a line's flag
+// sees the whole line. Readers vote per warp and reload until all four flags
+// match. Lines land in a bounded ring: warp w's k-th group goes to slot
+// (w * D + k % D) of its successor's ring with flag (epoch << 20 | k / D); a
+// writer reuses a slot once the successor's warp w has returned a credit
+// for the group D earlier (credits every D / 2 groups, per warp).
 __device__ __forceinline__ void st_volatile_v2u64(ulonglong2* p, unsigned long long a, unsigned long long b) {
   asm volatile("st.volatile.global.v2.u64 [%0], {%1,%2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const std::uint64_t* p) {
+  unsigned long long v;
+  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 __device__ __forceinline__ ulonglong2 ld_volatile_v2u64(const ulonglong2* p) {
   ulonglong2 v;
@@ -1042,11 +1063,9 @@ __device__ __forceinline__ void ll128_put(std::uint8_t* buf, std::uint64_t off, 
   for (std::uint32_t b = 0; b < len; ++b) buf[off + b] = static_cast<std::uint8_t>(v >> (8 * b));
 }
 
-// NL > 1: ranks sharing one GPU (cooperative launch, P.ctas CTAs per rank) —
-// the same line protocol through L2 instead of NVLink, so the cross-GPU
-// kernel is parity-tested on a single B200.
+// NL > 1: ranks sharing one GPU (cooperative launch, P.ctas CTAs per rank).
 template <int NL>
-__global__ void __launch_bounds__(kLLThreads) ll128_kernel(const __grid_constant__ LLParamsT<NL> P) {
+__global__ void __launch_bounds__(kLLThreads, 3) ll128_kernel(const __grid_constant__ LLParamsT<NL> P) {
   const LLRank& R = P.ranks[NL == 1 ? 0 : static_cast<int>(blockIdx.x) / P.ctas];
   const std::uint32_t cta = NL == 1 ? blockIdx.x : blockIdx.x % P.ctas;
   const int lane = static_cast<int>(threadIdx.x & 31);
@@ -1054,13 +1073,13 @@ __global__ void __launch_bounds__(kLLThreads) ll128_kernel(const __grid_constant
   const int sub = lane >> 3;  // line within the warp's group of four
   const std::uint32_t warp = (cta * blockDim.x + threadIdx.x) >> 5;
   const std::uint32_t warps = (static_cast<std::uint32_t>(P.ctas) * blockDim.x) >> 5;
-  const unsigned long long flag = P.epoch;
+  const unsigned long long epoch = P.epoch;
   const int n = P.n_ranks;
   const int logical = (R.rank - P.root + n) % n;
   const int next = (R.rank + 1) % n;
+  const int source = (R.rank + n - 1) % n;
   const bool writer = logical + 1 < n;
-  const std::size_t area = P.chain128_area + static_cast<std::size_t>(P.half) * P.chain128_lines * 8;
-  if (writer) {
+  if (writer) {  // the successor finished reading our previous LL128 call (ring reuse across calls)
     if (R.need_credit > 0 && static_cast<int>(threadIdx.x) == next) {
       const std::uint64_t t0 = globaltimer();
       std::uint64_t v;
@@ -1083,33 +1102,74 @@ __global__ void __launch_bounds__(kLLThreads) ll128_kernel(const __grid_constant
     *len0 = clip(*off);
     *len1 = part == 7 ? 0u : clip(*off + 8);
   };
-  uint4* const base_self = R.ll + area;
+  const ulonglong2* ring_self = reinterpret_cast<const ulonglong2*>(R.ll + P.chain128_area);
+  ulonglong2* ring_next = writer ? reinterpret_cast<ulonglong2*>(R.peers->ll[next] + P.chain128_area) : nullptr;
+  const std::uint64_t* my_credit = R.wcredit + warp;  // our successor's consumption of our groups
+  std::uint64_t* prev_credit = logical > 0 ? R.peers->wcredit[source] + warp : nullptr;
+  const unsigned long long ctag = epoch << 32;
+  auto at = [&](std::uint32_t k) -> std::size_t {  // this thread's 16-byte word of group k's slot
+    return ((static_cast<std::size_t>(warp) * kLL128Depth + k % kLL128Depth) * 4 + sub) * 8 + part;
+  };
+  auto flag_of = [&](std::uint32_t k) -> unsigned long long { return (epoch << 20) | (k / kLL128Depth); };
+  // Warp-collective: the successor has consumed our group k - D (its slot is
+  // free). The last credit seen is cached (warp-uniform), so the local credit
+  // word is polled about once per D / 2 groups. Like NCCL's LL128 credits the
+  // overwrite is ordered after the poll by its control dependency (no acquire:
+  // an acquire invalidates L1 on every call, ~6% at 64 MiB, n = 4).
+  unsigned long long seen = 0;
+  auto room = [&](std::uint32_t k) -> bool {
+    if (k < static_cast<std::uint32_t>(kLL128Depth)) return true;
+    const unsigned long long want = ctag | (k - kLL128Depth + 1);
+    if (seen >= want) return true;
+    int ok = 1;
+    unsigned long long v = 0;
+    if (lane == 0) {
+      v = ld_volatile_u64(my_credit);
+      if (v < want) {
+        const std::uint64_t t0 = globaltimer();
+        unsigned spins = 0;
+        while ((v = ld_volatile_u64(my_credit)) < want) {
+          if ((++spins & 1023u) == 0) {
+            if (*(volatile int*)R.abort != 0) { ok = 0; break; }
+            if (globaltimer() - t0 > P.timeout_ns) {
+              ll_fail(R, next, k, v, want);
+              ok = 0;
+              break;
+            }
+          }
+        }
+      }
+    }
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+    seen = __shfl_sync(0xffffffffu, v, 0);
+    return ok != 0;
+  };
   if (logical == 0) {
-    ulonglong2* dst = reinterpret_cast<ulonglong2*>(R.peers->ll[next] + area);
-    for (std::uint32_t g = warp; g * 4 < P.lines; g += warps) {
+    std::uint32_t k = 0;
+    for (std::uint32_t g = warp; g * 4 < P.lines; g += warps, ++k) {
+      if (!room(k)) return;
       const std::uint32_t line = g * 4 + sub;
       if (line >= P.lines) continue;
       std::uint64_t off;
       std::uint32_t l0, l1;
       piece(line, &off, &l0, &l1);
       const unsigned long long a = ll128_get(R.buf, off, l0, aligned);
-      const unsigned long long b = part == 7 ? flag : ll128_get(R.buf, off + 8, l1, aligned);
-      st_volatile_v2u64(dst + static_cast<std::size_t>(line) * 8 + part, a, b);
+      const unsigned long long b = part == 7 ? flag_of(k) : ll128_get(R.buf, off + 8, l1, aligned);
+      st_volatile_v2u64(ring_next + at(k), a, b);
     }
     return;
   }
-  const ulonglong2* src = reinterpret_cast<const ulonglong2*>(base_self);
-  ulonglong2* fwd = writer ? reinterpret_cast<ulonglong2*>(R.peers->ll[next] + area) : nullptr;
-  const int source = (R.rank + n - 1) % n;
   bool ok = true;
-  for (std::uint32_t g = warp; g * 4 < P.lines && ok; g += warps) {
+  std::uint32_t k = 0;
+  for (std::uint32_t g = warp; g * 4 < P.lines && ok; g += warps, ++k) {
     const std::uint32_t line = g * 4 + sub;
     const bool active = line < P.lines;
+    const unsigned long long flag = flag_of(k);
     ulonglong2 v = make_ulonglong2(0, 0);
     const std::uint64_t t0 = globaltimer();
     unsigned spins = 0;
     while (true) {
-      if (active) v = ld_volatile_v2u64(src + static_cast<std::size_t>(line) * 8 + part);
+      if (active) v = ld_volatile_v2u64(ring_self + at(k));
       const bool stale = active && part == 7 && v.y != flag;
       if (!__any_sync(0xffffffffu, stale)) break;
       if ((++spins & 1023u) == 0) {
@@ -1122,13 +1182,26 @@ __global__ void __launch_bounds__(kLLThreads) ll128_kernel(const __grid_constant
       }
     }
     if (!ok) break;
-    if (!active) continue;
-    if (fwd != nullptr) st_volatile_v2u64(fwd + static_cast<std::size_t>(line) * 8 + part, v.x, v.y);
-    std::uint64_t off;
-    std::uint32_t l0, l1;
-    piece(line, &off, &l0, &l1);
-    ll128_put(R.buf, off, l0, aligned, v.x);
-    if (part != 7) ll128_put(R.buf, off + 8, l1, aligned, v.y);
+    if (writer) {  // forward the very same line into the successor's ring
+      if (!room(k)) {
+        ok = false;
+        break;
+      }
+      if (active) st_volatile_v2u64(ring_next + at(k), v.x, v.y);
+    }
+    if (active) {
+      std::uint64_t off;
+      std::uint32_t l0, l1;
+      piece(line, &off, &l0, &l1);
+      ll128_put(R.buf, off, l0, aligned, v.x);
+      if (part != 7) ll128_put(R.buf, off + 8, l1, aligned, v.y);
+    }
+    if ((k + 1) % (kLL128Depth / 2) == 0) {
+      // Every lane's loads of these groups have returned (their values were
+      // stored above), so the predecessor may overwrite the slots.
+      __syncwarp();
+      if (lane == 0) st_relaxed_sys(prev_credit, ctag | (k + 1));
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0 && ok) {
@@ -1229,6 +1302,11 @@ int local_chain_occupancy(int* blocks_per_sm) {
   return static_cast<int>(cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, dev::local_chain_kernel, 256, 0));
 }
 
+int ll128_occupancy(int* blocks_per_sm) {
+  return static_cast<int>(
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, dev::ll128_kernel<1>, dev::kLLThreads, 0));
+}
+
 int launch_local_chain(const dev::LocalChainParams& p, int ctas, void* stream) {
   dev::local_chain_kernel<<<static_cast<unsigned>(ctas), 256, 0, static_cast<cudaStream_t>(stream)>>>(p);
   return static_cast<int>(cudaGetLastError());
@@ -1254,7 +1332,9 @@ int launch_ll(const dev::LLParams& p, void* stream) {
   cfg.stream = static_cast<cudaStream_t>(stream);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = p.n_local > 1 ? 1 : 0;
+  // LL128 writers wait on ring credits from the successor's CTAs: co-residency
+  // is required even for one rank per GPU (the successor's warp w may be any CTA).
+  attr[0].val.cooperative = (p.n_local > 1 || p.chain == 2) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (p.n_local == 1) {

@@ -50,7 +50,7 @@ def run_group(comms, devices, algo, root, m, chunk=0, radix=2, seed=1):
 def test_one_process_all_gpus_every_algorithm_and_root():
     devices = list(range(min(ngpu(), 8)))
     comms = B.Comm.local(devices, timeout_s=10)
-    assert comms[0].protocol_caps()["ll128"] == (512 << 20 if len(devices) > 2 else 32 << 20)  # own GPU each
+    assert comms[0].protocol_caps()["ll128"] == 1 << 62  # own GPU each: LL128 ring, no size limit but the table rule
     rng = random.Random(17)
     for algo in ("chain_pipelined", "chain_pipelined/ll", "chain_pipelined/pull", "chain_pipelined/push",
                  "knomial", "scatter_ring_allgather", "direct", "chain"):
@@ -113,7 +113,7 @@ def test_ll128_chain_back_to_back_stress():
         B.run_bcast(comms, root, views, m, cfg_of("chain_pipelined", 262144))
         for r in range(n):
             assert torch.equal(views[r].cpu(), src.cpu()), ("misaligned", m, offs, r)
-    with pytest.raises(ValueError):  # above the LL128 landing area
+    with pytest.raises(ValueError):  # above the communicator's ll128_max
         B.run_bcast(comms, 0, [b[:cap + 1] for b in bufs], cap + 1, cfg_of("chain_pipelined", 262144))
     for c in comms:
         c.set_protocol("auto")
@@ -174,6 +174,33 @@ def _ipc_worker(rank, world, port, q):
             comm.bcast(buf, m, "uint8", root, cfg_of(algo, 524288, 2))
             comm.check()
             ok &= buf[:m].cpu().numpy().tobytes() == payload
+        # arbitrary cudaMalloc'd buffers (torch's allocator): the line
+        # protocols take them as they are; the lane executor after a
+        # collective registration of their allocation (bcl_comm_register_*)
+        plain = torch.zeros((6 << 20) + 64, dtype=torch.uint8, device=f"cuda:{rank}")
+        for it, (proto, m, root, off) in enumerate([("auto", 100000, 0, 0), ("ll128", (5 << 20) + 1, world - 1, 3)]):
+            comm.set_protocol(proto)
+            payload = O.payload(200 + it, m)
+            view = plain[off:off + m]
+            (view.copy_(torch.frombuffer(bytearray(payload), dtype=torch.uint8)) if rank == root else view.zero_())
+            torch.cuda.synchronize()
+            dist.barrier()
+            comm.bcast(view, m, "uint8", root, cfg_of("chain_pipelined", 65536))
+            comm.check()
+            ok &= view.cpu().numpy().tobytes() == payload
+        comm.register(plain)
+        for it, (proto, m, root, off) in enumerate([("pull", (6 << 20) + 7, 0, 5), ("push", 1 << 20, world - 1, 0),
+                                                    ("pull", 3 << 20, 1 % world, 16)]):
+            comm.set_protocol(proto)
+            payload = O.payload(300 + it, m)
+            view = plain[off:off + m]
+            (view.copy_(torch.frombuffer(bytearray(payload), dtype=torch.uint8)) if rank == root else view.zero_())
+            torch.cuda.synchronize()
+            dist.barrier()
+            comm.bcast(view, m, "uint8", root, cfg_of("chain_pipelined", 262144))
+            comm.check()
+            ok &= view.cpu().numpy().tobytes() == payload
+        comm.set_protocol("auto")
         # host-buffer entry point (pipelined H2D / broadcast / D2H pieces)
         m = (9 << 20) + 3
         payload = O.payload(99, m)

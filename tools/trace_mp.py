@@ -21,6 +21,7 @@ torch.cuda.synchronize()  # ref is written on the default stream; s reads it
 cap = 1024
 tr = torch.zeros(L * cap * 4, dtype=torch.int64, device=dev)
 cfg = B.AlgorithmConfig(B.Algorithm.chain_pipelined, 0, chunk)
+comm.set_protocol(os.environ.get("TRACE_PROTO", "pull"))  # the timeline records the lane executor only
 s = torch.cuda.Stream(device=dev)
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 evb = torch.cuda.Event(enable_timing=True)
