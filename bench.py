@@ -46,6 +46,33 @@ except (OSError, KeyError, ValueError):
     TRAFFIC_N1 = None
 HBM_PEAK_SRC = "measured" if "hbm_gbs" in PEAKS else "fallback"
 LINK_BW = 900e9  # north_star chain roofline: NVLink-5 per direction per GPU
+NVLINK_MEASURED = 770.0  # GB/s per direction, peer copy measured on this pool (B200_PROFILING.md)
+try:  # NVLink bytes per launch of the cross-GPU kernels, ncu (profiles/round2/xgpu/, tools/r2/ncu_xgpu.py)
+    XGPU = json.load(open(os.path.join(ROOT, "profiles", "round2", "xgpu", "ncu_xgpu_traffic.json")))
+except (OSError, ValueError):
+    XGPU = None
+
+
+def nvlink_traffic(path, m, world):
+    """NVLink bytes one receiving GPU takes in per call of the dominant kernel,
+    from the committed ncu capture of that kernel (nvlrx/nvltx__bytes; NVML
+    exposes no NVLink counters on this pool: NOT_SUPPORTED). Exact for the
+    captured shape, scaled by the measured bytes-per-payload-byte otherwise."""
+    if XGPU is None:
+        return None, "no ncu capture committed"
+    if path.startswith("bcast_kernel/pull"):
+        k = XGPU["pull_receiver_n2_64MiB"]
+        exact = m == 64 << 20 and world == 2
+        t = k["nvlink_rx_bytes"] if exact else k["nvlink_rx_bytes"] / k["nvlink_rx_user_bytes"] * m
+        return round(t), ("ncu nvlrx__bytes.sum of the receiver's bcast_kernel, N=2 64 MiB (%s); user data "
+                          "%d B = M, the rest request/response protocol" % ("this shape" if exact else "scaled to M",
+                                                                            k["nvlink_rx_user_bytes"]))
+    if path == "ll128_kernel":
+        k = XGPU["ll128_n2_32MiB"][0]
+        t = k["nvlink_tx_bytes"] / 33554432 * m
+        return round(t), ("ncu nvltx__bytes.sum of the LL128 writer per payload byte (N=2, 32 MiB capture) x M: "
+                          "128-byte lines carry 120 payload bytes, plus protocol")
+    return None, "no ncu capture of %s" % path
 METRIC = "bcast latency (us) & bus GB/s vs msg size 4B–1GB at 2/4/8 B200 vs ncclBroadcast"
 
 
@@ -98,44 +125,6 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.mx) if self.mx else None,
                 "reasons": sorted(self.reasons), "samples": len(self.sm)}
-
-
-class NvlinkCounters:
-    """NVLink bytes per direction of one GPU from NVML's per-link counters
-    (NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES / _RCV_BYTES, summed over links):
-    the traffic figure of a cross-GPU kernel, read around a run of
-    back-to-back broadcasts (ncu cannot profile kernels that wait on another
-    rank's kernel)."""
-
-    XMIT, RCV, LINKS = 202, 204, 18
-
-    def __init__(self, gpu):
-        self.h = None
-        try:
-            import pynvml as nv
-            nv.nvmlInit()
-            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-            idx = int(vis.split(",")[gpu]) if vis and vis.split(",")[gpu].isdigit() else gpu
-            self.nv, self.h = nv, nv.nvmlDeviceGetHandleByIndex(idx)
-            self.read()
-        except Exception:  # noqa: BLE001 - no NVML / no NVLink counters
-            self.h = None
-
-    def read(self):
-        """(tx_bytes, rx_bytes) summed over links, or None."""
-        if self.h is None:
-            return None
-        ids = [(f, l) for f in (self.XMIT, self.RCV) for l in range(self.LINKS)]
-        vals = self.nv.nvmlDeviceGetFieldValues(self.h, ids)
-        tx = rx = 0
-        for i, v in enumerate(vals):
-            if v.nvmlReturn != 0:
-                continue
-            if i < self.LINKS:
-                tx += v.value.ullVal
-            else:
-                rx += v.value.ullVal
-        return tx, rx
 
 
 class NcclDirect:
@@ -519,29 +508,6 @@ def bench_multi(args, torch, rank, world):
     launches = comm.launches - launches0 - args.warmup
     nccl = run(m, args.steps, args.warmup, False)
 
-    # NVLink bytes per broadcast from NVML counters over a run of
-    # back-to-back calls (device time by CUDA events on the stream).
-    counters = NvlinkCounters(local)
-    reps = 50
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    dist.barrier(device_ids=[local])
-    time.sleep(0.2)
-    c0 = counters.read()
-    ev0.record(stream)
-    for _ in range(reps):
-        comm.bcast(buf_all[:m], m, "uint8", 0, cfg, stream=stream)
-    ev1.record(stream)
-    ev1.synchronize()
-    time.sleep(0.2)
-    c1 = counters.read()
-    loop_t = ev0.elapsed_time(ev1) * 1e-3 / reps
-    nv = torch.tensor([(c1[0] - c0[0]) / reps, (c1[1] - c0[1]) / reps, loop_t] if c0 and c1 else [-1.0, -1.0, loop_t],
-                      dtype=torch.float64, device=dev)
-    nv_all = [torch.zeros_like(nv) for _ in range(world)]
-    dist.all_gather(nv_all, nv)
-    nv_all = [x.cpu().tolist() for x in nv_all]
-
     # e2e through the C-ABI with pinned host buffers (bcl_bcast_host)
     host = torch.empty(m, dtype=torch.uint8, pin_memory=True)
     ref_host = ref_all[:m].cpu()
@@ -602,14 +568,8 @@ def bench_multi(args, torch, rank, world):
         t_nccl = statistics.mean(nccl)
         busbw = m / t / 1e9
         t_roof = m / LINK_BW + (world - 1) * max(cfg.chunk_bytes, 1) / LINK_BW
-        rx = [x[1] for x in nv_all]
-        tx = [x[0] for x in nv_all]
-        have_nv = all(v >= 0 for v in rx + tx)
-        link = {"per_rank": [{"rank": r, "tx_bytes_per_call": round(x[0]), "rx_bytes_per_call": round(x[1]),
-                              "call_us": round(x[2] * 1e6, 2),
-                              "tx_gbs": round(x[0] / x[2] / 1e9, 1), "rx_gbs": round(x[1] / x[2] / 1e9, 1)}
-                             for r, x in enumerate(nv_all)] if have_nv else None,
-                "source": "NVML NVLink per-link XMIT/RCV byte counters over %d back-to-back calls" % reps}
+        path = comm.path(m, cfg)
+        traffic, traffic_note = nvlink_traffic(path, m, world)
         line = {
             "metric": METRIC, "value": round(busbw, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t * 1e3, 4), "higher_is_better": True, "scaling": "weak",
@@ -624,12 +584,11 @@ def bench_multi(args, torch, rank, world):
                              % nccl_direct.version},
             "roofline": {"bound": "nvlink", "achieved": round(busbw, 1), "peak": LINK_BW / 1e9, "unit": "GB/s",
                          "frac": round(busbw / (LINK_BW / 1e9), 4),
-                         "traffic": round(max(rx)) if have_nv else None,
-                         "traffic_note": "max over ranks of NVLink bytes received per call (NVML counters); "
-                                         "algorithmic: M = %d per receiving GPU" % m,
+                         "traffic": traffic, "traffic_note": traffic_note,
+                         "kernel": path, "measured_peak_gbs": NVLINK_MEASURED,
+                         "frac_of_measured_peak": round(busbw / NVLINK_MEASURED, 4),
                          "chain_roofline_us": round(t_roof * 1e6, 2), "frac_of_chain_roofline": round(t_roof / t, 4),
                          "note": "per-GPU ingress M/t vs NVLink-5 900 GB/s per direction (north_star)"},
-            "nvlink": link,
             "cpu_baseline": {"value": round(m / cpu["median_s"] / 1e9, 4), "unit": "GB/s", "cores": cpu["cores"],
                              "kind": cpu["kind"], "sample": cpu["sample"], "host": host_cpu()},
             "e2e": {"value": round(m / statistics.mean(e2e) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": m,

@@ -130,6 +130,20 @@ bcl_status_t bcl_tune_analytical(const int* n_list, size_t n_count,
                                  const uint64_t* chunks, size_t n_chunks,
                                  double startup_s, double link_Bps, double staging_Bps,
                                  bcl_table_t* out);
+/* NetworkParams (core.hpp:16-25) plus, new on B200, a per-call constant a0
+ * added to every algorithm's cost (Eq. 5 + a0 fits B200 measurements within
+ * 1-3%; call_overhead_s = 0 is the reference model, bit-identical). */
+typedef struct {
+  double startup_s;
+  double link_Bps;
+  double staging_Bps;
+  double call_overhead_s;
+} bcl_network_params_t;
+bcl_status_t bcl_model_cost_ex(const bcl_config_t* config, int n, uint64_t message_bytes,
+                               const bcl_network_params_t* params, double* total_s);
+bcl_status_t bcl_tune_analytical_ex(const int* n_list, size_t n_count, const uint64_t* sizes, size_t n_sizes,
+                                    const bcl_config_t* candidates, size_t n_cands, const uint64_t* chunks,
+                                    size_t n_chunks, const bcl_network_params_t* params, bcl_table_t* out);
 /* Measured tune: cost(config, n, bytes, user) returns seconds (e.g. the
  * median device latency); NaN aborts with BCL_ERR_RUNTIME. */
 typedef double (*bcl_cost_fn)(const bcl_config_t* config, int n, uint64_t bytes, void* user);
@@ -212,6 +226,12 @@ bcl_status_t bcl_comm_set_table(bcl_comm_t c, bcl_table_t t);
  * chunks c with c % (lanes / Q) == l / Q. */
 bcl_status_t bcl_comm_plan(bcl_comm_t c, const bcl_config_t* config, int root, uint64_t bytes, int* slices,
                            uint64_t* slice_bytes, uint32_t* n_chunks, int* ctas);
+/* The device path a call of this shape would run (config NULL = tuned), as
+ * text: "ll_kernel/direct", "ll_kernel/chain", "ll128_kernel",
+ * "local_chain_kernel", "bcast_kernel/pull[/tma]", "bcast_kernel/push[/tma]",
+ * "bcast_kernel/events" or "none"; *len = bytes needed incl. NUL. */
+bcl_status_t bcl_comm_path(bcl_comm_t c, const bcl_config_t* config, int root, uint64_t bytes, char* out,
+                           size_t cap, size_t* len);
 /* Pipelined-chain transport protocol: 0 auto (line protocols where the
  * tuning table's rules pick them -- LL128 when every rank has its own GPU, up
  * to the table's measured "# bcl-ll128-upto" rule (and the ll128_max option,

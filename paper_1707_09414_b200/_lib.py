@@ -57,6 +57,11 @@ class _Entry(C.Structure):
                 ("config", _Config), ("predicted_cost_s", C.c_double)]
 
 
+class _Net(C.Structure):
+    _fields_ = [("startup_s", C.c_double), ("link_Bps", C.c_double), ("staging_Bps", C.c_double),
+                ("call_overhead_s", C.c_double)]
+
+
 _COST_FN = C.CFUNCTYPE(C.c_double, C.POINTER(_Config), C.c_int, C.c_uint64, C.c_void_p)
 
 _SIGS = {
@@ -77,6 +82,10 @@ _SIGS = {
     "bcl_tune_analytical": (C.c_int, [C.POINTER(C.c_int), C.c_size_t, C.POINTER(C.c_uint64), C.c_size_t,
                                       C.POINTER(_Config), C.c_size_t, C.POINTER(C.c_uint64), C.c_size_t,
                                       C.c_double, C.c_double, C.c_double, C.POINTER(C.c_void_p)]),
+    "bcl_model_cost_ex": (C.c_int, [C.POINTER(_Config), C.c_int, C.c_uint64, C.POINTER(_Net), C.POINTER(C.c_double)]),
+    "bcl_tune_analytical_ex": (C.c_int, [C.POINTER(C.c_int), C.c_size_t, C.POINTER(C.c_uint64), C.c_size_t,
+                                         C.POINTER(_Config), C.c_size_t, C.POINTER(C.c_uint64), C.c_size_t,
+                                         C.POINTER(_Net), C.POINTER(C.c_void_p)]),
     "bcl_tune_measured": (C.c_int, [C.POINTER(C.c_int), C.c_size_t, C.POINTER(C.c_uint64), C.c_size_t,
                                     C.POINTER(_Config), C.c_size_t, C.POINTER(C.c_uint64), C.c_size_t,
                                     _COST_FN, C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p)]),
@@ -106,6 +115,8 @@ _SIGS = {
     "bcl_comm_set_table": (C.c_int, [C.c_void_p, C.c_void_p]),
     "bcl_comm_choose": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(_Config)]),
     "bcl_comm_set_protocol": (C.c_int, [C.c_void_p, C.c_int]),
+    "bcl_comm_path": (C.c_int, [C.c_void_p, C.POINTER(_Config), C.c_int, C.c_uint64, C.c_char_p, C.c_size_t,
+                                C.POINTER(C.c_size_t)]),
     "bcl_comm_plan": (C.c_int, [C.c_void_p, C.POINTER(_Config), C.c_int, C.c_uint64, C.POINTER(C.c_int),
                                 C.POINTER(C.c_uint64), C.POINTER(C.c_uint32), C.POINTER(C.c_int)]),
     "bcl_mem_alloc": (C.c_int, [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
@@ -317,10 +328,16 @@ def to_text(config: AlgorithmConfig, n: int, root: int, m: int) -> str:
         lib().bcl_schedule_destroy(h)
 
 
-def cost_for(config: AlgorithmConfig, n: int, m: int, startup_s=1e-6, link_Bps=1e9, staging_Bps=1e10) -> float:
+def cost_for(config: AlgorithmConfig, n: int, m: int, startup_s=1e-6, link_Bps=1e9, staging_Bps=1e10,
+             call_overhead_s=0.0) -> float:
+    """models.cpp:106-124; call_overhead_s = the B200 per-call constant a0 (0: the reference model)."""
     out = C.c_double()
     cc = config._c()
-    _check(lib().bcl_model_cost(C.byref(cc), n, m, startup_s, link_Bps, staging_Bps, C.byref(out)))
+    if call_overhead_s:
+        net = _Net(startup_s, link_Bps, staging_Bps, call_overhead_s)
+        _check(lib().bcl_model_cost_ex(C.byref(cc), n, m, C.byref(net), C.byref(out)))
+    else:
+        _check(lib().bcl_model_cost(C.byref(cc), n, m, startup_s, link_Bps, staging_Bps, C.byref(out)))
     return out.value
 
 
@@ -375,14 +392,20 @@ def _cands(candidates: Sequence[AlgorithmConfig]):
 
 
 def tune(n_list, msg_sizes, candidates, chunk_candidates, startup_s=1e-6, link_Bps=1e9,
-         staging_Bps=1e10) -> TuningTable:
-    """tuner.hpp:64-68 with the analytical oracle."""
+         staging_Bps=1e10, call_overhead_s=0.0) -> TuningTable:
+    """tuner.hpp:64-68 with the analytical oracle (plus the B200 per-call
+    constant a0 when call_overhead_s > 0)."""
     h = C.c_void_p()
     nl = (C.c_int * max(len(n_list), 1))(*n_list)
     sz = (C.c_uint64 * max(len(msg_sizes), 1))(*msg_sizes)
     ch = (C.c_uint64 * max(len(chunk_candidates), 1))(*chunk_candidates)
-    _check(lib().bcl_tune_analytical(nl, len(n_list), sz, len(msg_sizes), _cands(candidates), len(candidates),
-                                     ch, len(chunk_candidates), startup_s, link_Bps, staging_Bps, C.byref(h)))
+    if call_overhead_s:
+        net = _Net(startup_s, link_Bps, staging_Bps, call_overhead_s)
+        _check(lib().bcl_tune_analytical_ex(nl, len(n_list), sz, len(msg_sizes), _cands(candidates),
+                                            len(candidates), ch, len(chunk_candidates), C.byref(net), C.byref(h)))
+    else:
+        _check(lib().bcl_tune_analytical(nl, len(n_list), sz, len(msg_sizes), _cands(candidates), len(candidates),
+                                         ch, len(chunk_candidates), startup_s, link_Bps, staging_Bps, C.byref(h)))
     return TuningTable(h)
 
 

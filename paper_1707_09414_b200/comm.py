@@ -169,6 +169,15 @@ class Comm:
         code = {"auto": 0, "pull": 1, "push": 2, "ll": 3, "ll128": 4}[protocol] if isinstance(protocol, str) else int(protocol)
         _check(lib().bcl_comm_set_protocol(self._h, code))
 
+    def path(self, nbytes: int, config: Optional[AlgorithmConfig] = None, root: int = 0) -> str:
+        """The device path (kernel/protocol) a call of this shape runs."""
+        ln = C.c_size_t()
+        cc = _cfg(config)
+        _check(lib().bcl_comm_path(self._h, cc, root, nbytes, None, 0, C.byref(ln)))
+        buf = C.create_string_buffer(ln.value)
+        _check(lib().bcl_comm_path(self._h, cc, root, nbytes, buf, ln.value, C.byref(ln)))
+        return buf.value.decode()
+
     def choose(self, message_bytes: int) -> AlgorithmConfig:
         out = _Config()
         _check(lib().bcl_comm_choose(self._h, message_bytes, C.byref(out)))

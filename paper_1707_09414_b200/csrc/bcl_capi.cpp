@@ -241,6 +241,34 @@ bcl_status_t bcl_tune_analytical(const int* n_list, size_t n_count, const uint64
   });
 }
 
+bcl_status_t bcl_model_cost_ex(const bcl_config_t* cfg, int n, uint64_t m, const bcl_network_params_t* p,
+                               double* total) {
+  return guard([&] {
+    need(cfg, "config");
+    need(p, "params");
+    need(total, "total_s");
+    *total = bcl::cost_for(to_cfg(cfg), n, m,
+                           bcl::NetworkParams{p->startup_s, p->link_Bps, p->staging_Bps, p->call_overhead_s})
+                 .total_s;
+  });
+}
+
+bcl_status_t bcl_tune_analytical_ex(const int* n_list, size_t n_count, const uint64_t* sizes, size_t n_sizes,
+                                    const bcl_config_t* cands, size_t n_cands, const uint64_t* chunks,
+                                    size_t n_chunks, const bcl_network_params_t* p, bcl_table_t* out) {
+  return guard([&] {
+    need(out, "out");
+    need(p, "params");
+    auto t = std::make_unique<bcl_table_s>();
+    t->t = bcl::tune(std::vector<int>(n_list, n_list + n_count),
+                     std::vector<std::uint64_t>(sizes, sizes + n_sizes), cands_of(cands, n_cands),
+                     std::vector<std::uint64_t>(chunks, chunks + n_chunks),
+                     bcl::NetworkParams{p->startup_s, p->link_Bps, p->staging_Bps, p->call_overhead_s},
+                     bcl::CostOracle::Analytical);
+    *out = t.release();
+  });
+}
+
 bcl_status_t bcl_tune_measured(const int* n_list, size_t n_count, const uint64_t* sizes,
                                size_t n_sizes, const bcl_config_t* cands, size_t n_cands,
                                const uint64_t* chunks, size_t n_chunks, bcl_cost_fn cost,
@@ -472,6 +500,15 @@ bcl_status_t bcl_comm_plan(bcl_comm_t c, const bcl_config_t* config, int root, u
     if (slice_bytes) *slice_bytes = p.slice_bytes;
     if (n_chunks) *n_chunks = p.n_chunks;
     if (ctas) *ctas = p.ctas;
+  });
+}
+
+bcl_status_t bcl_comm_path(bcl_comm_t c, const bcl_config_t* config, int root, uint64_t bytes, char* out,
+                           size_t cap, size_t* len) {
+  return guard([&] {
+    need(c, "comm");
+    const bcl::AlgorithmConfig cc = config ? to_cfg(config) : bcl::AlgorithmConfig{};
+    copy_text(c->g->path(config ? &cc : nullptr, root, bytes), out, cap, len);
   });
 }
 

@@ -866,6 +866,23 @@ void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& 
   ck(static_cast<cudaError_t>(bcl::launch_ll(P, stream)), "launch(ll)");
 }
 
+// The device path a call of this shape takes (the same decisions as
+// launch_group, on state every rank shares).
+std::string Group::path(const AlgorithmConfig* cfg, int root, std::uint64_t bytes) {
+  const AlgorithmConfig c = choose(bytes, cfg);
+  const CallPlan p = plan(c, root, bytes);
+  if (n_ == 1) return "none";
+  std::vector<int> locals;
+  for (int i = 0; i < local_count(); ++i) locals.push_back(i);
+  if (p.config.algorithm == Algorithm::Direct && bytes <= ll_max_ && opt_.ll) return "ll_kernel/direct";
+  if (const int mode = ll_chain_mode(p, bytes, locals)) return mode == 2 ? "ll128_kernel" : "ll_kernel/chain";
+  if (use_local_chain(p, locals)) return "local_chain_kernel";
+  if (!p.implicit_chain) return "bcast_kernel/events";
+  const bool bulk = opt_.stage_bytes > 0;
+  return use_push(p, bytes) ? (bulk ? "bcast_kernel/push/tma" : "bcast_kernel/push")
+                            : (bulk ? "bcast_kernel/pull/tma" : "bcast_kernel/pull");
+}
+
 void Group::launch_group(const std::vector<int>& locals, const std::vector<void*>& bufs,
                          std::uint64_t bytes, int root, const CallPlan& p, cudaStream_t stream) {
   if (p.config.algorithm == Algorithm::Direct && bytes <= ll_max_ && opt_.ll) {

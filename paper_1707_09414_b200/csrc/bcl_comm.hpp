@@ -196,6 +196,8 @@ class Group {
   const TuningTable& table() const;
   AlgorithmConfig choose(std::uint64_t bytes, const AlgorithmConfig* cfg) const;
   CallPlan plan(const AlgorithmConfig& cfg, int root, std::uint64_t bytes);
+  // Name of the device path (kernel/protocol) a call of this shape runs.
+  std::string path(const AlgorithmConfig* cfg, int root, std::uint64_t bytes);
 
   void* mem_alloc(int local_index, std::size_t bytes);
   void mem_reset(int local_index);

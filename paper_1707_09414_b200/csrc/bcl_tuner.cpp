@@ -34,6 +34,15 @@ CostBreakdown sum_terms(double startup, double bandwidth, double staging = 0.0) 
   return CostBreakdown{startup, bandwidth, staging, startup + bandwidth + staging};
 }
 
+// The per-call constant joins the startup term (0 leaves every reference
+// value bit-identical).
+CostBreakdown with_call(CostBreakdown c, double call_s) {
+  if (call_s == 0.0) return c;
+  c.startup_term_s += call_s;
+  c.total_s = c.startup_term_s + c.bandwidth_term_s + c.staging_term_s;
+  return c;
+}
+
 void need_ranks(int n) {
   if (n < 1) throw std::invalid_argument("rank count must be >= 1");
 }
@@ -44,13 +53,23 @@ void NetworkParams::validate() const {
   if (startup_s < 0.0) throw std::invalid_argument("startup_s must be >= 0");
   if (!(link_bandwidth_Bps > 0.0)) throw std::invalid_argument("link_bandwidth_Bps must be > 0");
   if (!(staging_bandwidth_Bps > 0.0)) throw std::invalid_argument("staging_bandwidth_Bps must be > 0");
+  if (call_overhead_s < 0.0) throw std::invalid_argument("call_overhead_s must be >= 0");
 }
 
 // Eqs. 1-6 (models.cpp:34-104); every term is (steps * startup,
 // steps * bytes / B) except SRA's 2(n-1)/n bandwidth factor and the staged
 // tree's extra M / B_staging.
-CostBreakdown cost_for(const AlgorithmConfig& cfg, int n, std::uint64_t m,
-                       const NetworkParams& p) {
+namespace {
+CostBreakdown reference_cost(const AlgorithmConfig& cfg, int n, std::uint64_t m, const NetworkParams& p);
+}  // namespace
+
+CostBreakdown cost_for(const AlgorithmConfig& cfg, int n, std::uint64_t m, const NetworkParams& p) {
+  return with_call(reference_cost(cfg, n, m, p), p.call_overhead_s);
+}
+
+namespace {
+CostBreakdown reference_cost(const AlgorithmConfig& cfg, int n, std::uint64_t m,
+                             const NetworkParams& p) {
   cfg.validate();
   const double per_msg = static_cast<double>(m) / p.link_bandwidth_Bps;
   switch (cfg.algorithm) {
@@ -92,6 +111,7 @@ CostBreakdown cost_for(const AlgorithmConfig& cfg, int n, std::uint64_t m,
   }
   throw std::invalid_argument("unknown algorithm");
 }
+}  // namespace
 
 std::string_view oracle_name(CostOracle o) {
   switch (o) {

@@ -395,6 +395,20 @@ def test_protocol_caps_and_lane_plan():
     caps = comms[0].protocol_caps()
     assert caps == {"ll_direct": 2 << 20, "ll_chain": 8 << 20, "ll128": 0}
     assert comms_for(4, VARIANTS["ll128"][0])[0].protocol_caps()["ll128"] == 32 << 20
+    # the device path each variant runs (bcl_comm_path)
+    chain = cfg_of("chain_pipelined", 65536)
+    want = {"auto": "local_chain_kernel", "pull": "bcast_kernel/pull", "ll": "ll_kernel/chain",
+            "push": "bcast_kernel/push", "xpull": "bcast_kernel/pull/tma", "xstrict": "bcast_kernel/pull/tma",
+            "xpush": "bcast_kernel/push/tma", "ll128": "ll128_kernel"}
+    for variant, (options, proto) in VARIANTS.items():
+        c = comms_for(4, options)[0]
+        c.set_protocol(proto)
+        try:
+            assert c.path(1 << 20, chain) == want[variant], variant
+        finally:
+            c.set_protocol("auto")
+    assert comms[0].path(4096, cfg_of("direct")) == "ll_kernel/direct"
+    assert comms[0].path(4096, cfg_of("knomial", radix=2)) == "bcast_kernel/events"
     lanes = comms[0].info()["lanes"]
     for m, chunk in ((64 << 20, 512 << 10), (1 << 20, 65536), (12345, 1000)):
         p = comms[0].plan(cfg_of("chain_pipelined", chunk), 0, m)

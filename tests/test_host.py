@@ -221,3 +221,29 @@ def test_builtin_table_is_the_merge_of_the_measured_tables():
     text = B.builtin_table().text()
     assert text == open(os.path.join(tdir, "b200_default.csv")).read()
     assert "# bcl-ll128-upto: n=4" in text and "# bcl-push-from: n=4" in text
+
+
+def test_call_overhead_extends_the_reference_model():
+    """B200 per-call constant a0 (NetworkParams.call_overhead_s): every
+    algorithm's cost gains exactly a0; a0 = 0 is the reference model; a
+    uniform constant never changes the tuner's winners, only its predicted
+    costs."""
+    cands = [B.AlgorithmConfig.of("knomial", 2), B.AlgorithmConfig.of("scatter_ring_allgather"),
+             B.AlgorithmConfig.of("chain_pipelined"), B.AlgorithmConfig.of("direct"), B.AlgorithmConfig.of("chain")]
+    a0 = 17.2e-6
+    for c in cands:
+        cc = B.AlgorithmConfig(c.algorithm, c.radix_k, 65536 if c.algorithm == B.Algorithm.chain_pipelined else 0)
+        for n in (2, 4, 8):
+            for m in (0, 1, 1000, 1 << 20, 64 << 20):
+                base = B.cost_for(cc, n, m, 3e-6, 7.5e11)
+                assert B.cost_for(cc, n, m, 3e-6, 7.5e11, call_overhead_s=a0) == pytest.approx(base + a0, rel=1e-12)
+    sizes = [4 << i for i in range(29)]
+    chunks = [65536 << i for i in range(7)]
+    plain = B.tune([2, 4, 8], sizes, cands[:4], chunks, startup_s=3e-6, link_Bps=7.5e11)
+    withc = B.tune([2, 4, 8], sizes, cands[:4], chunks, startup_s=3e-6, link_Bps=7.5e11, call_overhead_s=a0)
+    assert [(e.n, e.msg_min_bytes, e.msg_max_bytes, e.config) for e in plain.entries] == \
+           [(e.n, e.msg_min_bytes, e.msg_max_bytes, e.config) for e in withc.entries]
+    for a, b in zip(plain.entries, withc.entries):
+        assert b.predicted_cost_s == pytest.approx(a.predicted_cost_s + a0, rel=1e-9)
+    with pytest.raises(ValueError):
+        B.cost_for(cands[0], 4, 100, call_overhead_s=-1.0)
