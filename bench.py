@@ -40,7 +40,7 @@ except OSError:
     pass
 HBM_PEAK = float(PEAKS.get("hbm_gbs", 6650.0))
 try:  # DRAM bytes per launch of the N=1 kernel from the committed ncu --set full capture
-    TRAFFIC_N1 = json.load(open(os.path.join(ROOT, "profiles", "round1", "ncu_traffic.json")))[
+    TRAFFIC_N1 = json.load(open(os.path.join(ROOT, "profiles", "round2", "n1", "ncu_traffic.json")))[
         "n1_config1_local_chain_kernel"]["dram_bytes_per_launch"]
 except (OSError, KeyError, ValueError):
     TRAFFIC_N1 = None

@@ -215,12 +215,17 @@ def test_builtin_table_is_the_merge_of_the_measured_tables():
     with tempfile.TemporaryDirectory() as d:
         out = os.path.join(d, "merged.csv")
         subprocess.run(["python", os.path.join(ROOT, "tools", "merge_tables.py"), out,
-                        os.path.join(tdir, "b200_measured_n2.csv"), os.path.join(tdir, "b200_measured_n4.csv")],
+                        os.path.join(tdir, "b200_measured_n2.csv"), os.path.join(tdir, "b200_measured_n4.csv"),
+                        os.path.join(tdir, "b200_predicted_n8.csv")],
                        check=True, capture_output=True)
         assert open(out).read() == open(os.path.join(tdir, "b200_default.csv")).read()
     text = B.builtin_table().text()
     assert text == open(os.path.join(tdir, "b200_default.csv")).read()
     assert "# bcl-ll128-upto: n=4" in text and "# bcl-push-from: n=4" in text
+    # n = 8 rows exist (so select no longer falls back to the n = 4 rows) and
+    # are labelled as predicted, not measured (tools/predict_n8.py)
+    assert {e.n for e in B.builtin_table().entries} == {2, 4, 8}
+    assert "PREDICTED n=8" in text.splitlines()[0]
 
 
 def test_call_overhead_extends_the_reference_model():
