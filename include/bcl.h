@@ -288,6 +288,29 @@ bcl_status_t bcl_comm_set_provenance(bcl_comm_t comm, unsigned long long* counte
 bcl_status_t bcl_comm_set_trace(bcl_comm_t comm, unsigned long long* records, uint32_t per_lane);
 bcl_status_t bcl_comm_launches(bcl_comm_t comm, uint64_t* launches);
 
+/* ------------------------------- device fabric (Transport / TransportFabric) */
+/* A GPU-backed stand-in for the reference's message fabric
+ * (proj/include/bcastlab/runtime.hpp:20-39): n ranks (threads of one
+ * process), rank r on devices[r]. Same contract as the reference transports:
+ * ordered and reliable per (src, dst) pair, eager send, blocking receive that
+ * rejects an out-of-order chunk id (BCL_ERR_RUNTIME). The payload moves
+ * through the GPUs: send stages it in the sender's GPU, receive pulls it into
+ * the receiver's GPU with the library's copy kernel (NVLink P2P) and returns
+ * it to the host. include/bcl_transport.hpp adapts it to the reference's
+ * Transport / TransportFabric classes so execute_rank and run_bcast run on it.
+ * Each endpoint (src for send, dst for receive) is used by one thread. */
+typedef struct bcl_fabric_s* bcl_fabric_t;
+bcl_status_t bcl_fabric_create(int n, const int* devices, bcl_fabric_t* out);
+bcl_status_t bcl_fabric_destroy(bcl_fabric_t f);
+bcl_status_t bcl_fabric_n_ranks(bcl_fabric_t f, int* n);
+bcl_status_t bcl_fabric_send(bcl_fabric_t f, int src, int dst, uint32_t chunk, const void* data, size_t len);
+/* Blocks for the next message src -> dst, checks its chunk id, returns its
+ * length; bcl_fabric_recv then copies it into out (exactly len bytes). */
+bcl_status_t bcl_fabric_recv_size(bcl_fabric_t f, int dst, int src, uint32_t chunk, size_t* len);
+bcl_status_t bcl_fabric_recv(bcl_fabric_t f, int dst, int src, uint32_t chunk, void* out, size_t len);
+/* Messages and payload bytes delivered src -> dst so far (schedule fidelity). */
+bcl_status_t bcl_fabric_stats(bcl_fabric_t f, int src, int dst, uint64_t* messages, uint64_t* bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -9,6 +9,7 @@
 
 #include "../../include/bcl.h"
 #include "bcl_comm.hpp"
+#include "bcl_fabric.hpp"
 #include "bcl_core.hpp"
 #include "bcl_tuner.hpp"
 
@@ -17,6 +18,9 @@ struct bcl_schedule_s {
 };
 struct bcl_table_s {
   bcl::TuningTable t;
+};
+struct bcl_fabric_s {
+  std::unique_ptr<bcl::DeviceFabric> f;
 };
 struct bcl_comm_s {
   std::shared_ptr<bcl::Group> g;
@@ -647,6 +651,61 @@ bcl_status_t bcl_comm_launches(bcl_comm_t comm, uint64_t* launches) {
     need(comm, "comm");
     need(launches, "launches");
     *launches = comm->g->launches(comm->local);
+  });
+}
+
+bcl_status_t bcl_fabric_create(int n, const int* devices, bcl_fabric_t* out) {
+  return guard([&] {
+    need(devices, "devices");
+    need(out, "out");
+    if (n < 1) throw std::invalid_argument("rank count must be >= 1");
+    auto f = std::make_unique<bcl_fabric_s>();
+    f->f = std::make_unique<bcl::DeviceFabric>(std::vector<int>(devices, devices + n));
+    *out = f.release();
+  });
+}
+
+bcl_status_t bcl_fabric_destroy(bcl_fabric_t f) {
+  delete f;
+  return BCL_OK;
+}
+
+bcl_status_t bcl_fabric_n_ranks(bcl_fabric_t f, int* n) {
+  return guard([&] {
+    need(f, "fabric");
+    need(n, "n");
+    *n = f->f->n_ranks();
+  });
+}
+
+bcl_status_t bcl_fabric_send(bcl_fabric_t f, int src, int dst, uint32_t chunk, const void* data, size_t len) {
+  return guard([&] {
+    need(f, "fabric");
+    if (len) need(data, "data");
+    f->f->send(src, dst, chunk, static_cast<const std::uint8_t*>(data), len);
+  });
+}
+
+bcl_status_t bcl_fabric_recv_size(bcl_fabric_t f, int dst, int src, uint32_t chunk, size_t* len) {
+  return guard([&] {
+    need(f, "fabric");
+    need(len, "len");
+    *len = f->f->recv_size(dst, src, chunk);
+  });
+}
+
+bcl_status_t bcl_fabric_recv(bcl_fabric_t f, int dst, int src, uint32_t chunk, void* out, size_t len) {
+  return guard([&] {
+    need(f, "fabric");
+    if (len) need(out, "out");
+    f->f->recv(dst, src, chunk, static_cast<std::uint8_t*>(out), len);
+  });
+}
+
+bcl_status_t bcl_fabric_stats(bcl_fabric_t f, int src, int dst, uint64_t* messages, uint64_t* bytes) {
+  return guard([&] {
+    need(f, "fabric");
+    f->f->stats(src, dst, messages, bytes);
   });
 }
 

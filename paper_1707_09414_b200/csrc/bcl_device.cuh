@@ -210,6 +210,7 @@ struct BarrierParams {
 int launch_bcast(const dev::LaunchParams& p, int cooperative, void* stream);
 int launch_barrier(const dev::BarrierParams& p, void* stream);
 int launch_ll(const dev::LLParams& p, void* stream);
+int launch_peer_copy(std::uint8_t* dst, const std::uint8_t* src, std::uint64_t len, void* stream);
 int launch_local_chain(const dev::LocalChainParams& p, int ctas, void* stream);
 int local_chain_occupancy(int* blocks_per_sm);
 int ll128_occupancy(int* blocks_per_sm);

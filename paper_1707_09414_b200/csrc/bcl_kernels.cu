@@ -1242,8 +1242,37 @@ __global__ void barrier_kernel(const __grid_constant__ BarrierParams B) {
   __syncthreads();
 }
 
+// Plain copy of one message slab (the DeviceFabric transport, bcl_fabric.cpp):
+// 16-byte loads from the source GPU's slab (NVLink across GPUs), 4 in flight
+// per thread; both slabs are 256-byte aligned allocations.
+__global__ void __launch_bounds__(512) peer_copy_kernel(std::uint8_t* __restrict__ dst,
+                                                          const std::uint8_t* __restrict__ src, std::uint64_t len) {
+  const std::uint64_t nvec = len / 16;
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+  const uint4* vs = reinterpret_cast<const uint4*>(src);
+  uint4* vd = reinterpret_cast<uint4*>(dst);
+  std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < nvec; i += 4 * stride) {
+    uint4 r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) r[u] = ld_v4(vs + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) st_v4(vd + i + u * stride, r[u]);
+  }
+  for (; i < nvec; i += stride) st_v4(vd + i, ld_v4(vs + i));
+  const std::uint64_t t = nvec * 16 + static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < len) dst[t] = ld_u8(src + t);
+}
+
 }  // namespace
 }  // namespace dev
+
+int launch_peer_copy(std::uint8_t* dst, const std::uint8_t* src, std::uint64_t len, void* stream) {
+  const std::uint64_t nvec = (len + 15) / 16;
+  const unsigned blocks = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(296, (nvec + 511) / 512)));
+  dev::peer_copy_kernel<<<blocks, 512, 0, static_cast<cudaStream_t>(stream)>>>(dst, src, len);
+  return static_cast<int>(cudaGetLastError());
+}
 
 std::size_t bcast_smem_bytes(std::uint32_t stages, std::uint32_t stage_bytes) {
   return static_cast<std::size_t>(dev::kWarpsPerCta) * stages * stage_bytes;
