@@ -95,6 +95,7 @@ void set_option(GroupOptions& o, const std::string& key, const std::string& v) {
   else if (key == "local_item") o.local_item = u64();
   else if (key == "ll") o.ll = i32() != 0;
   else if (key == "ll128") o.ll128 = i32();
+  else if (key == "ll128_coop") o.ll128_coop = i32() != 0;
   else if (key == "protocol") {
     o.protocol = i32();
     if (o.protocol < 0 || o.protocol > 4) throw std::invalid_argument("protocol must be 0..4");
@@ -110,7 +111,7 @@ void set_option(GroupOptions& o, const std::string& key, const std::string& v) {
 
 constexpr const char* kOptionNames[] = {
     "poll_ns", "window_bytes", "min_slice", "max_ctas", "strict_sys", "sys_scope", "eager_post", "writer_fence",
-    "local_fused", "local_ctas", "local_item", "ll", "ll128", "protocol", "ll_max", "ll_chain_max", "ll128_max",
+    "local_fused", "local_ctas", "local_item", "ll", "ll128", "ll128_coop", "protocol", "ll_max", "ll_chain_max", "ll128_max",
     "host_piece", "stages", "stage_bytes"};
 
 }  // namespace
@@ -825,6 +826,7 @@ void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& 
     P.ctas = std::clamp<int>(static_cast<int>((P.lines + per_cta - 1) / per_cta), 1, cap);
   }
   P.timeout_ns = opt_.timeout_ns;
+  P.coop = opt_.ll128_coop ? 1 : 0;
   const std::size_t S = region_stride();
   std::uint64_t epoch = 0;
   for (std::size_t i = 0; i < locals.size(); ++i) {

@@ -83,6 +83,7 @@ struct GroupOptions {
   int writer_fence = 2;                                     // copy warps fence their own data before the hand-off:
                                                             // 0 no (the publisher fences), 1 gpu scope, 2 the call's
                                                             // scope (system across GPUs)
+  bool ll128_coop = true;                                   // LL128 with one rank per GPU: cooperative launch
   int ll128 = -1;                                           // LL128 chain lines: -1 auto (every rank on its own
                                                             // GPU), 0 off, 1 also for ranks sharing a GPU
   bool local_fused = true;                                  // single-GPU groups: fused flag-free chain kernel

@@ -171,6 +171,7 @@ struct LLParamsT {
   std::uint32_t chain128_lines;  // 128-byte lines of the LL128 ring (kLL128RingLines)
   std::uint32_t chain128_area;   // its offset from the LL base in 16-byte units (128-byte aligned)
   std::uint64_t timeout_ns;
+  std::uint32_t coop;            // LL128, one rank per GPU: cooperative launch (co-residency guaranteed)
   LLRank ranks[NL];
 };
 using LLParams = LLParamsT<kMaxLocal>;

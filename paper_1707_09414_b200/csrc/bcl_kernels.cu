@@ -1363,7 +1363,7 @@ int launch_ll(const dev::LLParams& p, void* stream) {
   attr[0].id = cudaLaunchAttributeCooperative;
   // LL128 writers wait on ring credits from the successor's CTAs: co-residency
   // is required even for one rank per GPU (the successor's warp w may be any CTA).
-  attr[0].val.cooperative = (p.n_local > 1 || p.chain == 2) ? 1 : 0;
+  attr[0].val.cooperative = (p.n_local > 1 || (p.chain == 2 && p.coop)) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (p.n_local == 1) {
