@@ -189,7 +189,7 @@ bcl_status_t bcl_comm_init_rank(int n, int rank, int device, size_t heap_bytes,
  *   sys_scope      1: system-scope flag polls and fences even when every rank
  *                  shares one GPU (the cross-GPU code path on one device)
  *   strict_sys     1: system-scope fence in the publisher before every flag
- *   writer_fence   0 publisher fences, 1 gpu scope, 2 the call's scope (default)
+ *   writer_fence   0 publisher fences, 1 gpu scope (default), 2 the call's scope
  *   ll128          -1 auto (ranks on distinct GPUs), 0 off, 1 also between
  *                  ranks sharing a GPU;  ll128_max, ll_chain_max, ll_max caps
  *   window_bytes, min_slice, max_ctas, stages, poll_ns, host_piece, ll,

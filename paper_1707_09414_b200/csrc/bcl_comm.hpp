@@ -80,9 +80,10 @@ struct GroupOptions {
   int sys_scope = -1;                                       // flag polls/fences at system scope: -1 auto (ranks
                                                             // span GPUs), 1 always (runs the cross-GPU code on one GPU)
   bool eager_post = true;                                   // bulk chain: forward a chunk once its store is done
-  int writer_fence = 2;                                     // copy warps fence their own data before the hand-off:
+  int writer_fence = 1;                                     // copy warps fence their own data before the hand-off:
                                                             // 0 no (the publisher fences), 1 gpu scope, 2 the call's
-                                                            // scope (system across GPUs)
+                                                            // scope (system across GPUs; 2.6x slower at n = 4, the
+                                                            // fence waits for the warp's in-flight TMA pulls)
   bool ll128_coop = true;                                   // LL128 with one rank per GPU: cooperative launch
   int ll128 = -1;                                           // LL128 chain lines: -1 auto (every rank on its own
                                                             // GPU), 0 off, 1 also for ranks sharing a GPU

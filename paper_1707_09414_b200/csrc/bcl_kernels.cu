@@ -241,10 +241,14 @@ __device__ bool wait_geq(const Ctx& c, const std::uint64_t* p, std::uint64_t tar
 // batch's remote flag stores, whose acknowledgements queue behind loaded
 // NVLink traffic (measured ~16 us per batch at n = 4, 64 MiB); the copy warp
 // has only its own, already completed, data writes outstanding.
-// writer_fence = 2 (the default across GPUs) fences at system scope: the
-// copy warp has no remote stores outstanding at that point (its data went to
-// its own HBM and its remote flags are stored by the publisher), so the fence
-// only waits for its local, completed writes.
+// writer_fence = 1 (default): gpu scope. The flag names data in this GPU's
+// own HBM, which NVLink readers reach through this GPU's L2 (its point of
+// coherence), so data performed at gpu scope is what a peer reads once it
+// sees the flag -- a hardware property, not a PTX-model guarantee (DESIGN.md
+// §5 "Memory ordering"; stress-tested across GPUs). writer_fence = 2 fences
+// at system scope, the textbook release: in a middle rank of the chain that
+// fence also waits for the warp's in-flight TMA pulls from its upstream
+// (64 MiB at n = 4: 376 us against 126-145 us), so it is an option.
 __device__ __forceinline__ void writer_fence(const LaunchParamsT<1>& P) {
   if (P.writer_fence == 2) {
     fence_acq_rel_sys();

@@ -120,6 +120,40 @@ def test_ll128_chain_back_to_back_stress():
 
 
 @needs2
+def test_pull_flag_ordering_litmus():
+    """The default pull path publishes a slice after a gpu-scope fence of the
+    producing warp (DESIGN.md §5 "Memory ordering": the producer's L2 is the
+    point of coherence for NVLink readers, a hardware property rather than a
+    PTX-model guarantee). Litmus-style stress: 300 back-to-back broadcasts
+    with small chunks and slices (thousands of flag hand-offs per call), a
+    fresh payload and a rotating root every call, every byte of every rank
+    checked before the next call reuses the buffers."""
+    devices = list(range(min(ngpu(), 8)))
+    n = len(devices)
+    comms = B.Comm.local(devices, timeout_s=10, min_slice=512, window_bytes=1 << 20)
+    for c in comms:
+        c.set_protocol("pull")
+    rng = random.Random(31)
+    cap = 4 << 20
+    bufs = [torch.empty(cap, dtype=torch.uint8, device=f"cuda:{d}") for d in devices]
+    try:
+        for it in range(300):
+            m = rng.choice([rng.randrange(1, 65536), rng.randrange(65536, cap), cap])
+            chunk = rng.choice([4096, 8192, 16384, 65536])
+            root = it % n
+            src = torch.randint(0, 256, (m,), dtype=torch.uint8, device=f"cuda:{devices[root]}")
+            for r in range(n):
+                (bufs[r][:m].copy_(src) if r == root else bufs[r][:m].fill_((it * 7) & 0xFF))
+            torch.cuda.synchronize(devices[root])
+            B.run_bcast(comms, root, [b[:m] for b in bufs], m, cfg_of("chain_pipelined", chunk))
+            for r in range(n):
+                assert torch.equal(bufs[r][:m].cpu(), src.cpu()), (it, m, chunk, root, r)
+    finally:
+        for c in comms:
+            c.set_protocol("auto")
+
+
+@needs2
 def test_two_ranks_per_gpu():
     devices = [d for d in range(min(ngpu(), 4)) for _ in range(2)]
     comms = B.Comm.local(devices, timeout_s=10)
