@@ -192,6 +192,9 @@ bcl_status_t bcl_comm_init_rank(int n, int rank, int device, size_t heap_bytes,
  *   writer_fence   0 publisher fences, 1 gpu scope (default), 2 the call's scope
  *   ll128          -1 auto (ranks on distinct GPUs), 0 off, 1 also between
  *                  ranks sharing a GPU;  ll128_max, ll_chain_max, ll_max caps
+ *   nvls           NVLS multicast team: -1 auto (ranks on two or more GPUs with
+ *                  multicast support), 0 off, 1 required (init fails without);
+ *                  nvls_strict 1: system-scope fence before every counter bump
  *   window_bytes, min_slice, max_ctas, stages, poll_ns, host_piece, ll,
  *   eager_post, local_fused, local_ctas, local_item  (tuning knobs)
  * Unknown keys fail with BCL_ERR_INVALID_ARGUMENT. New on B200. */
@@ -229,7 +232,7 @@ bcl_status_t bcl_comm_plan(bcl_comm_t c, const bcl_config_t* config, int root, u
 /* The device path a call of this shape would run (config NULL = tuned), as
  * text: "ll_kernel/direct", "ll_kernel/chain", "ll128_kernel",
  * "local_chain_kernel", "bcast_kernel/pull[/tma]", "bcast_kernel/push[/tma]",
- * "bcast_kernel/events" or "none"; *len = bytes needed incl. NUL. */
+ * "bcast_kernel/events", "nvls_kernel" or "none"; *len = bytes needed incl. NUL. */
 bcl_status_t bcl_comm_path(bcl_comm_t c, const bcl_config_t* config, int root, uint64_t bytes, char* out,
                            size_t cap, size_t* len);
 /* Pipelined-chain transport protocol: 0 auto (line protocols where the
@@ -240,10 +243,17 @@ bcl_status_t bcl_comm_path(bcl_comm_t c, const bcl_config_t* config, int root, u
  * 8 MiB) -- and above them the table's measured "# bcl-push-from" rule),
  * 1 pull (consumers load from the upstream buffer), 2 push (producers store
  * into the downstream buffer), 3 LL (flagged 16-byte lines forwarded hop by
- * hop), 4 LL128 (128-byte lines, 120 payload bytes each). 3 fails above
- * ll_chain_max, 4 above ll128_max or when ranks share a GPU without the
- * ll128=1 option. */
+ * hop), 4 LL128 (128-byte lines, 120 payload bytes each), 5 NVLS (the root
+ * writes each piece once through a multicast address, the NVSwitch
+ * replicates it to every GPU, receivers copy it out; any schedule -- in auto
+ * mode NVLS carries the `direct` schedule above the LL threshold). 3 fails
+ * above ll_chain_max, 4 above ll128_max or when ranks share a GPU without the
+ * ll128=1 option, 5 when the communicator has no multicast team. */
 bcl_status_t bcl_comm_set_protocol(bcl_comm_t c, int protocol);
+/* NVLS multicast team of this communicator: *available 1/0 and, when 0, why
+ * (text, *len = bytes needed incl. NUL). Every rank agrees at init/connect.
+ * New on B200; no reference counterpart. */
+bcl_status_t bcl_comm_nvls(bcl_comm_t c, int* available, char* reason, size_t cap, size_t* len);
 /* The config a NULL-config call would run for this size (select + clamp). */
 bcl_status_t bcl_comm_choose(bcl_comm_t c, uint64_t message_bytes, bcl_config_t* out);
 bcl_status_t bcl_mem_alloc(bcl_comm_t c, size_t bytes, void** ptr);

@@ -164,9 +164,20 @@ class Comm:
                                    C.byref(nc), C.byref(ctas)))
         return {"slices": q.value, "slice_bytes": sb.value, "n_chunks": nc.value, "ctas": ctas.value}
 
+    def nvls(self):
+        """(available, reason): the communicator's NVLS multicast team (every rank agrees)."""
+        ok, ln = C.c_int(), C.c_size_t()
+        _check(lib().bcl_comm_nvls(self._h, C.byref(ok), None, 0, C.byref(ln)))
+        buf = C.create_string_buffer(ln.value)
+        _check(lib().bcl_comm_nvls(self._h, C.byref(ok), buf, ln.value, C.byref(ln)))
+        return bool(ok.value), buf.value.decode()
+
+    PROTOCOLS = {"auto": 0, "pull": 1, "push": 2, "ll": 3, "ll128": 4, "nvls": 5}
+
     def set_protocol(self, protocol) -> None:
-        """Chain transport: "auto" (LL128/LL up to their caps, then the table rule), "pull", "push", "ll" or "ll128"."""
-        code = {"auto": 0, "pull": 1, "push": 2, "ll": 3, "ll128": 4}[protocol] if isinstance(protocol, str) else int(protocol)
+        """Transport: "auto" (LL128/LL up to their caps, then the table rule), "pull", "push", "ll", "ll128"
+        or "nvls" (NVLS multicast, any schedule)."""
+        code = self.PROTOCOLS[protocol] if isinstance(protocol, str) else int(protocol)
         _check(lib().bcl_comm_set_protocol(self._h, code))
 
     def path(self, nbytes: int, config: Optional[AlgorithmConfig] = None, root: int = 0) -> str:

@@ -516,6 +516,14 @@ bcl_status_t bcl_comm_path(bcl_comm_t c, const bcl_config_t* config, int root, u
   });
 }
 
+bcl_status_t bcl_comm_nvls(bcl_comm_t c, int* available, char* reason, size_t cap, size_t* len) {
+  return guard([&] {
+    need(c, "comm");
+    if (available) *available = c->g->nvls_available() ? 1 : 0;
+    copy_text(c->g->nvls_reason(), reason, cap, len);
+  });
+}
+
 bcl_status_t bcl_comm_set_protocol(bcl_comm_t c, int protocol) {
   return guard([&] {
     need(c, "comm");

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cctype>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <sstream>
@@ -30,6 +31,9 @@ struct ExportInfo {
   cudaUUID_t uuid;             // physical GPU identity (ordinals differ between processes)
   cudaIpcMemHandle_t region;
   cudaIpcMemHandle_t heap;
+  std::int32_t nvls_cap;       // this rank can join a multicast team (option on, device support)
+  std::int32_t nvls_owner;     // rank 0: the blob below carries the multicast object
+  std::uint8_t nvls[NvlsTeam::kBlobBytes];
 };
 
 void ck(cudaError_t e, const char* what) {
@@ -98,13 +102,15 @@ void set_option(GroupOptions& o, const std::string& key, const std::string& v) {
   else if (key == "ll128_coop") o.ll128_coop = i32() != 0;
   else if (key == "protocol") {
     o.protocol = i32();
-    if (o.protocol < 0 || o.protocol > 4) throw std::invalid_argument("protocol must be 0..4");
+    if (o.protocol < 0 || o.protocol > 5) throw std::invalid_argument("protocol must be 0..5");
   } else if (key == "ll_max") o.ll_max_bytes = u64();
   else if (key == "ll_chain_max") o.ll_chain_max_bytes = i64();
   else if (key == "ll128_max") o.ll128_max_bytes = i64();
   else if (key == "host_piece") o.host_piece = std::max<std::uint64_t>(4096, u64());
   else if (key == "stages") o.stages = static_cast<std::uint32_t>(std::clamp(i32(), 2, dev::kMaxStages));
   else if (key == "stage_bytes") o.stage_bytes = i64() < 0 ? -1 : i64() / 16 * 16;
+  else if (key == "nvls") o.nvls = i32();
+  else if (key == "nvls_strict") o.nvls_strict = i32() != 0;
   else if (key == "timeout_s") o.timeout_ns = static_cast<std::uint64_t>(std::strtod(s, nullptr) * 1e9);
   else throw std::invalid_argument("unknown communicator option '" + key + "'");
 }
@@ -112,7 +118,7 @@ void set_option(GroupOptions& o, const std::string& key, const std::string& v) {
 constexpr const char* kOptionNames[] = {
     "poll_ns", "window_bytes", "min_slice", "max_ctas", "strict_sys", "sys_scope", "eager_post", "writer_fence",
     "local_fused", "local_ctas", "local_item", "ll", "ll128", "ll128_coop", "protocol", "ll_max", "ll_chain_max", "ll128_max",
-    "host_piece", "stages", "stage_bytes"};
+    "host_piece", "stages", "stage_bytes", "nvls", "nvls_strict"};
 
 }  // namespace
 
@@ -160,7 +166,8 @@ AggregateRankError::AggregateRankError(std::vector<RankFailure> failures)
 
 void Group::alloc_rank(LocalRank& r, std::size_t heap_bytes) {
   DeviceScope ds(r.device);
-  r.region_bytes = (ll_offset(lanes_alloc_) + ll_words()) * sizeof(std::uint64_t);
+  // (+ 8 words: the last one is the connect-time agreement word, kCtlWord)
+  r.region_bytes = (ll_offset(lanes_alloc_) + ll_words() + 8) * sizeof(std::uint64_t);
   ck(cudaMalloc(&r.region, r.region_bytes), "cudaMalloc(region)");
   ck(cudaMemset(r.region, 0, r.region_bytes), "cudaMemset(region)");
   ck(cudaMalloc(&r.d_peers, sizeof(dev::PeerTable)), "cudaMalloc(peers)");
@@ -186,6 +193,7 @@ void Group::cache_device_limits(int device) {
   ck(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device), "sm count");
   ck(static_cast<cudaError_t>(local_chain_occupancy(&local_chain_occ_)), "occupancy(local chain)");
   ck(static_cast<cudaError_t>(ll128_occupancy(&ll128_occ_)), "occupancy(ll128)");
+  ck(static_cast<cudaError_t>(nvls_occupancy(&nvls_occ_)), "occupancy(nvls)");
 }
 
 void Group::upload_peers(LocalRank& r) {
@@ -316,6 +324,29 @@ std::shared_ptr<Group> Group::create_local(const std::vector<int>& devices, cons
     }
     g->upload_peers(lr);
   }
+  // NVLS multicast across the group's GPUs (one team; ranks sharing a GPU
+  // read that GPU's copy).
+  if (opt.nvls == 0) {
+    g->nvls_why_ = "disabled (nvls=0)";
+  } else if (g->by_device_.size() < 2) {
+    g->nvls_why_ = "every rank on one GPU (a multicast team needs two or more GPUs)";
+  } else {
+    std::vector<int> devs;
+    for (const auto& kv : g->by_device_) devs.push_back(kv.first);
+    for (int d : devs) {
+      if (!NvlsTeam::supported(d, &g->nvls_why_)) devs.clear();
+      if (devs.empty()) break;
+    }
+    if (!devs.empty()) {
+      try {
+        g->nvls_ = NvlsTeam::create_local(devs);
+        g->nvls_why_.clear();
+      } catch (const std::exception& e) {
+        g->nvls_why_ = e.what();
+      }
+    }
+  }
+  if (opt.nvls == 1 && !g->nvls_) throw std::runtime_error("NVLS multicast required but unavailable: " + g->nvls_why_);
   g->connected_ = true;
   return g;
 }
@@ -342,6 +373,19 @@ std::shared_ptr<Group> Group::create_rank(int n, int rank, int device, std::size
   g->local_[0].device = device;
   g->by_device_[device].push_back(0);
   g->alloc_rank(g->local_[0], heap_bytes);
+  // NVLS: rank 0 creates and exports the multicast object; the others import
+  // it in connect().
+  if (opt.nvls == 0) {
+    g->nvls_why_ = "disabled (nvls=0)";
+  } else if (n < 2) {
+    g->nvls_why_ = "one rank";
+  } else if (NvlsTeam::supported(device, &g->nvls_why_) && rank == 0) {
+    try {
+      g->nvls_ = NvlsTeam::create_owner(n, device);
+    } catch (const std::exception& e) {
+      g->nvls_why_ = e.what();
+    }
+  }
   return g;
 }
 
@@ -368,6 +412,10 @@ std::vector<std::uint8_t> Group::export_info() const {
   }
   ck(cudaIpcGetMemHandle(&info.region, r.region), "cudaIpcGetMemHandle(region)");
   if (r.heap) ck(cudaIpcGetMemHandle(&info.heap, r.heap), "cudaIpcGetMemHandle(heap)");
+  info.nvls_cap = opt_.nvls != 0 && n_ >= 2 && (r.rank != 0 || nvls_ != nullptr) &&
+                  NvlsTeam::supported(r.device, nullptr);
+  info.nvls_owner = r.rank == 0 && nvls_ != nullptr;
+  if (info.nvls_owner) nvls_->export_blob(info.nvls);
   std::vector<std::uint8_t> out(sizeof info);
   std::memcpy(out.data(), &info, sizeof info);
   return out;
@@ -502,6 +550,8 @@ void Group::connect(const std::vector<std::vector<std::uint8_t>>& infos) {
   LocalRank& me = local_[0];
   DeviceScope ds(me.device);
   const std::size_t S = region_stride();
+  std::vector<std::uint64_t*> regions;
+  std::vector<std::uint64_t> region_bytes;
   for (int p = 0; p < n_; ++p) {
     std::uint64_t* base = nullptr;
     std::uint64_t heap_base = 0;
@@ -532,9 +582,106 @@ void Group::connect(const std::vector<std::vector<std::uint8_t>>& infos) {
     me.h_peers.credit[p] = base + 4 * S + n_ + 1;
     me.h_peers.wcredit[p] = base + 4 * S + 3 * static_cast<std::size_t>(n_) + 2;
     me.h_peers.ll[p] = reinterpret_cast<uint4*>(base + ll_offset(lanes_));
+    regions.push_back(base);
+    region_bytes.push_back(all[static_cast<std::size_t>(p)].region_bytes);
   }
   upload_peers(me);
+  setup_nvls_ipc(infos, regions, region_bytes);
   connected_ = true;
+}
+
+namespace {
+
+// Connect-time agreement between per-process ranks: each rank publishes
+// (phase << 1 | failed) in the last word of its region and waits until every
+// rank reached the phase; returns whether every rank succeeded.
+bool agree(int n, int me, int phase, bool ok, const std::vector<std::uint64_t*>& regions,
+           const std::vector<std::uint64_t>& region_bytes, double timeout_s) {
+  auto word = [&](int p) { return regions[static_cast<std::size_t>(p)] + region_bytes[static_cast<std::size_t>(p)] / 8 - 1; };
+  const std::uint64_t mine = (static_cast<std::uint64_t>(phase) << 1) | (ok ? 0u : 1u);
+  ck(cudaMemcpy(word(me), &mine, sizeof mine, cudaMemcpyHostToDevice), "cudaMemcpy(agree)");
+  const auto t0 = std::chrono::steady_clock::now();
+  bool all_ok = ok;
+  for (int p = 0; p < n; ++p) {
+    for (;;) {
+      std::uint64_t v = 0;
+      ck(cudaMemcpy(&v, word(p), sizeof v, cudaMemcpyDeviceToHost), "cudaMemcpy(agree)");
+      if ((v >> 1) >= static_cast<std::uint64_t>(phase)) {
+        if ((v >> 1) == static_cast<std::uint64_t>(phase) && (v & 1u)) all_ok = false;
+        break;
+      }
+      if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s) {
+        throw std::runtime_error("connect: rank " + std::to_string(p) + " did not reach NVLS setup phase " +
+                                 std::to_string(phase));
+      }
+      ::usleep(200);
+    }
+  }
+  return all_ok;
+}
+
+}  // namespace
+
+// Per-process NVLS: every rank imports rank 0's multicast object and adds its
+// GPU (phase 1), then binds and maps its copy of the ring (phase 2); the
+// ranks agree after each phase, so NVLS is on for all of them or for none.
+void Group::setup_nvls_ipc(const std::vector<std::vector<std::uint8_t>>& infos,
+                           const std::vector<std::uint64_t*>& regions, const std::vector<std::uint64_t>& region_bytes) {
+  LocalRank& me = local_[0];
+  std::vector<ExportInfo> all(infos.size());
+  for (std::size_t i = 0; i < infos.size(); ++i) std::memcpy(&all[i], infos[i].data(), sizeof(ExportInfo));
+  bool eligible = n_ >= 2 && all[0].nvls_owner != 0;
+  for (std::size_t i = 0; i < all.size() && eligible; ++i) {
+    if (!all[i].nvls_cap) {
+      eligible = false;
+      nvls_why_ = "rank " + std::to_string(i) + " cannot join a multicast team";
+    }
+    for (std::size_t j = 0; j < i && eligible; ++j) {
+      if (std::memcmp(&all[i].uuid, &all[j].uuid, sizeof(cudaUUID_t)) == 0) {
+        eligible = false;
+        nvls_why_ = "ranks share a GPU (one process per GPU required for NVLS)";
+      }
+    }
+  }
+  if (n_ >= 2 && all[0].nvls_owner == 0 && nvls_why_ == "not set up") nvls_why_ = "rank 0 created no multicast object";
+  if (!eligible) {  // the same verdict on every rank (computed from the same blobs)
+    nvls_.reset();
+    if (opt_.nvls == 1) throw std::runtime_error("NVLS multicast required but unavailable: " + nvls_why_);
+    return;
+  }
+  bool ok = true;
+  const bool dbg = std::getenv("BCL_DEBUG_NVLS") != nullptr;
+  if (dbg) std::fprintf(stderr, "[bcl rank %d] nvls: import/add\n", me.rank);
+  try {
+    if (me.rank != 0) nvls_ = NvlsTeam::import(all[0].nvls, me.device);
+    if (dbg) std::fprintf(stderr, "[bcl rank %d] nvls: imported\n", me.rank);
+    nvls_->add_device();
+  } catch (const std::exception& e) {
+    ok = false;
+    nvls_why_ = e.what();
+  }
+  DeviceScope ds(me.device);
+  const double limit = 60.0;
+  if (dbg) std::fprintf(stderr, "[bcl rank %d] nvls: phase 1 ok=%d\n", me.rank, ok ? 1 : 0);
+  if (agree(n_, me.rank, 1, ok, regions, region_bytes, limit)) {
+    if (dbg) std::fprintf(stderr, "[bcl rank %d] nvls: agreed 1\n", me.rank);
+    try {
+      nvls_->bind_and_map();
+    } catch (const std::exception& e) {
+      ok = false;
+      nvls_why_ = e.what();
+    }
+    if (dbg) std::fprintf(stderr, "[bcl rank %d] nvls: bound ok=%d %s\n", me.rank, ok ? 1 : 0, nvls_why_.c_str());
+    if (agree(n_, me.rank, 2, ok, regions, region_bytes, limit)) {
+      nvls_why_.clear();
+      return;
+    }
+    if (ok) nvls_why_ = "another rank failed to bind its multicast memory";
+  } else if (ok) {
+    nvls_why_ = "another rank failed to join the multicast team";
+  }
+  nvls_.reset();
+  if (opt_.nvls == 1) throw std::runtime_error("NVLS multicast required but unavailable: " + nvls_why_);
 }
 
 Group::~Group() {
@@ -572,8 +719,8 @@ void Group::set_table(const TuningTable& t) {
 void Group::clear_table() { have_table_ = false; }
 
 void Group::set_protocol(int protocol) {
-  if (protocol < 0 || protocol > 4) {
-    throw std::invalid_argument("protocol must be 0 (auto), 1 (pull), 2 (push), 3 (ll) or 4 (ll128)");
+  if (protocol < 0 || protocol > 5) {
+    throw std::invalid_argument("protocol must be 0 (auto), 1 (pull), 2 (push), 3 (ll), 4 (ll128) or 5 (nvls)");
   }
   opt_.protocol = protocol;
 }
@@ -586,6 +733,53 @@ bool Group::use_push(const CallPlan& p, std::uint64_t bytes) const {
   if (opt_.protocol == 2) return true;
   return select_push(table(), n_, bytes);
 }
+// NVLS multicast: every schedule under protocol 5 (the broadcast's result
+// does not depend on the schedule); in auto mode the `direct` schedule above
+// the LL threshold (root -> every rank is what the switch's replication does;
+// the lane executor would send M once per receiver from the root).
+bool Group::use_nvls(const CallPlan& p, std::uint64_t bytes) const {
+  if (n_ < 2) return false;
+  if (opt_.protocol == 5) {
+    if (!nvls_) throw std::invalid_argument("NVLS multicast unavailable on this communicator: " + nvls_why_);
+    return true;
+  }
+  if (opt_.protocol != 0 || !nvls_ || bytes == 0) return false;
+  return p.config.algorithm == Algorithm::Direct && !(bytes <= ll_max_ && opt_.ll);
+}
+
+void Group::launch_nvls_group(const std::vector<int>& locals, const std::vector<void*>& bufs, std::uint64_t bytes,
+                              int root, cudaStream_t stream) {
+  if (bytes == 0) return;  // nothing moves (every rank skips alike)
+  const NvlsGeometry geo = nvls_geometry(bytes);
+  dev::NvlsParams P{};
+  P.n_local = static_cast<int>(locals.size());
+  const int cap = std::max(1, sms_ * std::max(nvls_occ_, 1) / P.n_local);
+  P.ctas = std::min<int>({static_cast<int>(geo.pieces), dev::kNvlsTargetCtas, cap});
+  P.n_recv = n_ - 1;
+  P.pieces = geo.pieces;
+  P.bytes = bytes;
+  P.piece_bytes = geo.piece_bytes;
+  const int device = local_[static_cast<std::size_t>(locals[0])].device;
+  P.seq_base = nvls_->take(device, geo.pieces);
+  P.timeout_ns = opt_.timeout_ns;
+  P.strict = opt_.nvls_strict ? 1 : 0;
+  P.mc = nvls_->mc(device);
+  P.uc = nvls_->uc(device);
+  const std::size_t S = region_stride();
+  for (std::size_t i = 0; i < locals.size(); ++i) {
+    LocalRank& r = local_[static_cast<std::size_t>(locals[i])];
+    dev::NvlsRank& w = P.ranks[i];
+    w.rank = r.rank;
+    w.is_root = r.rank == root ? 1 : 0;
+    w.buf = static_cast<std::uint8_t*>(bufs[i]);
+    w.err = r.err_dev;
+    w.abort = reinterpret_cast<int*>(r.region + 4 * S + static_cast<std::size_t>(n_));
+    ++r.launches;
+  }
+  DeviceScope ds(device);
+  ck(static_cast<cudaError_t>(launch_nvls(P, stream)), "launch(nvls)");
+}
+
 // Every rank on this GPU, pipelined chain, auto protocol: the fused
 // flag-free kernel (pull forces the lane executor; timelines need it too).
 // (The timeline hook needs the lane executor: single-process groups only, so
@@ -876,6 +1070,7 @@ std::string Group::path(const AlgorithmConfig* cfg, int root, std::uint64_t byte
   if (n_ == 1) return "none";
   std::vector<int> locals;
   for (int i = 0; i < local_count(); ++i) locals.push_back(i);
+  if (use_nvls(p, bytes)) return "nvls_kernel";
   if (p.config.algorithm == Algorithm::Direct && bytes <= ll_max_ && opt_.ll) return "ll_kernel/direct";
   if (const int mode = ll_chain_mode(p, bytes, locals)) return mode == 2 ? "ll128_kernel" : "ll_kernel/chain";
   if (use_local_chain(p, locals)) return "local_chain_kernel";
@@ -887,6 +1082,10 @@ std::string Group::path(const AlgorithmConfig* cfg, int root, std::uint64_t byte
 
 void Group::launch_group(const std::vector<int>& locals, const std::vector<void*>& bufs,
                          std::uint64_t bytes, int root, const CallPlan& p, cudaStream_t stream) {
+  if (use_nvls(p, bytes)) {
+    launch_nvls_group(locals, bufs, bytes, root, stream);
+    return;
+  }
   if (p.config.algorithm == Algorithm::Direct && bytes <= ll_max_ && opt_.ll) {
     launch_ll(locals, bufs, bytes, root, stream, 0);
     return;

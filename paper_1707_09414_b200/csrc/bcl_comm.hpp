@@ -31,6 +31,7 @@
 
 #include "bcl_core.hpp"
 #include "bcl_device.cuh"
+#include "bcl_nvls.hpp"
 #include "bcl_tuner.hpp"
 
 namespace bcl {
@@ -100,6 +101,9 @@ struct GroupOptions {
   std::int64_t stage_bytes = -1;                            // bulk-copy stage per warp: 0 = vector loads,
                                                             // -1 = auto (8 KiB across GPUs, 0 on one GPU)
   std::uint32_t stages = 2;                                 // bulk-copy stages per copy warp
+  int nvls = -1;                                            // NVLS multicast: -1 auto (ranks on >= 2 GPUs with
+                                                            // multicast support), 0 off, 1 required
+  bool nvls_strict = false;                                 // system-scope fence before every NVLS counter bump
   static GroupOptions from_env();                           // BCL_* overrides (tuning runs)
   // "key=value,key=value" with the BCL_* names in lower case (e.g.
   // "stage_bytes=8192,sys_scope=1,protocol=2"); applied over *this.
@@ -193,7 +197,11 @@ class Group {
   int local_index_of(int rank) const;
 
   void set_table(const TuningTable& t);
-  void set_protocol(int protocol);  // 0 auto (LL128/LL chain, then the table's push-from rule), 1 pull, 2 push, 3 LL, 4 LL128
+  void set_protocol(int protocol);  // 0 auto (LL128/LL chain, then the table's push-from rule), 1 pull, 2 push, 3 LL,
+                                    // 4 LL128, 5 NVLS multicast (any schedule)
+  // NVLS multicast availability (agreed by every rank) and, if unavailable, why.
+  bool nvls_available() const { return nvls_ != nullptr; }
+  const std::string& nvls_reason() const { return nvls_why_; }
   void clear_table();
   const TuningTable& table() const;
   AlgorithmConfig choose(std::uint64_t bytes, const AlgorithmConfig* cfg) const;
@@ -232,6 +240,11 @@ class Group {
   void launch_group(const std::vector<int>& locals, const std::vector<void*>& bufs,
                     std::uint64_t bytes, int root, const CallPlan& p, cudaStream_t stream);
   bool use_push(const CallPlan& p, std::uint64_t bytes) const;
+  bool use_nvls(const CallPlan& p, std::uint64_t bytes) const;
+  void launch_nvls_group(const std::vector<int>& locals, const std::vector<void*>& bufs, std::uint64_t bytes, int root,
+                         cudaStream_t stream);
+  void setup_nvls_ipc(const std::vector<std::vector<std::uint8_t>>& infos, const std::vector<std::uint64_t*>& regions,
+                      const std::vector<std::uint64_t>& region_bytes);
   cudaEvent_t event(LocalRank& r, std::size_t i);
   void ensure_scratch(int local_index, std::uint64_t bytes);
   void launch_ll(const std::vector<int>& locals, const std::vector<void*>& bufs, std::uint64_t bytes, int root,
@@ -281,6 +294,9 @@ class Group {
   int sms_{0};                  // SM count of the first device
   int local_chain_occ_{0};      // resident local_chain_kernel CTAs per SM
   int ll128_occ_{0};            // resident ll128_kernel CTAs per SM
+  int nvls_occ_{0};             // resident nvls_kernel CTAs per SM
+  std::unique_ptr<NvlsTeam> nvls_;  // multicast team (null: NVLS unavailable on this group)
+  std::string nvls_why_{"not set up"};
   std::mutex plan_mu_;
   std::map<std::tuple<int, int, std::uint64_t, int, std::uint64_t>, std::shared_ptr<CallPlan>> plans_;
 };

@@ -1,0 +1,132 @@
+// bcl_nvls — NVLS multicast broadcast (no reference
+// counterpart: the reference is CPU-only).
+//
+// One multicast object per communicator, bound to a staging ring on every GPU
+// of the group. The root streams the message through the multicast address
+// (multimem.st: the NVSwitch replicates every store to every GPU's copy, so
+// the root's NVLink egress carries M once and receivers only ingest); every
+// receiver copies its GPU's copy of each piece into its own buffer. All
+// signalling lives in the multicast-bound memory too: the root bumps a
+// per-slot `ready` counter and every receiver a per-slot `done` counter with
+// multimem.red (each GPU polls its local copy), so the path needs no peer
+// pointers at all.
+//
+// Ring geometry: kSlots slots of kSlotBytes; the message is cut into pieces
+// (<= one slot) identically on every rank; piece k of a call occupies global
+// sequence number seq_base + k, slot = seq % kSlots, round = seq / kSlots.
+// Writers wait for done[slot] >= n_recv * round, readers for
+// ready[slot] >= round + 1 (monotone counters: never reset).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "bcl_device.cuh"
+
+namespace bcl {
+
+namespace dev {
+
+constexpr std::uint32_t kNvlsSlots = 512;
+constexpr std::uint32_t kNvlsSlotBytes = 128u << 10;    // 64 MiB ring per GPU
+constexpr std::uint32_t kNvlsCtlBytes = 64u << 10;      // ready[kNvlsSlots] | done[kNvlsSlots], then data
+constexpr int kNvlsThreads = 512;
+constexpr int kNvlsTargetCtas = 148;                     // pieces per wave (identical on every rank)
+constexpr std::uint64_t kNvlsMinPiece = 16u << 10;
+
+struct NvlsRank {
+  int rank;
+  int is_root;
+  std::uint8_t* buf;
+  ErrorRecord* err;
+  int* abort;
+};
+
+template <int NL>
+struct NvlsParamsT {
+  int n_local;
+  int ctas;                 // CTAs per local rank
+  int n_recv;               // receivers of every piece (n - 1)
+  std::uint32_t pieces;
+  std::uint64_t bytes;
+  std::uint64_t piece_bytes;
+  std::uint64_t seq_base;
+  std::uint64_t timeout_ns;
+  std::uint32_t strict;     // fence.acq_rel.sys before every counter bump
+  std::uint8_t* mc;         // multicast mapping of the bound range (this GPU)
+  std::uint8_t* uc;         // this GPU's own copy
+  NvlsRank ranks[NL];
+};
+using NvlsParams = NvlsParamsT<kMaxLocal>;
+
+}  // namespace dev
+
+int launch_nvls(const dev::NvlsParams& p, void* stream);
+int nvls_occupancy(int* blocks_per_sm);
+
+// Piece geometry of an M-byte call (identical on every rank).
+struct NvlsGeometry {
+  std::uint64_t piece_bytes{};
+  std::uint32_t pieces{};
+};
+NvlsGeometry nvls_geometry(std::uint64_t bytes);
+
+// The multicast object and its per-device bindings owned by one process.
+class NvlsTeam {
+ public:
+  ~NvlsTeam();
+  // Whether the device (and driver) support multicast objects; `why` says
+  // why not.
+  static bool supported(int device, std::string* why);
+  // One process drives every GPU of the team.
+  static std::unique_ptr<NvlsTeam> create_local(const std::vector<int>& devices);
+
+  // One process per GPU. The owner (rank 0) creates the object for n GPUs and
+  // exports it: a fabric handle when the driver allows, else a POSIX fd served
+  // over an abstract Unix socket to the n - 1 importers.
+  static std::unique_ptr<NvlsTeam> create_owner(int n_devices, int device);
+  static constexpr std::size_t kBlobBytes = 128;
+  void export_blob(std::uint8_t out[kBlobBytes]) const;
+  static std::unique_ptr<NvlsTeam> import(const std::uint8_t blob[kBlobBytes], int device);
+  // Per-process steps after every rank imported: add this GPU, then bind and
+  // map (after every rank added its GPU; the caller agrees between steps).
+  void add_device();
+  void bind_and_map();
+
+  std::uint8_t* mc(int device) const;
+  std::uint8_t* uc(int device) const;
+  std::uint64_t size() const { return size_; }
+  // Reserve `pieces` ring sequence numbers for the next call on `device`;
+  // returns the first. Every GPU of the team walks the same sequence (one
+  // launch per GPU per call).
+  std::uint64_t take(int device, std::uint32_t pieces);
+  const std::string& handle_kind() const { return kind_; }
+
+ private:
+  NvlsTeam() = default;
+  struct Binding {
+    int device{-1};
+    unsigned long long mem{};  // CUmemGenericAllocationHandle
+    unsigned long long uc{};   // CUdeviceptr
+    unsigned long long mc{};
+    std::uint64_t seq{0};      // next ring sequence number of this GPU's launches
+    bool bound{false};
+  };
+  void bind_device(Binding& b);
+  unsigned long long handle_{};  // CUmemGenericAllocationHandle of the multicast object
+  std::uint64_t size_{};
+  std::uint64_t gran_{};
+  std::vector<Binding> bindings_;
+  std::string kind_;             // "local", "fabric" or "fd"
+  std::uint8_t fabric_[64]{};
+  std::string socket_name_;
+  int fd_{-1};
+  int listen_fd_{-1};
+  std::thread server_;
+  int n_devices_{0};
+};
+
+}  // namespace bcl
