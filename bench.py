@@ -532,6 +532,7 @@ def bench_multi(args, torch, rank, world):
     raw = comm.alloc(cap)  # same region; the e2e scratch lived above it
 
     sweep = []
+    nvls_ok, nvls_why = comm.nvls()
     if sweep_max:
         size = 4
         while size <= sweep_max:
@@ -544,6 +545,13 @@ def bench_multi(args, torch, rank, world):
             if size <= (1 << 20):  # CUDA events tick every ~2 us here: average 50 back-to-back calls too
                 bo, bn = back_to_back(size, True), back_to_back(size, False)
                 b2b = {"ours_us": round(bo * 1e6, 3), "nccl_us": round(bn * 1e6, 3), "vs_nccl": verdict(bo, bn)}
+            nv = None
+            if nvls_ok and size >= 1024:  # NVLS multicast comparison point (north_star), protocol forced
+                comm.set_protocol("nvls")
+                tv = run(size, steps, 3, True, B.AlgorithmConfig(B.Algorithm.direct, 0, 0), flush=False)
+                comm.set_protocol("auto")
+                nv = {"min": round(min(tv) * 1e6, 2), "median": round(statistics.median(tv) * 1e6, 2),
+                      "max": round(max(tv) * 1e6, 2), "busbw": round(size / statistics.median(tv) / 1e9, 2)}
             ch = c.chunk_bytes if c.algorithm == B.Algorithm.chain_pipelined else size
             t_roof = size / LINK_BW + (world - 1) * min(max(ch, 1), size) / LINK_BW
             sweep.append({"bytes": size, "algorithm": c.algorithm.name, "chunk": c.chunk_bytes,
@@ -554,7 +562,8 @@ def bench_multi(args, torch, rank, world):
                           "ours_busbw": round(size / to / 1e9, 2), "nccl_busbw": round(size / tn / 1e9, 2),
                           "frac_of_chain_roofline": round(t_roof / to, 4) if size >= (1 << 20) else None,
                           "vs_nccl": verdict(to, tn), "iterations": steps, "back_to_back": b2b,
-                          "ours_mean_us": round(statistics.mean(ours) * 1e6, 2)})
+                          "ours_mean_us": round(statistics.mean(ours) * 1e6, 2), "nvls_us": nv,
+                          "path": comm.path(size, None)})
             size *= 2
 
     cpu = None
@@ -603,6 +612,9 @@ def bench_multi(args, torch, rank, world):
             line["sweep_vs_nccl_back_to_back"] = {k: sum(1 for e in sweep if e["back_to_back"] and
                                                          e["back_to_back"]["vs_nccl"] == k)
                                                   for k in ("win", "tie", "loss")}
+            line["nvls"] = {"available": nvls_ok, "reason": nvls_why or None,
+                            "note": "nvls_us: the same broadcast forced onto the NVLS multicast path (protocol 5, "
+                                    "direct schedule), single-call medians like ours_us"}
             line["sweep_note"] = ("single-call medians (osu method; CUDA events tick every ~2 us on this box, so "
                                   "differences under one tick are noise) and, up to 1 MiB, the mean of 50 "
                                   "back-to-back calls; within 3% = tie")

@@ -111,6 +111,13 @@ void set_option(GroupOptions& o, const std::string& key, const std::string& v) {
   else if (key == "stage_bytes") o.stage_bytes = i64() < 0 ? -1 : i64() / 16 * 16;
   else if (key == "nvls") o.nvls = i32();
   else if (key == "nvls_strict") o.nvls_strict = i32() != 0;
+  else if (key == "nvls_slot") {
+    const std::uint64_t v = u64();
+    if (v < (16u << 10) || v > (8u << 20) || (v & (v - 1)) != 0) {
+      throw std::invalid_argument("nvls_slot must be a power of two in [16 KiB, 8 MiB]");
+    }
+    o.nvls_slot = static_cast<std::uint32_t>(v);
+  } else if (key == "nvls_ctas") o.nvls_ctas = std::max(1, i32());
   else if (key == "timeout_s") o.timeout_ns = static_cast<std::uint64_t>(std::strtod(s, nullptr) * 1e9);
   else throw std::invalid_argument("unknown communicator option '" + key + "'");
 }
@@ -118,7 +125,7 @@ void set_option(GroupOptions& o, const std::string& key, const std::string& v) {
 constexpr const char* kOptionNames[] = {
     "poll_ns", "window_bytes", "min_slice", "max_ctas", "strict_sys", "sys_scope", "eager_post", "writer_fence",
     "local_fused", "local_ctas", "local_item", "ll", "ll128", "ll128_coop", "protocol", "ll_max", "ll_chain_max", "ll128_max",
-    "host_piece", "stages", "stage_bytes", "nvls", "nvls_strict"};
+    "host_piece", "stages", "stage_bytes", "nvls", "nvls_strict", "nvls_slot", "nvls_ctas"};
 
 }  // namespace
 
@@ -750,11 +757,15 @@ bool Group::use_nvls(const CallPlan& p, std::uint64_t bytes) const {
 void Group::launch_nvls_group(const std::vector<int>& locals, const std::vector<void*>& bufs, std::uint64_t bytes,
                               int root, cudaStream_t stream) {
   if (bytes == 0) return;  // nothing moves (every rank skips alike)
-  const NvlsGeometry geo = nvls_geometry(bytes);
+  const std::uint32_t slot = opt_.nvls_slot ? opt_.nvls_slot : dev::kNvlsDefaultSlot;
+  const int wave = opt_.nvls_ctas > 0 ? opt_.nvls_ctas : dev::kNvlsDefaultCtas;
+  const NvlsGeometry geo = nvls_geometry(bytes, slot, wave);
   dev::NvlsParams P{};
   P.n_local = static_cast<int>(locals.size());
   const int cap = std::max(1, sms_ * std::max(nvls_occ_, 1) / P.n_local);
-  P.ctas = std::min<int>({static_cast<int>(geo.pieces), dev::kNvlsTargetCtas, cap});
+  P.ctas = std::min<int>({static_cast<int>(geo.pieces), wave, cap});
+  P.slot_bytes = slot;
+  P.slots = static_cast<std::uint32_t>(dev::kNvlsRingBytes / slot);
   P.n_recv = n_ - 1;
   P.pieces = geo.pieces;
   P.bytes = bytes;

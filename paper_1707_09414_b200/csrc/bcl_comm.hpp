@@ -104,6 +104,9 @@ struct GroupOptions {
   int nvls = -1;                                            // NVLS multicast: -1 auto (ranks on >= 2 GPUs with
                                                             // multicast support), 0 off, 1 required
   bool nvls_strict = false;                                 // system-scope fence before every NVLS counter bump
+  std::uint32_t nvls_slot = 0;                              // NVLS ring slot bytes (0 = 256 KiB; power of two,
+                                                            // 16 KiB .. 8 MiB; identical on every rank)
+  int nvls_ctas = 0;                                        // NVLS pieces per wave / CTAs per rank (0 = 148)
   static GroupOptions from_env();                           // BCL_* overrides (tuning runs)
   // "key=value,key=value" with the BCL_* names in lower case (e.g.
   // "stage_bytes=8192,sys_scope=1,protocol=2"); applied over *this.

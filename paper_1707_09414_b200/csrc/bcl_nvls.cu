@@ -123,20 +123,20 @@ __global__ void __launch_bounds__(kNvlsThreads) nvls_kernel(const __grid_constan
   if (li >= P.n_local) return;
   const NvlsRank& R = P.ranks[li];
   std::uint64_t* mc_ready = reinterpret_cast<std::uint64_t*>(P.mc);
-  std::uint64_t* mc_done = mc_ready + kNvlsSlots;
+  std::uint64_t* mc_done = mc_ready + kNvlsMaxSlots;
   const std::uint64_t* uc_ready = reinterpret_cast<const std::uint64_t*>(P.uc);
-  const std::uint64_t* uc_done = uc_ready + kNvlsSlots;
+  const std::uint64_t* uc_done = uc_ready + kNvlsMaxSlots;
   const unsigned T = blockDim.x;
   const unsigned tid = threadIdx.x;
   for (std::uint32_t k = static_cast<std::uint32_t>(j); k < P.pieces; k += static_cast<std::uint32_t>(P.ctas)) {
     const std::uint64_t seq = P.seq_base + k;
-    const std::uint32_t slot = static_cast<std::uint32_t>(seq % kNvlsSlots);
-    const std::uint64_t round = seq / kNvlsSlots;
+    const std::uint32_t slot = static_cast<std::uint32_t>(seq % P.slots);
+    const std::uint64_t round = seq / P.slots;
     const std::uint64_t off = static_cast<std::uint64_t>(k) * P.piece_bytes;
     const std::uint32_t len = static_cast<std::uint32_t>(min(P.piece_bytes, P.bytes - off));
     const std::uint32_t n16 = len / 16;
     const std::uint32_t tail = len % 16;
-    const std::size_t data_off = kNvlsCtlBytes + static_cast<std::size_t>(slot) * kNvlsSlotBytes;
+    const std::size_t data_off = kNvlsCtlBytes + static_cast<std::size_t>(slot) * P.slot_bytes;
     if (R.is_root) {
       // The slot's previous occupant must be consumed by every receiver.
       if (round > 0 && !cta_wait_geq(R, uc_done + slot, static_cast<std::uint64_t>(P.n_recv) * round, P.timeout_ns, k,
@@ -209,13 +209,15 @@ __global__ void __launch_bounds__(kNvlsThreads) nvls_kernel(const __grid_constan
 }  // namespace
 }  // namespace dev
 
-NvlsGeometry nvls_geometry(std::uint64_t bytes) {
+NvlsGeometry nvls_geometry(std::uint64_t bytes, std::uint32_t slot_bytes, int wave) {
   NvlsGeometry g;
   if (bytes == 0) return g;
-  const std::uint64_t per_wave = static_cast<std::uint64_t>(dev::kNvlsTargetCtas) * dev::kNvlsSlotBytes;
+  const std::uint64_t w = static_cast<std::uint64_t>(std::max(wave, 1));
+  const std::uint64_t per_wave = w * slot_bytes;
   const std::uint64_t waves = (bytes + per_wave - 1) / per_wave;
-  std::uint64_t piece = (bytes + dev::kNvlsTargetCtas * waves - 1) / (dev::kNvlsTargetCtas * waves);
-  piece = std::clamp<std::uint64_t>((piece + 15) / 16 * 16, dev::kNvlsMinPiece, dev::kNvlsSlotBytes);
+  std::uint64_t piece = (bytes + w * waves - 1) / (w * waves);
+  piece = std::clamp<std::uint64_t>((piece + 15) / 16 * 16, std::min<std::uint64_t>(dev::kNvlsMinPiece, slot_bytes),
+                                    slot_bytes);
   g.piece_bytes = piece;
   g.pieces = static_cast<std::uint32_t>((bytes + piece - 1) / piece);
   return g;
@@ -325,10 +327,7 @@ void rt(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string("NVLS: ") + what + ": " + cudaGetErrorString(e));
 }
 
-std::uint64_t bound_bytes() {
-  return static_cast<std::uint64_t>(dev::kNvlsCtlBytes) +
-         static_cast<std::uint64_t>(dev::kNvlsSlots) * dev::kNvlsSlotBytes;
-}
+std::uint64_t bound_bytes() { return static_cast<std::uint64_t>(dev::kNvlsCtlBytes) + dev::kNvlsRingBytes; }
 
 CUmulticastObjectProp mc_prop(int n_devices, std::uint64_t size, unsigned long long handle_types) {
   CUmulticastObjectProp prop = {};

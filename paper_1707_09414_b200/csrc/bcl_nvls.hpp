@@ -11,9 +11,10 @@
 // multimem.red (each GPU polls its local copy), so the path needs no peer
 // pointers at all.
 //
-// Ring geometry: kSlots slots of kSlotBytes; the message is cut into pieces
-// (<= one slot) identically on every rank; piece k of a call occupies global
-// sequence number seq_base + k, slot = seq % kSlots, round = seq / kSlots.
+// Ring geometry: a 64 MiB ring of `slots` slots (slot size: the nvls_slot
+// option); the message is cut into pieces (<= one slot) identically on every
+// rank; piece k of a call occupies global sequence number seq_base + k,
+// slot = seq % slots, round = seq / slots.
 // Writers wait for done[slot] >= n_recv * round, readers for
 // ready[slot] >= round + 1 (monotone counters: never reset).
 #pragma once
@@ -30,11 +31,12 @@ namespace bcl {
 
 namespace dev {
 
-constexpr std::uint32_t kNvlsSlots = 512;
-constexpr std::uint32_t kNvlsSlotBytes = 128u << 10;    // 64 MiB ring per GPU
-constexpr std::uint32_t kNvlsCtlBytes = 64u << 10;      // ready[kNvlsSlots] | done[kNvlsSlots], then data
+constexpr std::uint64_t kNvlsRingBytes = 64ull << 20;  // staging ring per GPU
+constexpr std::uint32_t kNvlsMaxSlots = 4096;            // ring / slot bytes (slot >= 16 KiB)
+constexpr std::uint32_t kNvlsCtlBytes = 64u << 10;      // ready[kNvlsMaxSlots] | done[kNvlsMaxSlots], then data
+constexpr std::uint32_t kNvlsDefaultSlot = 256u << 10;  // 1 GiB at n = 4: 2007 us vs 2350 us with 128 KiB (profiles/round2/nvls)
 constexpr int kNvlsThreads = 512;
-constexpr int kNvlsTargetCtas = 148;                     // pieces per wave (identical on every rank)
+constexpr int kNvlsDefaultCtas = 148;                    // pieces per wave (identical on every rank)
 constexpr std::uint64_t kNvlsMinPiece = 16u << 10;
 
 struct NvlsRank {
@@ -54,6 +56,8 @@ struct NvlsParamsT {
   std::uint64_t bytes;
   std::uint64_t piece_bytes;
   std::uint64_t seq_base;
+  std::uint32_t slots;      // ring slots (kNvlsRingBytes / slot_bytes)
+  std::uint32_t slot_bytes;
   std::uint64_t timeout_ns;
   std::uint32_t strict;     // fence.acq_rel.sys before every counter bump
   std::uint8_t* mc;         // multicast mapping of the bound range (this GPU)
@@ -67,12 +71,13 @@ using NvlsParams = NvlsParamsT<kMaxLocal>;
 int launch_nvls(const dev::NvlsParams& p, void* stream);
 int nvls_occupancy(int* blocks_per_sm);
 
-// Piece geometry of an M-byte call (identical on every rank).
+// Piece geometry of an M-byte call (identical on every rank, given the same
+// slot size and wave width): about `wave` pieces per wave, each <= one slot.
 struct NvlsGeometry {
   std::uint64_t piece_bytes{};
   std::uint32_t pieces{};
 };
-NvlsGeometry nvls_geometry(std::uint64_t bytes);
+NvlsGeometry nvls_geometry(std::uint64_t bytes, std::uint32_t slot_bytes, int wave);
 
 // The multicast object and its per-device bindings owned by one process.
 class NvlsTeam {
