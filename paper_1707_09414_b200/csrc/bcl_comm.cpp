@@ -97,6 +97,7 @@ void set_option(GroupOptions& o, const std::string& key, const std::string& v) {
   } else if (key == "local_fused") o.local_fused = i32() != 0;
   else if (key == "local_ctas") o.local_ctas = i32();
   else if (key == "local_item") o.local_item = u64();
+  else if (key == "local_claim") o.local_claim = i32();
   else if (key == "ll") o.ll = i32() != 0;
   else if (key == "ll128") o.ll128 = i32();
   else if (key == "ll128_coop") o.ll128_coop = i32() != 0;
@@ -124,7 +125,7 @@ void set_option(GroupOptions& o, const std::string& key, const std::string& v) {
 
 constexpr const char* kOptionNames[] = {
     "poll_ns", "window_bytes", "min_slice", "max_ctas", "strict_sys", "sys_scope", "eager_post", "writer_fence",
-    "local_fused", "local_ctas", "local_item", "ll", "ll128", "ll128_coop", "protocol", "ll_max", "ll_chain_max", "ll128_max",
+    "local_fused", "local_ctas", "local_item", "local_claim", "ll", "ll128", "ll128_coop", "protocol", "ll_max", "ll_chain_max", "ll128_max",
     "host_piece", "stages", "stage_bytes", "nvls", "nvls_strict", "nvls_slot", "nvls_ctas"};
 
 }  // namespace
@@ -700,6 +701,7 @@ Group::~Group() {
     if (r.d_peers) cudaFree(r.d_peers);
     if (r.d_regs) cudaFree(r.d_regs);
     if (r.heap) cudaFree(r.heap);
+    if (lc_claim_ != nullptr && &r == &local_.front()) cudaFree(lc_claim_);
     if (r.scratch && !ipc_) cudaFree(r.scratch);
     if (r.err_host) cudaFreeHost(r.err_host);
     if (r.stream) cudaStreamDestroy(r.stream);
@@ -826,12 +828,30 @@ void Group::launch_local_chain(const std::vector<int>& locals, const std::vector
   DeviceScope ds(local_[static_cast<std::size_t>(locals[0])].device);
   const int ctas = opt_.local_ctas > 0 ? opt_.local_ctas : sms_ * std::max(local_chain_occ_, 1);
   const std::uint64_t warps = static_cast<std::uint64_t>(ctas) * 8;
-  // ~4 items per warp (load balance; ~3.5 KiB at 64 MiB: 52 us vs 56 us with
-  // 7 KiB items, profiles/round1/fused_n1_variants.log), 2 KiB .. one chunk.
-  std::uint64_t item = opt_.local_item > 0 ? opt_.local_item : bytes / (4 * warps);
+  // Items claimed dynamically (load balance) of ~4 KiB: 43.6-43.9 us at
+  // config 1 against 44.3-45.3 us for 2, 3 or 6 KiB (profiles/round2/n1/
+  // variants.log); very large messages use larger items (fewer claims on the
+  // one counter), small ones smaller items (every warp busy).
+  std::uint64_t item = opt_.local_item;
+  if (item == 0) {
+    const std::uint64_t cap = std::max<std::uint64_t>(4096, bytes / (64 * warps));
+    item = std::clamp<std::uint64_t>(bytes / (4 * warps), 2048, cap);
+  }
   const std::uint64_t hi = std::max<std::uint64_t>(p.chunk_bytes, 16);
   item = std::clamp<std::uint64_t>((item + 15) / 16 * 16, std::min<std::uint64_t>(2048, hi), hi);
   P.item_bytes = std::min<std::uint64_t>(item, p.chunk_bytes);
+  if (opt_.local_claim) {
+    constexpr int kClaimSlots = 64;  // launches that may run concurrently (different streams)
+    if (lc_claim_ == nullptr) {
+      ck(cudaMalloc(&lc_claim_, kClaimSlots * sizeof(unsigned long long)), "cudaMalloc(claims)");
+      ck(cudaMemset(lc_claim_, 0, kClaimSlots * sizeof(unsigned long long)), "cudaMemset(claims)");
+    }
+    const std::uint64_t ipc = (p.chunk_bytes + P.item_bytes - 1) / P.item_bytes;
+    if (static_cast<std::uint64_t>(p.n_chunks) * ipc + warps >= (1ull << 32)) {
+      throw std::invalid_argument("local chain: too many items for one launch (raise local_item)");
+    }
+    P.claim = lc_claim_ + (lc_launches_++ % kClaimSlots);
+  }
   ck(static_cast<cudaError_t>(bcl::launch_local_chain(P, ctas, stream)), "launch(local chain)");
 }
 

@@ -91,6 +91,8 @@ struct GroupOptions {
   bool local_fused = true;                                  // single-GPU groups: fused flag-free chain kernel
   int local_ctas = 0;                                       // its grid (0 = all resident CTAs)
   std::uint64_t local_item = 0;                             // its per-warp item bytes (0 = auto)
+  int local_claim = 1;                                      // its items: 1 claimed dynamically (46.3 vs 49.6 us,
+                                                            // config 1), 0 static round robin
   bool ll = true;                                           // LL push protocol for small `direct` calls
   int protocol = 0;                                         // chain: 0 auto (table), 1 pull, 2 push
   std::uint64_t ll_max_bytes = 0;                           // LL threshold (0 = 2 MiB, lowered for many ranks)
@@ -298,6 +300,8 @@ class Group {
   int local_chain_occ_{0};      // resident local_chain_kernel CTAs per SM
   int ll128_occ_{0};            // resident ll128_kernel CTAs per SM
   int nvls_occ_{0};             // resident nvls_kernel CTAs per SM
+  unsigned long long* lc_claim_{nullptr};  // local_chain_kernel item counters [64] (device; zero between uses)
+  std::uint64_t lc_launches_{0};
   std::unique_ptr<NvlsTeam> nvls_;  // multicast team (null: NVLS unavailable on this group)
   std::string nvls_why_{"not set up"};
   std::mutex plan_mu_;

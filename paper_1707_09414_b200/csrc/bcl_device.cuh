@@ -192,6 +192,8 @@ struct LocalChainParams {
   std::uint8_t* buf[kMaxLocal];              // by logical rank (root first)
   int rank[kMaxLocal];                       // global rank of each logical rank
   unsigned long long* prov[kMaxLocal];       // optional provenance of each logical rank
+  unsigned long long* claim;                 // dynamic item claims: a zeroed counter this launch owns
+                                             // (the last claimer re-zeroes it), or null: static
 };
 
 struct BarrierParams {

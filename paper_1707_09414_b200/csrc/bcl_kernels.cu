@@ -108,6 +108,7 @@ __device__ __forceinline__ void st_v4(uint4* p, const uint4& v) {
                : "memory");
 }
 
+
 __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
   return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -862,31 +863,50 @@ __global__ void __launch_bounds__(kThreads, NL == 1 ? 1 : BCL_SHARED_MIN_BLOCKS)
 
 // Single-GPU groups: the chain's hops fused per item (LocalChainParams).
 #ifndef BCL_LC_MINB
-#define BCL_LC_MINB 4
+#define BCL_LC_MINB 3  // 80 registers, no spills: 43.7 us at config 1 vs 47.5 us at 4 CTAs/SM (64 registers,
+                       // spilling once items are claimed dynamically; profiles/round2/n1/variants.log)
 #endif
 __global__ void __launch_bounds__(256, BCL_LC_MINB) local_chain_kernel(const __grid_constant__ LocalChainParams P) {
   const int lane = static_cast<int>(threadIdx.x & 31);
-  const std::uint64_t g = (static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const std::uint64_t G = (static_cast<std::uint64_t>(gridDim.x) * blockDim.x) >> 5;
-  const std::uint64_t ipc = (P.chunk_bytes + P.item_bytes - 1) / P.item_bytes;  // items per chunk
-  const std::uint64_t items = static_cast<std::uint64_t>(P.n_chunks) * ipc;
+  const std::uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const std::uint32_t G = (gridDim.x * blockDim.x) >> 5;
+  const std::uint32_t ipc = static_cast<std::uint32_t>((P.chunk_bytes + P.item_bytes - 1) / P.item_bytes);
+  const std::uint32_t items = P.n_chunks * ipc;  // < 2^32 (host-checked)
   Ctx c{};
   c.lane_id = lane;
-  for (std::uint64_t i = g; i < items; i += G) {
-    const std::uint32_t ch = static_cast<std::uint32_t>(i / ipc);
+  // Items are claimed statically (i = g, g + G, ...) or, with a claim
+  // counter, dynamically: each warp takes the next unclaimed item, so warps
+  // whose items ran slower do not leave the others idle at the end. Every
+  // warp claims once past the last item, so the claim that returns
+  // items + G - 1 is the launch's last: it re-zeroes the counter for the
+  // launch that reuses it (stream order; the host rotates 64 counters).
+  const bool dyn = P.claim != nullptr;
+  auto claim = [&]() -> std::uint32_t {
+    unsigned long long v = 0;
+    if (lane == 0) {
+      v = atomicAdd(P.claim, 1ull);
+      if (v == static_cast<unsigned long long>(items) + G - 1) *P.claim = 0;
+    }
+    return static_cast<std::uint32_t>(__shfl_sync(0xffffffffu, v, 0));
+  };
+  std::uint32_t i = dyn ? claim() : g;
+  while (i < items) {
+    const std::uint32_t ch = i / ipc;
     const std::uint64_t off = static_cast<std::uint64_t>(ch) * P.chunk_bytes;
-    const std::uint64_t len = P.bytes - off < P.chunk_bytes ? P.bytes - off : P.chunk_bytes;
-    const std::uint64_t lo = off + (i % ipc) * P.item_bytes;
-    if (lo >= off + len) continue;
-    const std::uint64_t hi = lo + P.item_bytes < off + len ? lo + P.item_bytes : off + len;
-    for (int h = 1; h < P.n_ranks; ++h) {
-      warp_copy(c, P.buf[h - 1], P.buf[h], lo, hi);
-      __syncwarp();  // hop h's stores are visible to hop h + 1's loads (same warp)
-      if (P.prov[h] != nullptr && lane == 0) {
-        atomicAdd(&P.prov[h][static_cast<std::uint64_t>(P.rank[h - 1]) * P.n_chunks + ch],
-                  static_cast<unsigned long long>(hi - lo));
+    const std::uint64_t end = P.bytes - off < P.chunk_bytes ? P.bytes : off + P.chunk_bytes;
+    const std::uint64_t lo = off + static_cast<std::uint64_t>(i - ch * ipc) * P.item_bytes;
+    if (lo < end) {
+      const std::uint64_t hi = lo + P.item_bytes < end ? lo + P.item_bytes : end;
+      for (int h = 1; h < P.n_ranks; ++h) {
+        warp_copy(c, P.buf[h - 1], P.buf[h], lo, hi);
+        __syncwarp();  // hop h's stores are visible to hop h + 1's loads (same warp)
+        if (P.prov[h] != nullptr && lane == 0) {
+          atomicAdd(&P.prov[h][static_cast<std::uint64_t>(P.rank[h - 1]) * P.n_chunks + ch],
+                    static_cast<unsigned long long>(hi - lo));
+        }
       }
     }
+    i = dyn ? claim() : i + G;
   }
 }
 

@@ -189,6 +189,45 @@ def test_config1_full_size_all_ranks_equal_root():
         assert torch.equal(bufs[r], bufs[0])
 
 
+@pytest.mark.parametrize("claim", [1, 0])
+def test_fused_chain_claimed_items_back_to_back_and_two_streams(claim):
+    """The fused single-GPU kernel claims items from a per-launch counter that
+    its last claimer re-zeroes: 60 back-to-back calls of changing size, item
+    size and root (no host sync between them), then calls on two streams that
+    may overlap (each launch owns its own counter), every byte checked."""
+    n = 4
+    comms = comms_for(n, {"local_claim": claim})
+    assert comms[0].path(1 << 20, cfg_of("chain_pipelined", 65536)) == "local_chain_kernel"
+    rng = random.Random(61 + claim)
+    cap = 9 << 20
+    bufs = [torch.zeros(cap, dtype=torch.uint8, device="cuda:0") for _ in range(n)]
+    expect = []
+    for it in range(60):
+        m = rng.choice([rng.randrange(1, 5000), rng.randrange(5000, 1 << 20), rng.randrange(1 << 20, cap + 1)])
+        root = rng.randrange(n)
+        bufs[root][:m].fill_((it * 13 + 1) & 0xFF)
+        B.bcast_all(comms, [b[:m] for b in bufs], m, "uint8", root, cfg_of("chain_pipelined", rng.choice([4096, 65536, 524288])))
+        expect.append((m, (it * 13 + 1) & 0xFF))
+        if it % 10 == 9:
+            torch.cuda.synchronize()
+            for r in range(n):
+                assert int(bufs[r][:m].min()) == expect[-1][1] == int(bufs[r][:m].max()), (it, m, r)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    other = [torch.zeros(cap, dtype=torch.uint8, device="cuda:0") for _ in range(n)]
+    torch.cuda.synchronize()
+    for it in range(8):
+        for k, (bs, st) in enumerate(((bufs, s1), (other, s2))):
+            with torch.cuda.stream(st):
+                bs[0].fill_(100 + 2 * it + k)
+            B.bcast_all(comms, bs, cap, "uint8", 0, cfg_of("chain_pipelined", 524288), streams=[st] * n)
+    torch.cuda.synchronize()
+    for k, bs in enumerate((bufs, other)):
+        for r in range(n):
+            assert int(bs[r].min()) == 100 + 14 + k == int(bs[r].max()), (k, r)
+    for c in comms:
+        c.check()
+
+
 @pytest.mark.parametrize("variant", ["auto", "xpull", "xpush", "ll128"])
 def test_back_to_back_calls_change_payload_and_root(variant):
     """Epoch stress: buffers reused immediately, roots and payloads vary; the

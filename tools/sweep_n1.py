@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Dev tool: BASELINE config 1 (4 ranks on cuda:0, 64 MiB, 512 KiB chunks,
 pipelined chain) under a grid of GroupOptions env settings; mean device time
-per broadcast with an L2 flush between steps (bench.py's method, no checks
+per broadcast with an L2 read-sweep flush between steps (bench.py's method, no checks
 beyond a final equality).  SWEEP='A=1,B=2;C=3' python tools/sweep_n1.py"""
 import os, statistics, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -12,7 +12,7 @@ chunks = [int(x) for x in os.environ.get("CHUNKS", str(512 << 10)).split(",")]
 dev = torch.device("cuda:0")
 bufs = [torch.zeros(m, dtype=torch.uint8, device=dev) for _ in range(n)]
 bufs[0].copy_(torch.randint(0, 256, (m,), dtype=torch.uint8, device=dev))
-flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+flush = torch.ones(256 << 18, dtype=torch.int32, device=dev)
 stream = torch.cuda.Stream()
 torch.cuda.synchronize()
 for setting in [""] + [s for s in os.environ.get("SWEEP", "").split(";") if s]:
@@ -30,7 +30,7 @@ for setting in [""] + [s for s in os.environ.get("SWEEP", "").split(";") if s]:
             with torch.cuda.stream(stream):
                 for r in range(1, n):
                     bufs[r].zero_()
-                flush.fill_(it & 0xFF)
+                torch.sum(flush)  # read sweep (bench.py flush_l2)
                 torch.cuda._sleep(200_000)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
@@ -41,7 +41,7 @@ for setting in [""] + [s for s in os.environ.get("SWEEP", "").split(";") if s]:
                 ts.append(e0.elapsed_time(e1) * 1e3)
         ok = all(torch.equal(bufs[r], bufs[0]) for r in range(1, n))
         t = statistics.mean(ts)
-        out.append(f"C={c}: {t:.1f}us ({2 * (n - 1) * m / t / 1e3:.0f} GB/s HBM) ok={ok}")
+        out.append(f"C={c}: {t:.1f}us (P*M {n * m / t / 1e3:.0f} GB/s) ok={ok}")
     print(f"[{setting or 'default'}] lanes={comms[0].info()['lanes']} " + " | ".join(out), flush=True)
     for c_ in comms:
         c_.close()
