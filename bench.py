@@ -296,6 +296,16 @@ def main():
 GATE_CYCLES = 1_000_000  # ~0.5 ms spin: the host enqueues the timed ops behind it
 
 
+HOST_RESET_NOTE = ("receivers' host buffers zeroed before every step by a D2H copy of zeros (outside the timed "
+                   "region); a CPU memset would leave them dirty in the CPU caches, which the broadcast's D2H "
+                   "DMA then pays for (raw 192 MiB D2H 4.75 vs 3.55 ms, profiles/round2/n1/e2e_probe4.log)")
+
+
+def host_reset(host, zeros):
+    """Zero a pinned host buffer by DMA (see HOST_RESET_NOTE)."""
+    host.copy_(zeros[:host.numel()])
+
+
 def flush_l2(torch, flush):
     """Evict L2 with a READ sweep of 256 MiB: it writes back the previous
     step's dirty lines before the timed region and leaves only clean lines
@@ -375,16 +385,17 @@ def bench_single(args, torch):
     # e2e through the C-ABI with pinned host buffers (run_bcast_host).
     hosts = [torch.empty(m, dtype=torch.uint8, pin_memory=True) for _ in range(n)]
     hosts[0].copy_(bufs[0].cpu())
+    zeros = torch.zeros(m, dtype=torch.uint8, device=dev)
     e2e = []
     for it in range(args.warmup + max(3, args.steps // 2)):
         for r in range(1, n):
-            hosts[r].zero_()
+            host_reset(hosts[r], zeros)
         w = B.run_bcast_host(comms, 0, hosts, m, cfg)
+        for r in range(1, n):  # verify before recording
+            if not torch.equal(hosts[r], hosts[0]):
+                raise RuntimeError("e2e verification failed")
         if it >= args.warmup:
             e2e.append(w)
-    for r in range(1, n):
-        if not torch.equal(hosts[r], hosts[0]):
-            raise RuntimeError("e2e verification failed")
     e2e_t = statistics.mean(e2e)
 
     cpu = reference_cpu(n, m, chunk, args.cpu_iters)
@@ -407,7 +418,7 @@ def bench_single(args, torch):
                          "kind": cpu["kind"], "sample": cpu["sample"]},
         "e2e": {"value": round(m / e2e_t / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": m,
                 "d2h_bytes_per_step": (n - 1) * m, "latency_ms": round(e2e_t * 1e3, 3),
-                "path": "bcl_run_bcast_host (C-ABI), pinned host buffers"},
+                "path": "bcl_run_bcast_host (C-ABI), pinned host buffers", "reset": HOST_RESET_NOTE},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
@@ -512,11 +523,12 @@ def bench_multi(args, torch, rank, world):
     host = torch.empty(m, dtype=torch.uint8, pin_memory=True)
     ref_host = ref_all[:m].cpu()
     e2e = []
+    zeros = torch.zeros(m, dtype=torch.uint8, device=dev)
     for it in range(args.warmup + max(3, args.steps // 2)):
         if rank == 0:
             host.copy_(ref_host)
         else:
-            host.zero_()
+            host_reset(host, zeros)
         dist.barrier(device_ids=[local])
         t0 = time.perf_counter()
         comm.bcast_host(host, m, "uint8", 0, cfg, stream=stream)
@@ -602,7 +614,7 @@ def bench_multi(args, torch, rank, world):
                              "kind": cpu["kind"], "sample": cpu["sample"], "host": host_cpu()},
             "e2e": {"value": round(m / statistics.mean(e2e) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": m,
                     "d2h_bytes_per_step": (world - 1) * m, "latency_ms": round(statistics.mean(e2e) * 1e3, 3),
-                    "path": "bcl_bcast_host (C-ABI) per rank, pinned host buffers"},
+                    "path": "bcl_bcast_host (C-ABI) per rank, pinned host buffers", "reset": HOST_RESET_NOTE},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "sweep": sweep,

@@ -189,6 +189,7 @@ void Group::alloc_rank(LocalRank& r, std::size_t heap_bytes) {
   ck(cudaStreamCreateWithFlags(&r.stream, cudaStreamDefault), "cudaStreamCreate");
   ck(cudaStreamCreateWithFlags(&r.copy_in, cudaStreamNonBlocking), "cudaStreamCreate(copy_in)");
   ck(cudaStreamCreateWithFlags(&r.copy_out, cudaStreamNonBlocking), "cudaStreamCreate(copy_out)");
+  ck(cudaStreamCreateWithFlags(&r.host_mid, cudaStreamNonBlocking), "cudaStreamCreate(host_mid)");
   if (heap_bytes > 0) {
     ck(cudaMalloc(&r.heap, heap_bytes), "cudaMalloc(heap)");
     r.heap_bytes = heap_bytes;
@@ -707,6 +708,7 @@ Group::~Group() {
     if (r.stream) cudaStreamDestroy(r.stream);
     if (r.copy_in) cudaStreamDestroy(r.copy_in);
     if (r.copy_out) cudaStreamDestroy(r.copy_out);
+    if (r.host_mid) cudaStreamDestroy(r.host_mid);
     for (cudaEvent_t e : r.events) cudaEventDestroy(e);
   }
 }
@@ -1350,8 +1352,9 @@ double Group::run_bcast_host(const std::vector<void*>& host_bufs, std::uint64_t 
   const auto ps = pieces_of(bytes, opt_.host_piece);
   const auto t0 = std::chrono::steady_clock::now();
   LocalRank& R = local_[static_cast<std::size_t>(root_li)];
-  // Ranks sharing a GPU run in one launch on the first local rank's stream.
-  auto compute_of = [this](int dev) { return local_[static_cast<std::size_t>(by_device_.at(dev).front())].stream; };
+  // Ranks sharing a GPU run in one launch on the first local rank's stream
+  // (a non-blocking one: the scratch buffers depend on no legacy-stream work).
+  auto compute_of = [this](int dev) { return local_[static_cast<std::size_t>(by_device_.at(dev).front())].host_mid; };
   auto owner_of = [this](int dev) -> LocalRank& { return local_[static_cast<std::size_t>(by_device_.at(dev).front())]; };
   std::map<int, std::size_t> ev;  // per device event cursor
   for (const auto& kv : by_device_) ev[kv.first] = 0;
@@ -1365,8 +1368,12 @@ double Group::run_bcast_host(const std::vector<void*>& host_bufs, std::uint64_t 
       ck(cudaStreamWaitEvent(compute_of(R.device), in, 0), "cudaStreamWaitEvent");
     }
     std::vector<void*> dbufs;
-    for (LocalRank& r : local_) dbufs.push_back(r.scratch + p.off);
-    bcast_all(dbufs, p.len, root, cfg, {});
+    std::vector<cudaStream_t> mids;
+    for (LocalRank& r : local_) {
+      dbufs.push_back(r.scratch + p.off);
+      mids.push_back(compute_of(r.device));
+    }
+    bcast_all(dbufs, p.len, root, cfg, mids);
     if (!p.len) continue;
     for (const auto& kv : by_device_) {
       DeviceScope ds(kv.first);
@@ -1387,7 +1394,7 @@ double Group::run_bcast_host(const std::vector<void*>& host_bufs, std::uint64_t 
     DeviceScope ds(kv.first);
     LocalRank& owner = owner_of(kv.first);
     ck(cudaStreamSynchronize(owner.copy_out), "synchronize");
-    ck(cudaStreamSynchronize(owner.stream), "synchronize");
+    ck(cudaStreamSynchronize(owner.host_mid), "synchronize");
     ck(cudaStreamSynchronize(owner.copy_in), "synchronize");
     all.insert(all.end(), kv.second.begin(), kv.second.end());
   }

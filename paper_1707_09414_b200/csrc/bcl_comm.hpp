@@ -99,7 +99,8 @@ struct GroupOptions {
   std::int64_t ll_chain_max_bytes = -1;                     // LL pipelined chain up to this size (-1 = default)
   std::int64_t ll128_max_bytes = -1;                        // LL128 pipelined chain up to this size (-1 = no limit
                                                             // beyond the table's rule; 0 = off)
-  std::uint64_t host_piece = 4ull << 20;                    // host-buffer calls: H2D/bcast/D2H pipeline piece
+  std::uint64_t host_piece = 16ull << 20;                   // host-buffer calls: H2D/bcast/D2H pipeline piece
+                                                            // (config 1 e2e: 4.78 ms vs 5.25 ms with 4 MiB)
   std::int64_t stage_bytes = -1;                            // bulk-copy stage per warp: 0 = vector loads,
                                                             // -1 = auto (8 KiB across GPUs, 0 on one GPU)
   std::uint32_t stages = 2;                                 // bulk-copy stages per copy warp
@@ -147,6 +148,7 @@ struct LocalRank {
   cudaStream_t stream{};        // internal stream for run_bcast
   cudaStream_t copy_in{};       // host-buffer calls: H2D stream
   cudaStream_t copy_out{};      // host-buffer calls: D2H stream
+  cudaStream_t host_mid{};      // run_bcast_host: broadcast stream (non-blocking)
   std::vector<cudaEvent_t> events;
   unsigned long long* prov{};   // optional provenance counters
   unsigned long long* trace{};  // optional per-lane event timestamps
