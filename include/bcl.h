@@ -188,8 +188,11 @@ bcl_status_t bcl_comm_init_rank(int n, int rank, int device, size_t heap_bytes,
  *                  default 8192 across GPUs, 0 when every rank shares one GPU)
  *   sys_scope      1: system-scope flag polls and fences even when every rank
  *                  shares one GPU (the cross-GPU code path on one device)
- *   strict_sys     1: system-scope fence in the publisher before every flag
- *   writer_fence   0 publisher fences, 1 gpu scope (default), 2 the call's scope
+ *   strict_sys     1 (default): system-scope fence in the publisher before
+ *                  every flag batch (the PTX-model release); 0: the copy warps'
+ *                  gpu-scope writer fence instead (faster for pull at n >= 3)
+ *   writer_fence   with strict_sys=0: 0 publisher fences, 1 gpu scope, 2 the
+ *                  call's scope
  *   ll128          -1 auto (ranks on distinct GPUs), 0 off, 1 also between
  *                  ranks sharing a GPU;  ll128_max, ll_chain_max, ll_max caps
  *   nvls           NVLS multicast team: -1 auto (ranks on two or more GPUs with

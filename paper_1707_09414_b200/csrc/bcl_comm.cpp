@@ -101,6 +101,7 @@ void set_option(GroupOptions& o, const std::string& key, const std::string& v) {
   else if (key == "ll") o.ll = i32() != 0;
   else if (key == "ll128") o.ll128 = i32();
   else if (key == "ll128_coop") o.ll128_coop = i32() != 0;
+  else if (key == "ll128_ctas") o.ll128_ctas = std::clamp(i32(), 0, dev::kLL128MaxCtas);
   else if (key == "protocol") {
     o.protocol = i32();
     if (o.protocol < 0 || o.protocol > 5) throw std::invalid_argument("protocol must be 0..5");
@@ -125,7 +126,7 @@ void set_option(GroupOptions& o, const std::string& key, const std::string& v) {
 
 constexpr const char* kOptionNames[] = {
     "poll_ns", "window_bytes", "min_slice", "max_ctas", "strict_sys", "sys_scope", "eager_post", "writer_fence",
-    "local_fused", "local_ctas", "local_item", "local_claim", "ll", "ll128", "ll128_coop", "protocol", "ll_max", "ll_chain_max", "ll128_max",
+    "local_fused", "local_ctas", "local_item", "local_claim", "ll", "ll128", "ll128_coop", "ll128_ctas", "protocol", "ll_max", "ll_chain_max", "ll128_max",
     "host_piece", "stages", "stage_bytes", "nvls", "nvls_strict", "nvls_slot", "nvls_ctas"};
 
 }  // namespace
@@ -219,6 +220,12 @@ int lanes_for(int device, int ranks_per_device, int cap, const GroupOptions& opt
   ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
   const std::size_t smem =
       opt.stage_bytes > 0 ? bcast_smem_bytes(opt.stages, static_cast<std::uint32_t>(opt.stage_bytes)) : 0;
+  int smem_max = 0;
+  ck(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, device), "smem limit");
+  if (smem + 4096 > static_cast<std::size_t>(smem_max)) {
+    throw std::invalid_argument("stages x stage_bytes x 8 copy warps (" + std::to_string(smem) +
+                                " B) exceeds the per-CTA shared memory (" + std::to_string(smem_max) + " B)");
+  }
   ck(static_cast<cudaError_t>(prepare_bcast_kernels(smem)), "cudaFuncSetAttribute(smem)");
   int occ = 0;
   ck(static_cast<cudaError_t>(bcast_kernel_occupancy(&occ, smem)), "occupancy");
@@ -1049,7 +1056,8 @@ void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& 
   if (mode == 2) {  // a warp moves 4 lines per step: ~2 steps per warp, up to 3 CTAs per SM
     const std::uint32_t per_cta = dev::kLLThreads / 32 * 4 * 2;
     // every CTA of every rank co-resident (writers wait on ring credits)
-    const int cap = std::max(1, std::min(dev::kLL128MaxCtas, sms_ * std::max(ll128_occ_, 1)) / P.n_local);
+    int cap = std::max(1, std::min(dev::kLL128MaxCtas, sms_ * std::max(ll128_occ_, 1)) / P.n_local);
+    if (opt_.ll128_ctas > 0) cap = std::min(cap, opt_.ll128_ctas);
     P.ctas = std::clamp<int>(static_cast<int>((P.lines + per_cta - 1) / per_cta), 1, cap);
   }
   P.timeout_ns = opt_.timeout_ns;

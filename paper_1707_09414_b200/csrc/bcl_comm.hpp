@@ -77,7 +77,12 @@ struct GroupOptions {
   std::uint64_t min_slice = 2048;                           // smallest per-lane slice of a chunk
   int max_ctas_per_rank = 0;                                // 0 = SM count
   std::uint32_t poll_ns = 64;                               // back-off between flag polls (ns)
-  bool strict_sys = false;                                  // system-scope fence before every flag
+  bool strict_sys = true;                                   // the publisher releases every flag batch with a
+                                                            // system-scope fence (the PTX-model release; free at
+                                                            // n = 2, where no rank forwards; and LL128, the n >= 3
+                                                            // default, needs no fence). 0: the copy warps' gpu-scope
+                                                            // writer fence instead (a hardware property, ~1.5x
+                                                            // faster for pull at n = 4)
   int sys_scope = -1;                                       // flag polls/fences at system scope: -1 auto (ranks
                                                             // span GPUs), 1 always (runs the cross-GPU code on one GPU)
   bool eager_post = true;                                   // bulk chain: forward a chunk once its store is done
@@ -85,6 +90,8 @@ struct GroupOptions {
                                                             // 0 no (the publisher fences), 1 gpu scope, 2 the call's
                                                             // scope (system across GPUs; 2.6x slower at n = 4, the
                                                             // fence waits for the warp's in-flight TMA pulls)
+  int ll128_ctas = 0;                                       // LL128 CTAs per rank cap (0 = 3 per SM; identical on
+                                                            // every rank)
   bool ll128_coop = true;                                   // LL128 with one rank per GPU: cooperative launch
   int ll128 = -1;                                           // LL128 chain lines: -1 auto (every rank on its own
                                                             // GPU), 0 off, 1 also for ranks sharing a GPU

@@ -52,8 +52,8 @@ VARIANTS = {
     "pull": ({}, "pull"),
     "ll": ({}, "ll"),
     "push": ({}, "push"),
-    "xpull": (XGPU, "pull"),
-    "xstrict": (dict(XGPU, strict_sys=1), "pull"),
+    "xpull": (dict(XGPU, strict_sys=0), "pull"),  # gpu-scope writer fence (opt-in)
+    "xstrict": (XGPU, "pull"),                   # system-scope publisher release (default)
     "xpush": (XGPU, "push"),
     "ll128": ({"ll128": 1, "ll128_max": 32 << 20, "sys_scope": 1}, "ll128"),
 }
@@ -353,6 +353,10 @@ def test_host_buffer_run_bcast():
 def test_options_are_validated():
     with pytest.raises(ValueError):
         B.Comm.local([0, 0], bogus_knob=1)
+    with pytest.raises(ValueError, match="shared memory"):  # 4 x 8 KiB stages x 8 warps > 227 KiB
+        B.Comm.local([0, 0], stage_bytes=8192, stages=4)
+    with pytest.raises(ValueError, match="nvls_slot"):
+        B.Comm.local([0, 0], nvls_slot=3000)
     comms = comms_for(2)  # ranks sharing a GPU: LL128 only with the ll128=1 option
     bufs = [torch.zeros(16, dtype=torch.uint8, device="cuda:0") for _ in comms]
     for c in comms:
