@@ -9,10 +9,12 @@ acks until its device timeout (--timeout, default 3 s) fires; the receiver's
 kernel then runs with every flag already set and pulls the whole message over
 NVLink (every ncu replay repeats exactly that). LL128 up to ~54 MB never waits
 at the root (each warp writes fewer groups than its ring depth), so both
-kernels complete. Without ncu both kernels run concurrently and the call
+kernels complete. NVLS below the 64 MiB ring never waits at the root either
+(the root's multicast stores land in every GPU's ring copy; the receiver then
+copies its copy out). Without ncu both kernels run concurrently and the call
 succeeds; the receiver's buffer is verified either way.
 
-  python tools/r2/ncu_xgpu.py pull|ll128|xpull_vec BYTES [--timeout S]
+  python tools/r2/ncu_xgpu.py pull|ll128|pull_vec|nvls BYTES [--timeout S]
 """
 import argparse
 import os
@@ -25,7 +27,7 @@ import paper_1707_09414_b200 as B  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=["pull", "ll128", "pull_vec"])
+    ap.add_argument("mode", choices=["pull", "ll128", "pull_vec", "nvls"])
     ap.add_argument("bytes", type=int)
     ap.add_argument("--chunk", type=int, default=65536)
     ap.add_argument("--timeout", type=float, default=3.0)
@@ -33,7 +35,7 @@ def main():
     opts = {"stage_bytes": 0} if args.mode == "pull_vec" else {}
     comms = B.Comm.local([0, 1], timeout_s=args.timeout, **opts)
     for c in comms:
-        c.set_protocol("ll128" if args.mode == "ll128" else "pull")
+        c.set_protocol({"ll128": "ll128", "nvls": "nvls"}.get(args.mode, "pull"))
     m = args.bytes
     bufs = [torch.zeros(m, dtype=torch.uint8, device=f"cuda:{d}") for d in (0, 1)]
     bufs[0].copy_(torch.randint(0, 256, (m,), dtype=torch.uint8, device="cuda:0",
