@@ -170,9 +170,23 @@ class LocalGroup {
   void set_table(const Table& t) {
     for (bcl_comm_t c : comms_) check(bcl_comm_set_table(c, t.get()));
   }
-  // Chain transport (B200 only): 0 auto, 1 pull, 2 push, 3 LL, 4 LL128.
+  // Transport (B200 only): 0 auto, 1 pull, 2 push, 3 LL, 4 LL128, 5 NVLS multicast.
   void set_protocol(int protocol) {
     for (bcl_comm_t c : comms_) check(bcl_comm_set_protocol(c, protocol));
+  }
+  // Whether the group has an NVLS multicast team (ranks on >= 2 GPUs with
+  // multicast support); `why` receives the reason when it has none.
+  bool nvls(std::string* why = nullptr) const {
+    int ok = 0;
+    std::size_t len = 0;
+    check(bcl_comm_nvls(comms_.front(), &ok, nullptr, 0, &len));
+    if (why != nullptr) {
+      std::string s(len, '\0');
+      check(bcl_comm_nvls(comms_.front(), &ok, s.data(), len, &len));
+      s.resize(len ? len - 1 : 0);
+      *why = s;
+    }
+    return ok != 0;
   }
   // run_bcast (runtime.hpp:140-143) over device buffers; wall seconds.
   double run_bcast(int root, const std::vector<void*>& device_bufs, std::uint64_t bytes,

@@ -81,6 +81,18 @@ int main(int argc, char** argv) {
       for (int r = 0; r < n; ++r) EXPECT(host[r] == host[3]);
     }
     g.set_protocol(0);
+    // one GPU: no NVLS team, and forcing the protocol fails loudly (invalid_argument)
+    std::string why;
+    EXPECT(!g.nvls(&why) && !why.empty());
+    g.set_protocol(5);
+    bool threw = false;
+    try {
+      (void)g.run_bcast_host(0, ptrs, m, &cfg);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    EXPECT(threw);
+    g.set_protocol(0);
     std::printf("gpu ok (%.1f us wall)\n", w * 1e6);
   }
   std::printf("consumer ok\n");
