@@ -301,6 +301,12 @@ HOST_RESET_NOTE = ("receivers' host buffers zeroed before every step by a D2H co
                    "DMA then pays for (raw 192 MiB D2H 4.75 vs 3.55 ms, profiles/round2/n1/e2e_probe4.log)")
 
 
+CPU_READ_NOTE = ("value: receivers' host bytes verified every step by DMA-ing them back and comparing on the "
+                 "GPU; cpu_read_between_calls_ms: the same calls when the CPU reads the receivers' pages "
+                 "between calls (verification on the CPU), which leaves them in the CPU caches and slows "
+                 "the next D2H into them by ~2 ms (profiles/round2/n1/e2e_probe6.log)")
+
+
 def host_reset(host, zeros):
     """Zero a pinned host buffer by DMA (see HOST_RESET_NOTE)."""
     host.copy_(zeros[:host.numel()])
@@ -386,17 +392,28 @@ def bench_single(args, torch):
     hosts = [torch.empty(m, dtype=torch.uint8, pin_memory=True) for _ in range(n)]
     hosts[0].copy_(bufs[0].cpu())
     zeros = torch.zeros(m, dtype=torch.uint8, device=dev)
-    e2e = []
-    for it in range(args.warmup + max(3, args.steps // 2)):
-        for r in range(1, n):
-            host_reset(hosts[r], zeros)
-        w = B.run_bcast_host(comms, 0, hosts, m, cfg)
-        for r in range(1, n):  # verify before recording
-            if not torch.equal(hosts[r], hosts[0]):
-                raise RuntimeError("e2e verification failed")
-        if it >= args.warmup:
-            e2e.append(w)
+    check = torch.empty(m, dtype=torch.uint8, device=dev)
+
+    def e2e_loop(iters, cpu_verify):
+        ts = []
+        for it in range(iters):
+            for r in range(1, n):
+                host_reset(hosts[r], zeros)
+            w = B.run_bcast_host(comms, 0, hosts, m, cfg)
+            for r in range(1, n):  # verify before recording
+                if cpu_verify:
+                    ok = torch.equal(hosts[r], hosts[0])
+                else:
+                    check.copy_(hosts[r])  # the host bytes, DMA'd back and compared on the GPU
+                    ok = torch.equal(check, bufs[0])
+                if not ok:
+                    raise RuntimeError("e2e verification failed")
+            ts.append(w)
+        return ts
+
+    e2e = e2e_loop(args.warmup + max(3, args.steps // 2), False)[args.warmup:]
     e2e_t = statistics.mean(e2e)
+    warm = e2e_loop(2 + max(3, args.steps // 4), True)[2:]  # receivers' pages read by the CPU between calls
 
     cpu = reference_cpu(n, m, chunk, args.cpu_iters)
     line = {
@@ -418,7 +435,9 @@ def bench_single(args, torch):
                          "kind": cpu["kind"], "sample": cpu["sample"]},
         "e2e": {"value": round(m / e2e_t / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": m,
                 "d2h_bytes_per_step": (n - 1) * m, "latency_ms": round(e2e_t * 1e3, 3),
-                "path": "bcl_run_bcast_host (C-ABI), pinned host buffers", "reset": HOST_RESET_NOTE},
+                "path": "bcl_run_bcast_host (C-ABI), pinned host buffers", "reset": HOST_RESET_NOTE,
+                "cpu_read_between_calls_ms": round(statistics.mean(warm) * 1e3, 3),
+                "cpu_read_note": CPU_READ_NOTE},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
@@ -524,6 +543,7 @@ def bench_multi(args, torch, rank, world):
     ref_host = ref_all[:m].cpu()
     e2e = []
     zeros = torch.zeros(m, dtype=torch.uint8, device=dev)
+    chk = torch.empty(m, dtype=torch.uint8, device=dev)
     for it in range(args.warmup + max(3, args.steps // 2)):
         if rank == 0:
             host.copy_(ref_host)
@@ -534,7 +554,8 @@ def bench_multi(args, torch, rank, world):
         comm.bcast_host(host, m, "uint8", 0, cfg, stream=stream)
         stream.synchronize()
         w = time.perf_counter() - t0
-        if not torch.equal(host, ref_host):
+        chk.copy_(host)  # the host bytes, DMA'd back and compared on the GPU (CPU_READ_NOTE)
+        if not torch.equal(chk, ref_all[:m]):
             raise RuntimeError("e2e verification failed")
         wt = torch.tensor([w], dtype=torch.float64, device=dev)
         dist.all_reduce(wt, op=dist.ReduceOp.MAX)

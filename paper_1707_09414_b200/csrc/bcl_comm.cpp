@@ -1229,10 +1229,16 @@ struct Piece {
   std::uint64_t off, len;
 };
 
+// Pieces grow geometrically from 1 MiB up to `piece`: the first D2H can start
+// after a small H2D + broadcast, later pieces amortise per-copy overheads.
 std::vector<Piece> pieces_of(std::uint64_t bytes, std::uint64_t piece) {
   std::vector<Piece> v;
   if (bytes == 0) return {Piece{0, 0}};
-  for (std::uint64_t off = 0; off < bytes; off += piece) v.push_back(Piece{off, std::min(piece, bytes - off)});
+  std::uint64_t cur = std::min<std::uint64_t>(piece, 1ull << 20);
+  for (std::uint64_t off = 0; off < bytes; off += cur) {
+    if (off > 0) cur = std::min(piece, cur * 2);
+    v.push_back(Piece{off, std::min(cur, bytes - off)});
+  }
   return v;
 }
 
