@@ -271,6 +271,8 @@ def main():
     ap.add_argument("--workload", default="config1", choices=["config1", "vgg16", "alexnet", "resnet50", "lenet"],
                     help="config1 (default) or a layer-wise parameter broadcast (BASELINE configs 4/5)")
     ap.add_argument("--bucket", type=int, default=0, help="parameter workloads: coalesce tensors into >= this")
+    ap.add_argument("--fused", action="store_true",
+                    help="parameter workloads: issue the per-tensor broadcasts inside one bcl_group_start/end")
     ap.add_argument("--csv", default=None, help="N>1: write the sweep as the reference bench CSV here")
     ap.add_argument("--fixed-chunk", dest="tuned", action="store_false",
                     help="N>1: pipelined chain with --chunk instead of the tuned selection")
@@ -685,7 +687,7 @@ def bench_params(args, torch, rank, world):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
-    pb = ParamBroadcaster(MODELS[args.workload], bucket_bytes=args.bucket)
+    pb = ParamBroadcaster(MODELS[args.workload], bucket_bytes=args.bucket, fused=args.fused)
     comm = B.Comm.connect_torch(world, rank, local, heap_bytes=pb.total_bytes + (16 << 20), timeout_s=30)
     flat = torch.as_tensor(DevicePtr(comm.alloc(pb.total_bytes), pb.total_bytes), device=dev)
     g = torch.Generator(device=dev).manual_seed(2)
@@ -696,6 +698,7 @@ def bench_params(args, torch, rank, world):
     torch.cuda.synchronize()
     roots = [0] if args.workload == "vgg16" else [world - 1, world // 2]
     results = {}
+    launches_total = 0
     for root in roots:
         for impl in ("ours", "nccl"):
             def prepare(it):
@@ -718,8 +721,11 @@ def bench_params(args, torch, rank, world):
             def verify(it):
                 return all(torch.equal(flat[o:o + n], ref[o:o + n]) for o, n in zip(pb.offsets, pb.sizes))
 
+            l0 = comm.launches
             times = time_steps(torch, args.steps, args.warmup, prepare, body, verify, stream,
                                align=lambda: comm.barrier(stream))
+            if impl == "ours":  # our kernels in the timed steps (the barrier kernels excluded)
+                launches_total += (comm.launches - l0) * args.steps // (args.steps + args.warmup)
             t = torch.tensor(times, dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             results[(root, impl)] = statistics.mean(t.cpu().tolist())
@@ -732,13 +738,14 @@ def bench_params(args, torch, rank, world):
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32 (moved as bytes)",
                 "data": "synthetic parameters (random bytes), torchvision layer shapes",
                 "config": {"workload": f"{args.workload}: {len(pb.sizes)} tensors, {sum(pb.sizes)} bytes, "
-                                       f"{len(pb.msgs)} broadcasts per iteration (bucket {args.bucket} B), roots {roots}",
+                                       f"{len(pb.msgs)} broadcasts per iteration (bucket {args.bucket} B"
+                                       f"{', grouped: bcl_group_start/end' if args.fused else ''}), roots {roots}",
                            "tensors": len(pb.sizes), "bytes": sum(pb.sizes), "messages": len(pb.msgs)},
                 "per_root_ms": {str(r): {"ours": round(results[(r, 'ours')] * 1e3, 4),
                                          "nccl": round(results[(r, 'nccl')] * 1e3, 4)} for r in roots},
                 "nccl_ms": round(nccl * 1e3, 4),
                 "link_bound_ms": round(sum(pb.sizes) / LINK_BW * 1e3, 4),
-                "gpu_launches": len(pb.msgs) * args.steps}
+                "gpu_launches": launches_total}
         print(json.dumps(line), flush=True)
     dist.barrier(device_ids=[local])
     nccl_direct.close()

@@ -253,6 +253,19 @@ bcl_status_t bcl_comm_path(bcl_comm_t c, const bcl_config_t* config, int root, u
  * above ll_chain_max, 4 above ll128_max or when ranks share a GPU without the
  * ll128=1 option, 5 when the communicator has no multicast team. */
 bcl_status_t bcl_comm_set_protocol(bcl_comm_t c, int protocol);
+/* Group fusion (NCCL-style ncclGroupStart/End; per calling thread, nestable).
+ * bcl_bcast / bcl_bcast_all calls issued between start and end are deferred;
+ * at the outermost end, runs of consecutive calls on one communicator that take
+ * the same line protocol (LL `direct`, LL or LL128 chain) with the same root
+ * and stream are fused into one kernel launch carrying up to 32 messages (8
+ * when ranks share a GPU), everything else launches as usual, in call order.
+ * Every rank must issue the same calls between the same start/end (MPI
+ * semantics); host-buffer and synchronous run_bcast calls cannot be grouped
+ * (BCL_ERR_INVALID_ARGUMENT). The paper's caller broadcasts every layer of a
+ * model (configs 4/5): grouped, ResNet-50's 161 per-tensor broadcasts run in
+ * ~10 launches. New on B200; no reference counterpart. */
+bcl_status_t bcl_group_start(void);
+bcl_status_t bcl_group_end(void);
 /* NVLS multicast team of this communicator: *available 1/0 and, when 0, why
  * (text, *len = bytes needed incl. NUL). Every rank agrees at init/connect.
  * New on B200; no reference counterpart. */

@@ -21,4 +21,4 @@ from ._lib import (  # noqa: F401
     select, load_table, load_table_text, save_table, save_table_text, builtin_table,
     DTYPES,
 )
-from .comm import Comm, run_bcast, run_bcast_host, bcast_all, barrier_all, DevicePtr  # noqa: F401
+from .comm import Comm, run_bcast, run_bcast_host, bcast_all, barrier_all, DevicePtr, group  # noqa: F401

@@ -115,6 +115,8 @@ _SIGS = {
     "bcl_comm_set_table": (C.c_int, [C.c_void_p, C.c_void_p]),
     "bcl_comm_choose": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(_Config)]),
     "bcl_comm_set_protocol": (C.c_int, [C.c_void_p, C.c_int]),
+    "bcl_group_start": (C.c_int, []),
+    "bcl_group_end": (C.c_int, []),
     "bcl_comm_nvls": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "bcl_comm_path": (C.c_int, [C.c_void_p, C.POINTER(_Config), C.c_int, C.c_uint64, C.c_char_p, C.c_size_t,
                                 C.POINTER(C.c_size_t)]),

@@ -234,6 +234,22 @@ class Comm:
         _check(lib().bcl_comm_set_provenance(self._h, C.c_void_p(_ptr(counters))))
 
 
+class group:
+    """``with group(): ...`` -- bcl_group_start/end (NCCL-style fusion): the
+    broadcasts issued inside are deferred and, at the end, consecutive ones on
+    the same line protocol, root and stream are fused into one launch."""
+
+    def __enter__(self):
+        _check(lib().bcl_group_start())
+        return self
+
+    def __exit__(self, exc_type, exc, tb):
+        status = lib().bcl_group_end()
+        if exc_type is None:
+            _check(status)
+        return False
+
+
 def exchange_blobs(blob: bytes, group=None) -> List[bytes]:
     """All-gather one opaque blob per rank (ordered by rank) over an
     initialised torch.distributed group (any backend; plumbing only)."""

@@ -516,6 +516,14 @@ bcl_status_t bcl_comm_path(bcl_comm_t c, const bcl_config_t* config, int root, u
   });
 }
 
+bcl_status_t bcl_group_start(void) {
+  return guard([&] { bcl::Group::group_start(); });
+}
+
+bcl_status_t bcl_group_end(void) {
+  return guard([&] { bcl::Group::group_end(); });
+}
+
 bcl_status_t bcl_comm_nvls(bcl_comm_t c, int* available, char* reason, size_t cap, size_t* len) {
   return guard([&] {
     need(c, "comm");

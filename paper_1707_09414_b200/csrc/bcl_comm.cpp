@@ -7,12 +7,17 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <sstream>
 #include <unistd.h>
 
 namespace bcl {
 
 namespace {
+
+// bcl_group_start/end nesting depth and the groups with deferred calls (per thread).
+thread_local int g_group_depth = 0;
+thread_local std::vector<Group*> g_group_touched;
 
 constexpr std::uint32_t kInfoMagic = 0xB200BC57u;
 
@@ -701,6 +706,8 @@ void Group::setup_nvls_ipc(const std::vector<std::vector<std::uint8_t>>& infos,
 }
 
 Group::~Group() {
+  // (A group destroyed between bcl_group_start and _end drops its deferred calls.)
+  std::erase(g_group_touched, this);
   for (LocalRank& r : local_) {
     cudaSetDevice(r.device);
     cudaDeviceSynchronize();
@@ -1034,14 +1041,39 @@ void Group::fill_rank_work(dev::RankWork& w, LocalRank& r, const CallPlan& p, vo
 
 void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& bufs, std::uint64_t bytes,
                       int root, cudaStream_t stream, int mode) {
+  launch_ll_segs(locals, {bufs}, {bytes}, root, stream, mode);
+}
+
+std::uint64_t Group::ll_lines_of(std::uint64_t bytes, int mode) {
+  return mode == 2 ? (bytes + dev::kLL128Payload - 1) / dev::kLL128Payload : (bytes + 7) / 8;
+}
+
+// One launch of a line protocol carrying one or more messages (segments):
+// seg_bufs[s][i] is local rank i's buffer of message s.
+void Group::launch_ll_segs(const std::vector<int>& locals, const std::vector<std::vector<void*>>& seg_bufs,
+                           const std::vector<std::uint64_t>& seg_bytes, int root, cudaStream_t stream, int mode) {
   const bool chain = mode != 0;
   dev::LLParams P{};
   P.n_ranks = n_;
   P.root = root;
   P.n_local = static_cast<int>(locals.size());
-  P.bytes = bytes;
-  P.lines = static_cast<std::uint32_t>(mode == 2 ? (bytes + dev::kLL128Payload - 1) / dev::kLL128Payload
-                                                  : (bytes + 7) / 8);
+  P.n_seg = static_cast<int>(seg_bytes.size());
+  if (P.n_seg < 1 || P.n_seg > dev::max_segs(P.n_local)) {
+    throw std::invalid_argument("line-protocol launch: too many messages");
+  }
+  std::uint64_t lines = 0;
+  for (int s = 0; s < P.n_seg; ++s) {
+    P.seg_line[s] = static_cast<std::uint32_t>(lines);
+    P.seg_bytes[s] = seg_bytes[static_cast<std::size_t>(s)];
+    lines += ll_lines_of(seg_bytes[static_cast<std::size_t>(s)], mode);
+    for (std::size_t i = 0; i < locals.size(); ++i) {
+      P.seg_buf[i][s] = static_cast<std::uint8_t*>(seg_bufs[static_cast<std::size_t>(s)][i]);
+    }
+  }
+  if (lines >= (1ull << 31)) throw std::invalid_argument("line-protocol launch too large");
+  P.seg_line[P.n_seg] = static_cast<std::uint32_t>(lines);
+  P.bytes = seg_bytes.front();
+  P.lines = static_cast<std::uint32_t>(lines);
   P.area_lines = static_cast<std::uint32_t>(ll_max_ / 8);
   P.chain = static_cast<std::uint32_t>(mode);
   P.chain_lines = static_cast<std::uint32_t>(ll_chain_max_ / 8);
@@ -1071,7 +1103,7 @@ void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& 
     if (e != epoch) throw std::runtime_error("ranks sharing a GPU drifted apart in call count");
     dev::LLRank& w = P.ranks[i];
     w.rank = r.rank;
-    w.buf = static_cast<std::uint8_t*>(bufs[i]);
+    w.buf = static_cast<std::uint8_t*>(seg_bufs.front()[i]);
     w.credit = r.region + 4 * S + static_cast<std::size_t>(n_) + 1 + (chain ? static_cast<std::size_t>(n_) + 1 : 0);
     w.wcredit = r.region + 4 * S + 3 * static_cast<std::size_t>(n_) + 2;
     w.ll = reinterpret_cast<uint4*>(r.region + ll_offset(lanes_));
@@ -1192,6 +1224,7 @@ void Group::bcast(int li, void* buf, std::uint64_t bytes, int root, const Algori
   const AlgorithmConfig c = choose(bytes, cfg);
   const CallPlan p = plan(c, root, bytes);
   if (n_ == 1) return;  // nothing moves (reference: n = 1 leaves the buffer untouched)
+  if (defer(Deferred{false, li, {buf}, bytes, root, p, {stream}})) return;
   launch_group({li}, {buf}, bytes, root, p, stream);
 }
 
@@ -1209,13 +1242,137 @@ void Group::bcast_all(const std::vector<void*>& bufs, std::uint64_t bytes, int r
   const AlgorithmConfig c = choose(bytes, cfg);
   const CallPlan p = plan(c, root, bytes);
   if (n_ == 1) return;
+  std::vector<cudaStream_t> per;  // per device, first rank's stream
+  for (const auto& kv : by_device_) {
+    const int first = kv.second.front();
+    per.push_back(streams.empty() ? local_[static_cast<std::size_t>(first)].stream
+                                  : streams[static_cast<std::size_t>(first)]);
+  }
+  if (defer(Deferred{true, -1, bufs, bytes, root, p, per})) return;
+  std::size_t d = 0;
   for (const auto& kv : by_device_) {
     std::vector<void*> b;
     for (int li : kv.second) b.push_back(bufs[static_cast<std::size_t>(li)]);
-    const int first = kv.second.front();
-    cudaStream_t s = streams.empty() ? local_[static_cast<std::size_t>(first)].stream
-                                     : streams[static_cast<std::size_t>(first)];
-    launch_group(kv.second, b, bytes, root, p, s);
+    launch_group(kv.second, b, bytes, root, p, per[d++]);
+  }
+}
+
+// ------------------------------------------------------------- group fusion
+//
+// bcl_group_start/end (NCCL-style): broadcasts issued in between are
+// deferred; at the end, runs of consecutive calls that take the same line
+// protocol (LL direct, LL chain, LL128 chain) with the same root and stream
+// are fused into one launch carrying up to 32 messages (segments), the rest
+// launch as usual, in order. Every rank sees the same call sequence, so every
+// rank fuses identically (the fused launch is one call epoch everywhere).
+
+void Group::group_start() { ++g_group_depth; }
+
+void Group::group_end() {
+  if (g_group_depth <= 0) throw std::invalid_argument("group_end without group_start");
+  if (--g_group_depth > 0) return;
+  std::vector<Group*> touched;
+  touched.swap(g_group_touched);
+  std::exception_ptr first;
+  for (Group* g : touched) {
+    try {
+      g->flush_deferred();
+    } catch (...) {
+      if (!first) first = std::current_exception();
+    }
+  }
+  if (first) std::rethrow_exception(first);
+}
+
+bool Group::in_group() { return g_group_depth > 0; }
+
+bool Group::defer(Deferred d) {
+  if (g_group_depth <= 0) return false;
+  if (deferred_.empty()) g_group_touched.push_back(this);
+  deferred_.push_back(std::move(d));
+  return true;
+}
+
+// The line protocol a call takes (1 LL direct, 2 LL chain, 3 LL128 chain),
+// or 0 when it cannot be fused -- the decisions of launch_group.
+int Group::fuse_kind(const Deferred& d) {
+  const CallPlan& p = d.plan;
+  std::vector<int> locals;
+  if (d.all) {
+    for (int i = 0; i < local_count(); ++i) locals.push_back(i);
+  } else {
+    locals.push_back(d.li);
+  }
+  if (use_nvls(p, d.bytes)) return 0;
+  if (p.config.algorithm == Algorithm::Direct && d.bytes <= ll_max_ && opt_.ll) return 1;
+  const int mode = ll_chain_mode(p, d.bytes, locals);
+  if (mode == 1) return 2;
+  if (mode == 2) {
+    for (const auto& kv : by_device_) {
+      if (kv.second.size() > 1) return 0;  // no fused LL128 for ranks sharing a GPU
+    }
+    return 3;
+  }
+  return 0;
+}
+
+void Group::flush_deferred() {
+  std::vector<Deferred> calls;
+  calls.swap(deferred_);
+  std::size_t i = 0;
+  while (i < calls.size()) {
+    const Deferred& d = calls[i];
+    const int kind = fuse_kind(d);
+    // Extend the run: same kind, root, shape and streams; within the segment
+    // and landing-area caps.
+    std::size_t j = i + 1;
+    if (kind != 0) {
+      int per_dev = 1;
+      for (const auto& kv : by_device_) per_dev = std::max(per_dev, static_cast<int>(kv.second.size()));
+      const std::size_t max_segs = static_cast<std::size_t>(dev::max_segs(d.all ? per_dev : 1));
+      const std::uint64_t cap = kind == 1 ? ll_max_ / 8 : kind == 2 ? ll_chain_max_ / 8 : (1ull << 31) - 1;
+      std::uint64_t lines = ll_lines_of(d.bytes, kind - 1);
+      while (j < calls.size() && j - i < max_segs) {
+        const Deferred& e = calls[j];
+        if (e.all != d.all || e.li != d.li || e.root != d.root || e.streams != d.streams || fuse_kind(e) != kind) break;
+        const std::uint64_t more = ll_lines_of(e.bytes, kind - 1);
+        if (lines + more > cap) break;
+        lines += more;
+        ++j;
+      }
+    }
+    if (j == i + 1) {  // a lone call: exactly what the call would have done
+      if (d.all) {
+        std::size_t k = 0;
+        for (const auto& kv : by_device_) {
+          std::vector<void*> b;
+          for (int li : kv.second) b.push_back(d.bufs[static_cast<std::size_t>(li)]);
+          launch_group(kv.second, b, d.bytes, d.root, d.plan, d.streams[k++]);
+        }
+      } else {
+        launch_group({d.li}, d.bufs, d.bytes, d.root, d.plan, d.streams.front());
+      }
+    } else {
+      std::vector<std::uint64_t> seg_bytes;
+      for (std::size_t k = i; k < j; ++k) seg_bytes.push_back(calls[k].bytes);
+      if (d.all) {
+        std::size_t k = 0;
+        for (const auto& kv : by_device_) {
+          std::vector<std::vector<void*>> seg_bufs;
+          for (std::size_t c = i; c < j; ++c) {
+            std::vector<void*> b;
+            for (int li : kv.second) b.push_back(calls[c].bufs[static_cast<std::size_t>(li)]);
+            seg_bufs.push_back(std::move(b));
+          }
+          launch_ll_segs(kv.second, seg_bufs, seg_bytes, d.root, d.streams[k++], kind - 1);
+        }
+      } else {
+        std::vector<std::vector<void*>> seg_bufs;
+        for (std::size_t c = i; c < j; ++c) seg_bufs.push_back({calls[c].bufs.front()});
+        launch_ll_segs({d.li}, seg_bufs, seg_bytes, d.root, d.streams.front(), kind - 1);
+      }
+    }
+    i = j;
   }
 }
 
@@ -1275,6 +1432,7 @@ void Group::ensure_scratch(int li, std::uint64_t bytes) {
 
 void Group::bcast_host(int li, void* host_buf, std::uint64_t bytes, int root,
                        const AlgorithmConfig* cfg, cudaStream_t stream) {
+  if (in_group()) throw std::invalid_argument("host-buffer broadcasts cannot be grouped");
   LocalRank& r = local_.at(static_cast<std::size_t>(li));
   if (root < 0 || root >= n_) throw std::invalid_argument("root out of range");
   if (bytes > 0 && host_buf == nullptr) throw std::invalid_argument("null buffer");
@@ -1328,6 +1486,7 @@ void Group::check(int li, cudaStream_t stream) {
 
 double Group::run_bcast(const std::vector<void*>& bufs, std::uint64_t bytes, int root,
                         const AlgorithmConfig* cfg) {
+  if (in_group()) throw std::invalid_argument("run_bcast is synchronous and cannot be grouped");
   if (static_cast<int>(bufs.size()) != n_ || local_count() != n_) {
     throw std::invalid_argument("one buffer per rank required");
   }
@@ -1354,6 +1513,7 @@ double Group::run_bcast(const std::vector<void*>& bufs, std::uint64_t bytes, int
 
 double Group::run_bcast_host(const std::vector<void*>& host_bufs, std::uint64_t bytes, int root,
                              const AlgorithmConfig* cfg) {
+  if (in_group()) throw std::invalid_argument("run_bcast_host is synchronous and cannot be grouped");
   if (static_cast<int>(host_bufs.size()) != n_ || local_count() != n_) {
     throw std::invalid_argument("one buffer per rank required");
   }

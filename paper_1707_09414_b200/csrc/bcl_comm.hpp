@@ -240,12 +240,31 @@ class Group {
   void barrier_all(const std::vector<cudaStream_t>& streams);
   // Synchronizes `stream` (or the device) and raises the first device error.
   void check(int local_index, cudaStream_t stream);
+  // Group fusion (bcl_group_start / bcl_group_end, per thread, nestable):
+  // broadcasts issued in between are deferred and fused at the end.
+  static void group_start();
+  static void group_end();
+  static bool in_group();
+
   void set_provenance(int local_index, unsigned long long* counters);
   void set_trace(int local_index, unsigned long long* records, std::uint32_t per_lane);
   std::uint64_t launches(int local_index) const;
 
  private:
   Group() = default;
+  struct Deferred {
+    bool all;                           // bcast_all (every local rank) or bcast (rank li)
+    int li;
+    std::vector<void*> bufs;            // bcast_all: one per local rank
+    std::uint64_t bytes;
+    int root;
+    CallPlan plan;
+    std::vector<cudaStream_t> streams;  // bcast_all: one per device (by_device_ order)
+  };
+  bool defer(Deferred d);
+  int fuse_kind(const Deferred& d);
+  void flush_deferred();
+  std::vector<Deferred> deferred_;
   void alloc_rank(LocalRank& r, std::size_t heap_bytes);
   void upload_peers(LocalRank& r);
   void cache_device_limits(int device);
@@ -263,6 +282,9 @@ class Group {
   void ensure_scratch(int local_index, std::uint64_t bytes);
   void launch_ll(const std::vector<int>& locals, const std::vector<void*>& bufs, std::uint64_t bytes, int root,
                  cudaStream_t stream, int mode);
+  void launch_ll_segs(const std::vector<int>& locals, const std::vector<std::vector<void*>>& seg_bufs,
+                      const std::vector<std::uint64_t>& seg_bytes, int root, cudaStream_t stream, int mode);
+  static std::uint64_t ll_lines_of(std::uint64_t bytes, int mode);
   void raise_errors(const std::vector<int>& locals);
   int ll_chain_mode(const CallPlan& p, std::uint64_t bytes, const std::vector<int>& locals) const;
   bool use_local_chain(const CallPlan& p, const std::vector<int>& locals) const;

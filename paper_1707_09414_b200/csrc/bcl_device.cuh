@@ -155,14 +155,13 @@ struct LLRank {
   unsigned long long done_target;  // receiver: value of *done once every CTA of this call finished
 };
 
-template <int NL>
-struct LLParamsT {
+struct LLHeader {
   int n_ranks;
   int root;
   int n_local;
   int ctas;                   // CTAs per rank
-  std::uint32_t lines;
-  std::uint64_t bytes;
+  std::uint32_t lines;        // lines of the launch (every segment's)
+  std::uint64_t bytes;        // one segment: its bytes
   std::uint64_t epoch;
   std::uint32_t half;
   std::uint32_t area_lines;   // lines per (source, half) landing area of the direct schedule
@@ -172,9 +171,24 @@ struct LLParamsT {
   std::uint32_t chain128_area;   // its offset from the LL base in 16-byte units (128-byte aligned)
   std::uint64_t timeout_ns;
   std::uint32_t coop;            // LL128, one rank per GPU: cooperative launch (co-residency guaranteed)
-  LLRank ranks[NL];
+  int n_seg;                     // messages fused into this launch (bcl_group_*); 1 = an ordinary call
 };
-using LLParams = LLParamsT<kMaxLocal>;
+
+// A launch of the line protocols may carry up to NS messages ("segments",
+// fused by bcl_group_start/end): segment s owns lines [seg_line[s],
+// seg_line[s + 1]) and its own buffer on every rank. NS = 1 is an ordinary
+// call (the segment is R.buf / bytes; the tables stay unused).
+constexpr int kMaxSegs = 32;        // one rank per launch
+constexpr int kMaxSegsShared = 8;   // ranks sharing a GPU (a 16-rank parameter block; no spills)
+constexpr int max_segs(int n_local) { return n_local > 1 ? kMaxSegsShared : kMaxSegs; }
+template <int NL, int NS = 1>
+struct LLParamsT : LLHeader {
+  std::uint32_t seg_line[NS + 1];
+  std::uint64_t seg_bytes[NS];
+  LLRank ranks[NL];
+  std::uint8_t* seg_buf[NL][NS];
+};
+using LLParams = LLParamsT<kMaxLocal, kMaxSegs>;  // host-side superset; launchers copy into the smallest fit
 
 // Every rank of the group on this GPU (one process): the pipelined chain's
 // hops run as one flag-free kernel. Each warp takes byte ranges ("items") of

@@ -944,9 +944,32 @@ __device__ void ll_fail(const LLRank& R, int peer, std::uint64_t line, std::uint
 // each line's payload out and forwards the very same line to l + 1, so the
 // hops overlap line by line with no fence and no flag round trip. Writers
 // first wait for their targets' credits for the half they are about to reuse.
-template <int NL>
-__global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ LLParamsT<NL> P) {
-  const LLRank& R = P.ranks[NL == 1 ? 0 : static_cast<int>(blockIdx.x) / P.ctas];
+// The message ("segment") a line belongs to: its first line, this rank's
+// buffer and its bytes. One segment for an ordinary call; a binary search of
+// the launch's segment table for a fused group (bcl_group_start/end).
+struct LineSeg {
+  std::uint32_t line0;
+  std::uint8_t* buf;
+  std::uint64_t bytes;
+};
+template <int NL, int NS>
+__device__ __forceinline__ LineSeg seg_of(const LLParamsT<NL, NS>& P, int li, std::uint32_t line) {
+  if constexpr (NS == 1) {
+    return LineSeg{0, P.ranks[li].buf, P.bytes};
+  } else {
+    int lo = 0, hi = P.n_seg - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (P.seg_line[mid] <= line) lo = mid; else hi = mid - 1;
+    }
+    return LineSeg{P.seg_line[lo], P.seg_buf[li][lo], P.seg_bytes[lo]};
+  }
+}
+
+template <int NL, int NS>
+__global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ LLParamsT<NL, NS> P) {
+  const int li = NL == 1 ? 0 : static_cast<int>(blockIdx.x) / P.ctas;
+  const LLRank& R = P.ranks[li];
   const std::uint32_t cta = NL == 1 ? blockIdx.x : blockIdx.x % P.ctas;
   const std::uint32_t first = cta * blockDim.x + threadIdx.x;
   const std::uint32_t stride = static_cast<std::uint32_t>(P.ctas) * blockDim.x;
@@ -977,17 +1000,18 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ 
     __syncthreads();
   }
   if (logical == 0) {
-    const bool aligned = (reinterpret_cast<std::uintptr_t>(R.buf) & 7u) == 0;
     for (std::uint32_t i = first; i < P.lines; i += stride) {
-      const std::uint64_t off = static_cast<std::uint64_t>(i) * 8;
+      const LineSeg sg = seg_of(P, li, i);
+      const bool aligned = (reinterpret_cast<std::uintptr_t>(sg.buf) & 7u) == 0;
+      const std::uint64_t off = static_cast<std::uint64_t>(i - sg.line0) * 8;
       std::uint32_t lo = 0, hi = 0;
-      if (aligned && off + 8 <= P.bytes) {
-        const uint2 v = *reinterpret_cast<const uint2*>(R.buf + off);
+      if (aligned && off + 8 <= sg.bytes) {
+        const uint2 v = *reinterpret_cast<const uint2*>(sg.buf + off);
         lo = v.x;
         hi = v.y;
       } else {
-        for (std::uint32_t b = 0; b < 8 && off + b < P.bytes; ++b) {
-          const std::uint32_t byte = R.buf[off + b];
+        for (std::uint32_t b = 0; b < 8 && off + b < sg.bytes; ++b) {
+          const std::uint32_t byte = sg.buf[off + b];
           if (b < 4) lo |= byte << (8 * b); else hi |= byte << (8 * (b - 4));
         }
       }
@@ -1006,7 +1030,6 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ 
   const uint4* src = R.ll + area;
   uint4* fwd = chain && writer ? R.peers->ll[next] + area : nullptr;
   const int source = chain ? (R.rank + n - 1) % n : P.root;
-  const bool aligned = (reinterpret_cast<std::uintptr_t>(R.buf) & 7u) == 0;
   bool ok = true;
   for (std::uint32_t i = first; i < P.lines && ok; i += stride) {
     uint4 v = ld_volatile_v4(src + i);
@@ -1027,12 +1050,14 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ 
       if (!ok) break;
     }
     if (fwd != nullptr) st_volatile_v4(fwd + i, v.x, v.y, v.z, v.w);
-    const std::uint64_t off = static_cast<std::uint64_t>(i) * 8;
-    if (aligned && off + 8 <= P.bytes) {
-      *reinterpret_cast<uint2*>(R.buf + off) = make_uint2(v.x, v.z);
+    const LineSeg sg = seg_of(P, li, i);
+    const bool aligned = (reinterpret_cast<std::uintptr_t>(sg.buf) & 7u) == 0;
+    const std::uint64_t off = static_cast<std::uint64_t>(i - sg.line0) * 8;
+    if (aligned && off + 8 <= sg.bytes) {
+      *reinterpret_cast<uint2*>(sg.buf + off) = make_uint2(v.x, v.z);
     } else {
-      for (std::uint32_t b = 0; b < 8 && off + b < P.bytes; ++b) {
-        R.buf[off + b] = static_cast<std::uint8_t>((b < 4 ? v.x >> (8 * b) : v.z >> (8 * (b - 4))) & 0xFFu);
+      for (std::uint32_t b = 0; b < 8 && off + b < sg.bytes; ++b) {
+        sg.buf[off + b] = static_cast<std::uint8_t>((b < 4 ? v.x >> (8 * b) : v.z >> (8 * (b - 4))) & 0xFFu);
       }
     }
   }
@@ -1088,9 +1113,10 @@ __device__ __forceinline__ void ll128_put(std::uint8_t* buf, std::uint64_t off, 
 }
 
 // NL > 1: ranks sharing one GPU (cooperative launch, P.ctas CTAs per rank).
-template <int NL>
-__global__ void __launch_bounds__(kLLThreads, 3) ll128_kernel(const __grid_constant__ LLParamsT<NL> P) {
-  const LLRank& R = P.ranks[NL == 1 ? 0 : static_cast<int>(blockIdx.x) / P.ctas];
+template <int NL, int NS>
+__global__ void __launch_bounds__(kLLThreads, 3) ll128_kernel(const __grid_constant__ LLParamsT<NL, NS> P) {
+  const int li = NL == 1 ? 0 : static_cast<int>(blockIdx.x) / P.ctas;
+  const LLRank& R = P.ranks[li];
   const std::uint32_t cta = NL == 1 ? blockIdx.x : blockIdx.x % P.ctas;
   const int lane = static_cast<int>(threadIdx.x & 31);
   const int part = lane & 7;  // 16-byte piece of the line
@@ -1116,12 +1142,13 @@ __global__ void __launch_bounds__(kLLThreads, 3) ll128_kernel(const __grid_const
     }
     __syncthreads();
   }
-  const bool aligned = (reinterpret_cast<std::uintptr_t>(R.buf) & 7u) == 0;
-  auto piece = [&](std::uint32_t line, std::uint64_t* off, std::uint32_t* len0, std::uint32_t* len1) {
+  // `line` counts from its segment's first line; `bytes` = the segment's.
+  auto piece = [&](std::uint32_t line, std::uint64_t bytes, std::uint64_t* off, std::uint32_t* len0,
+                   std::uint32_t* len1) {
     // payload bytes of this thread: [off, off + len0) -> word 0, [off + 8, ... + len1) -> word 1
     *off = static_cast<std::uint64_t>(line) * kLL128Payload + static_cast<std::uint64_t>(part) * 16;
     const std::uint64_t end = static_cast<std::uint64_t>(line) * kLL128Payload + kLL128Payload;
-    const std::uint64_t lim = end < P.bytes ? end : P.bytes;
+    const std::uint64_t lim = end < bytes ? end : bytes;
     auto clip = [&](std::uint64_t a) -> std::uint32_t { return a >= lim ? 0u : static_cast<std::uint32_t>(lim - a < 8 ? lim - a : 8); };
     *len0 = clip(*off);
     *len1 = part == 7 ? 0u : clip(*off + 8);
@@ -1174,11 +1201,13 @@ __global__ void __launch_bounds__(kLLThreads, 3) ll128_kernel(const __grid_const
       if (!room(k)) return;
       const std::uint32_t line = g * 4 + sub;
       if (line >= P.lines) continue;
+      const LineSeg sg = seg_of(P, li, line);
+      const bool aligned = (reinterpret_cast<std::uintptr_t>(sg.buf) & 7u) == 0;
       std::uint64_t off;
       std::uint32_t l0, l1;
-      piece(line, &off, &l0, &l1);
-      const unsigned long long a = ll128_get(R.buf, off, l0, aligned);
-      const unsigned long long b = part == 7 ? flag_of(k) : ll128_get(R.buf, off + 8, l1, aligned);
+      piece(line - sg.line0, sg.bytes, &off, &l0, &l1);
+      const unsigned long long a = ll128_get(sg.buf, off, l0, aligned);
+      const unsigned long long b = part == 7 ? flag_of(k) : ll128_get(sg.buf, off + 8, l1, aligned);
       st_volatile_v2u64(ring_next + at(k), a, b);
     }
     return;
@@ -1214,11 +1243,13 @@ __global__ void __launch_bounds__(kLLThreads, 3) ll128_kernel(const __grid_const
       if (active) st_volatile_v2u64(ring_next + at(k), v.x, v.y);
     }
     if (active) {
+      const LineSeg sg = seg_of(P, li, line);
+      const bool aligned = (reinterpret_cast<std::uintptr_t>(sg.buf) & 7u) == 0;
       std::uint64_t off;
       std::uint32_t l0, l1;
-      piece(line, &off, &l0, &l1);
-      ll128_put(R.buf, off, l0, aligned, v.x);
-      if (part != 7) ll128_put(R.buf, off + 8, l1, aligned, v.y);
+      piece(line - sg.line0, sg.bytes, &off, &l0, &l1);
+      ll128_put(sg.buf, off, l0, aligned, v.x);
+      if (part != 7) ll128_put(sg.buf, off + 8, l1, aligned, v.y);
     }
     if ((k + 1) % (kLL128Depth / 2) == 0) {
       // Every lane's loads of these groups have returned (their values were
@@ -1357,7 +1388,7 @@ int local_chain_occupancy(int* blocks_per_sm) {
 
 int ll128_occupancy(int* blocks_per_sm) {
   return static_cast<int>(
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, dev::ll128_kernel<1>, dev::kLLThreads, 0));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, dev::ll128_kernel<1, 1>, dev::kLLThreads, 0));
 }
 
 int launch_local_chain(const dev::LocalChainParams& p, int ctas, void* stream) {
@@ -1378,6 +1409,31 @@ int launch_barrier(const dev::BarrierParams& p, void* stream) {
   return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::barrier_kernel, p));
 }
 
+namespace {
+
+// Copy the host-side superset into the smallest parameter block that holds
+// the launch (NL local ranks, NS segments).
+template <int NL, int NS>
+int launch_ll_as(cudaLaunchConfig_t& cfg, const dev::LLParams& p) {
+  dev::LLParamsT<NL, NS> q;
+  static_cast<dev::LLHeader&>(q) = p;
+  for (int s = 0; s <= NS && s <= p.n_seg; ++s) q.seg_line[s] = p.seg_line[s];
+  for (int s = 0; s < NS && s < p.n_seg; ++s) q.seg_bytes[s] = p.seg_bytes[s];
+  for (int i = 0; i < p.n_local; ++i) {
+    q.ranks[i] = p.ranks[i];
+    for (int s = 0; s < NS && s < p.n_seg; ++s) q.seg_buf[i][s] = p.seg_buf[i][s];
+  }
+  if (p.chain == 2) {
+    // (LL128 groups are not fused for ranks sharing a GPU: the 16-rank fused
+    // block would spill at LL128's 42-register budget; the host never asks.)
+    if constexpr (NL > 1 && NS > 1) return static_cast<int>(cudaErrorInvalidValue);
+    else return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::ll128_kernel<NL, NS>, q));
+  }
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::ll_kernel<NL, NS>, q));
+}
+
+}  // namespace
+
 int launch_ll(const dev::LLParams& p, void* stream) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(p.n_local * p.ctas));
@@ -1390,15 +1446,10 @@ int launch_ll(const dev::LLParams& p, void* stream) {
   attr[0].val.cooperative = (p.n_local > 1 || (p.chain == 2 && p.coop)) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (p.n_local == 1) {
-    dev::LLParamsT<1> one;
-    std::memcpy(&one, &p, offsetof(dev::LLParams, ranks));
-    one.ranks[0] = p.ranks[0];
-    if (p.chain == 2) return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::ll128_kernel<1>, one));
-    return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::ll_kernel<1>, one));
-  }
-  if (p.chain == 2) return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::ll128_kernel<dev::kMaxLocal>, p));
-  return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::ll_kernel<dev::kMaxLocal>, p));
+  if (p.n_seg < 1 || p.n_seg > dev::max_segs(p.n_local)) return static_cast<int>(cudaErrorInvalidValue);
+  const bool fused = p.n_seg > 1;
+  if (p.n_local == 1) return fused ? launch_ll_as<1, dev::kMaxSegs>(cfg, p) : launch_ll_as<1, 1>(cfg, p);
+  return fused ? launch_ll_as<dev::kMaxLocal, dev::kMaxSegsShared>(cfg, p) : launch_ll_as<dev::kMaxLocal, 1>(cfg, p);
 }
 
 int bcast_kernel_occupancy(int* blocks_per_sm, std::size_t smem) {

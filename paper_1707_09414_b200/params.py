@@ -10,7 +10,9 @@ BASELINE.json use it with the sizes in `workloads.MODELS`.
 """
 from typing import List, Optional, Sequence, Tuple
 
-from .comm import Comm, _ptr, bcast_all
+from contextlib import nullcontext
+
+from .comm import Comm, _ptr, bcast_all, group
 
 
 def layout(sizes: Sequence[int], align: int = 256) -> Tuple[List[int], int]:
@@ -43,9 +45,13 @@ def messages(sizes: Sequence[int], bucket_bytes: int = 0, align: int = 256) -> L
 
 
 class ParamBroadcaster:
-    """Broadcast a model's parameters (flat buffer) from `root`."""
+    """Broadcast a model's parameters (flat buffer) from `root`. With
+    `fused`, the per-tensor broadcasts are issued inside one
+    bcl_group_start/end: still one message per tensor (tuned per size), but
+    runs of small ones share a launch."""
 
-    def __init__(self, sizes: Sequence[int], bucket_bytes: int = 0):
+    def __init__(self, sizes: Sequence[int], bucket_bytes: int = 0, fused: bool = False):
+        self.fused = fused
         self.sizes = list(sizes)
         self.msgs = messages(self.sizes, bucket_bytes)
         self.offsets, self.total_bytes = layout(self.sizes)
@@ -56,12 +62,14 @@ class ParamBroadcaster:
     def bcast(self, comm: Comm, flat, root: int, stream=None, config=None) -> None:
         """Per-rank call (one process per GPU): every rank passes its own flat buffer."""
         base = _ptr(flat)
-        for off, n in self.msgs:
-            comm.bcast(base + off, n, "uint8", root, config, stream)
+        with group() if self.fused else nullcontext():
+            for off, n in self.msgs:
+                comm.bcast(base + off, n, "uint8", root, config, stream)
 
     def bcast_all(self, comms: Sequence[Comm], flats: Sequence, root: int, streams: Optional[Sequence] = None,
                   config=None) -> None:
         """All ranks of a one-process group."""
         bases = [_ptr(f) for f in flats]
-        for off, n in self.msgs:
-            bcast_all(comms, [b + off for b in bases], n, "uint8", root, config, streams)
+        with group() if self.fused else nullcontext():
+            for off, n in self.msgs:
+                bcast_all(comms, [b + off for b in bases], n, "uint8", root, config, streams)

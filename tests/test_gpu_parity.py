@@ -459,3 +459,112 @@ def test_protocol_caps_and_lane_plan():
         assert p["n_chunks"] == -(-m // chunk)
         assert p["slices"] * p["slice_bytes"] >= min(chunk, m)
         assert 1 <= p["ctas"] * 8 <= lanes
+
+
+def _grouped_round(comms, bufs, sizes, root, algo, chunk=65536, offs=None):
+    """Issue one broadcast per size inside one bcl_group_start/end; returns
+    the expected payload per message."""
+    n = len(comms)
+    expect = []
+    at = 0
+    views = []
+    for k, m in enumerate(sizes):
+        off = at + (offs[k] if offs else 0)
+        views.append([b[off:off + m] for b in bufs])
+        at = off + m + 16
+    for k, m in enumerate(sizes):
+        src = torch.randint(0, 256, (m,), dtype=torch.uint8, device=bufs[root].device)
+        for r in range(n):
+            (views[k][r].copy_(src) if r == root else views[k][r].fill_(0x3C))
+        expect.append(src)
+    torch.cuda.synchronize()
+    with B.group():
+        for k, m in enumerate(sizes):
+            B.bcast_all(comms, views[k], m, "uint8", root, cfg_of(algo, chunk))
+    torch.cuda.synchronize()
+    for k in range(len(sizes)):
+        for r in range(n):
+            assert torch.equal(views[k][r], expect[k]), (algo, sizes[k], r)
+
+
+def test_group_fuses_line_protocol_calls():
+    """bcl_group_start/end: consecutive LL direct calls (and LL chain calls
+    under protocol ll) share launches, with
+    odd sizes, misaligned views and an empty message, bit-exact (8 messages
+    per launch when ranks share a GPU: 40 in 5 launches); calls that
+    cannot fuse (the fused single-GPU chain) run as usual, in order."""
+    n = 4
+    comms = comms_for(n)
+    bufs = [torch.zeros(8 << 20, dtype=torch.uint8, device="cuda:0") for _ in range(n)]
+    rng = random.Random(71)
+    sizes = [rng.choice([1, 7, 8, 9, 255, 4096, rng.randrange(1, 100000)]) for _ in range(39)] + [0]
+    before = comms[0].launches
+    _grouped_round(comms, bufs, sizes, 2, "direct", offs=[rng.randrange(0, 8) for _ in sizes])
+    assert comms[0].launches - before == 5  # 40 messages, 8 per launch on a shared GPU
+    # mixed: direct (fusable) and chain (fused single-GPU kernel, not fusable)
+    before = comms[0].launches
+    sizes = [1000, 2000, 3000]
+    at = 0
+    views = []
+    for m in sizes + [1 << 20] + sizes:
+        views.append([b[at:at + m] for b in bufs])
+        at += m + 64
+    for r in range(n):
+        for v in views:
+            (v[r].fill_(0x11) if r == 1 else v[r].zero_())
+    torch.cuda.synchronize()
+    with B.group():
+        for k, v in enumerate(views):
+            algo = "chain_pipelined" if k == 3 else "direct"
+            B.bcast_all(comms, v, v[0].numel(), "uint8", 1, cfg_of(algo, 65536))
+    torch.cuda.synchronize()
+    assert comms[0].launches - before == 3
+    for v in views:
+        for r in range(n):
+            assert int(v[r].min()) == 0x11 == int(v[r].max())
+    for c in comms:
+        c.set_protocol("ll")
+    try:
+        before = comms[0].launches
+        _grouped_round(comms, bufs, [5, 100, 65536, 3 << 20, 17], 0, "chain_pipelined")
+        assert comms[0].launches - before == 1
+    finally:
+        for c in comms:
+            c.set_protocol("auto")
+
+
+def test_group_rules():
+    comms = comms_for(2)
+    buf = [torch.zeros(64, dtype=torch.uint8, device="cuda:0") for _ in comms]
+    with pytest.raises(ValueError):
+        B._lib._check(B.lib().bcl_group_end())  # end without start
+    with pytest.raises(ValueError):
+        with B.group():
+            B.run_bcast(comms, 0, buf, 64, cfg_of("direct"))
+    with B.group():
+        with B.group():  # nested: fused at the outermost end
+            B.bcast_all(comms, buf, 64, "uint8", 0, cfg_of("direct"))
+        B.bcast_all(comms, buf, 64, "uint8", 0, cfg_of("direct"))
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("model", ["resnet50", "lenet"])
+def test_layerwise_parameter_broadcast_fused(model):
+    """Configs 4/5 with the per-tensor broadcasts grouped: still one message
+    per tensor, far fewer launches, every tensor bit-exact."""
+    from paper_1707_09414_b200.params import ParamBroadcaster
+    from paper_1707_09414_b200.workloads import MODELS
+    n, root = 4, 1
+    pb = ParamBroadcaster(MODELS[model], fused=True)
+    comms = comms_for(n)
+    g = torch.Generator(device="cuda:0").manual_seed(7)
+    flats = [torch.zeros(pb.total_bytes, dtype=torch.uint8, device="cuda:0") for _ in range(n)]
+    flats[root].copy_(torch.randint(0, 256, (pb.total_bytes,), dtype=torch.uint8, device="cuda:0", generator=g))
+    torch.cuda.synchronize()
+    before = comms[0].launches
+    pb.bcast_all(comms, flats, root)
+    torch.cuda.synchronize()
+    assert comms[0].launches - before < len(pb)
+    for r in range(n):
+        for off, size in zip(pb.offsets, pb.sizes):
+            assert torch.equal(flats[r][off:off + size], flats[root][off:off + size]), (model, r, off)

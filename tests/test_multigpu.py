@@ -268,3 +268,55 @@ def test_one_process_per_gpu_over_ipc():
         p.join(timeout=60)
     for rank, ok, err in res:
         assert ok, (rank, err)
+
+
+@needs2
+def test_group_fusion_across_gpus():
+    """bcl_group_start/end across GPUs: runs of LL128 chain calls and of LL
+    direct calls fuse into shared launches (odd sizes, every root), calls on
+    the lane executor stay separate, everything bit-exact and in order."""
+    devices = list(range(min(ngpu(), 8)))
+    n = len(devices)
+    comms = B.Comm.local(devices, timeout_s=10)
+    rng = random.Random(83)
+    for root in range(n):
+        sizes = [rng.choice([1, 119, 120, 121, 5000, rng.randrange(1, 3 << 20)]) for _ in range(12)]
+        algos = ["chain_pipelined"] * 6 + ["direct"] * 5 + ["chain_pipelined"]
+        bufs = [[torch.empty(m, dtype=torch.uint8, device=f"cuda:{d}") for d in devices] for m in sizes]
+        srcs = []
+        for k, m in enumerate(sizes):
+            src = torch.randint(0, 256, (m,), dtype=torch.uint8, device=f"cuda:{devices[root]}")
+            for r in range(n):
+                (bufs[k][r].copy_(src) if r == root else bufs[k][r].fill_(0x77))
+            srcs.append(src)
+        for d in devices:
+            torch.cuda.synchronize(d)
+        before = comms[0].launches
+        with B.group():
+            for k, m in enumerate(sizes):
+                B.bcast_all(comms, bufs[k], m, "uint8", root, cfg_of(algos[k], 262144))
+        for d in devices:
+            torch.cuda.synchronize(d)
+        assert comms[0].launches - before <= 3, comms[0].launches - before
+        for k in range(len(sizes)):
+            for r in range(n):
+                assert torch.equal(bufs[k][r].cpu(), srcs[k].cpu()), (root, k, sizes[k], r)
+    # a large chain call inside the group goes to the lane executor, alone
+    big = [torch.zeros(64 << 20, dtype=torch.uint8, device=f"cuda:{d}") for d in devices]
+    big[0].fill_(9)
+    small = [torch.zeros(999, dtype=torch.uint8, device=f"cuda:{d}") for d in devices]
+    small[0].fill_(5)
+    for c in comms:
+        c.set_protocol("pull")
+    try:
+        with B.group():
+            B.bcast_all(comms, small, 999, "uint8", 0, cfg_of("direct"))
+            B.bcast_all(comms, big, 64 << 20, "uint8", 0, cfg_of("chain_pipelined", 65536))
+            B.bcast_all(comms, small, 999, "uint8", 0, cfg_of("direct"))
+    finally:
+        for c in comms:
+            c.set_protocol("auto")
+    for d in devices:
+        torch.cuda.synchronize(d)
+    for r in range(n):
+        assert int(big[r].min()) == 9 == int(big[r].max()) and int(small[r].min()) == 5 == int(small[r].max())

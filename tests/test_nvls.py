@@ -26,8 +26,8 @@ needs2 = pytest.mark.skipif(ngpu() < 2, reason="needs >= 2 GPUs")
 needs1 = pytest.mark.skipif(ngpu() < 1, reason="needs a GPU")
 
 
-def _team(devices, **opts):
-    comms = B.Comm.local(devices, timeout_s=10, **opts)
+def _team(devices, timeout_s=10, **opts):
+    comms = B.Comm.local(devices, timeout_s=timeout_s, **opts)
     ok, why = comms[0].nvls()
     if not ok:
         pytest.skip("no multicast team on this box: " + why)
@@ -143,6 +143,17 @@ def test_nvls_ranks_sharing_gpus():
         run_group(comms, devices, "direct", root, (5 << 20) + 11, seed=root)
     for c in comms:
         c.set_protocol("auto")
+
+
+@needs2
+def test_nvls_missing_root_times_out_with_named_error():
+    comms = _team([0, 1], timeout_s=1.0)
+    comms[0].set_protocol("nvls")
+    buf = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda:0")
+    comms[0].bcast(buf, 1 << 20, "uint8", 1, cfg_of("direct"))  # the root (rank 1) never calls
+    with pytest.raises(B.DeviceTimeout) as e:
+        comms[0].check()
+    assert "rank 0" in str(e.value)
 
 
 def _free_port():
