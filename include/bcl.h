@@ -256,9 +256,10 @@ bcl_status_t bcl_comm_set_protocol(bcl_comm_t c, int protocol);
 /* Group fusion (NCCL-style ncclGroupStart/End; per calling thread, nestable).
  * bcl_bcast / bcl_bcast_all calls issued between start and end are deferred;
  * at the outermost end, runs of consecutive calls on one communicator that take
- * the same line protocol (LL `direct`, LL or LL128 chain) with the same root
- * and stream are fused into one kernel launch carrying up to 32 messages (8
- * when ranks share a GPU), everything else launches as usual, in call order.
+ * a line protocol (LL `direct`, LL or LL128 chain) with the same root and
+ * stream are fused into one kernel launch carrying up to 32 messages (8 when
+ * ranks share a GPU) on the run's most capable protocol (LL128 chain > LL
+ * chain > LL direct), everything else launches as usual, in call order.
  * Every rank must issue the same calls between the same start/end (MPI
  * semantics); host-buffer and synchronous run_bcast calls cannot be grouped
  * (BCL_ERR_INVALID_ARGUMENT). The paper's caller broadcasts every layer of a

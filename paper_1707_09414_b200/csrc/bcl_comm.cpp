@@ -1260,10 +1260,10 @@ void Group::bcast_all(const std::vector<void*>& bufs, std::uint64_t bytes, int r
 // ------------------------------------------------------------- group fusion
 //
 // bcl_group_start/end (NCCL-style): broadcasts issued in between are
-// deferred; at the end, runs of consecutive calls that take the same line
-// protocol (LL direct, LL chain, LL128 chain) with the same root and stream
-// are fused into one launch carrying up to 32 messages (segments), the rest
-// launch as usual, in order. Every rank sees the same call sequence, so every
+// deferred; at the end, runs of consecutive calls on a line protocol (LL
+// direct, LL chain, LL128 chain) with the same root and stream are fused into
+// one launch carrying up to 32 messages (segments) on the run's most capable
+// protocol; the rest launch as usual, in order. Every rank sees the same call sequence, so every
 // rank fuses identically (the fused launch is one call epoch everywhere).
 
 void Group::group_start() { ++g_group_depth; }
@@ -1322,22 +1322,30 @@ void Group::flush_deferred() {
   std::size_t i = 0;
   while (i < calls.size()) {
     const Deferred& d = calls[i];
-    const int kind = fuse_kind(d);
-    // Extend the run: same kind, root, shape and streams; within the segment
-    // and landing-area caps.
+    int kind = fuse_kind(d);
+    // Extend the run: same root, shape and streams, every member on a line
+    // protocol; the run travels on its most capable member's protocol (LL128
+    // chain > LL chain > LL direct: small messages ride along a chain launch
+    // rather than cut the run), within the segment and landing-area caps.
     std::size_t j = i + 1;
     if (kind != 0) {
       int per_dev = 1;
       for (const auto& kv : by_device_) per_dev = std::max(per_dev, static_cast<int>(kv.second.size()));
       const std::size_t max_segs = static_cast<std::size_t>(dev::max_segs(d.all ? per_dev : 1));
-      const std::uint64_t cap = kind == 1 ? ll_max_ / 8 : kind == 2 ? ll_chain_max_ / 8 : (1ull << 31) - 1;
-      std::uint64_t lines = ll_lines_of(d.bytes, kind - 1);
+      auto fits = [&](std::size_t end, int k) {
+        const std::uint64_t cap = k == 1 ? ll_max_ / 8 : k == 2 ? ll_chain_max_ / 8 : (1ull << 31) - 1;
+        std::uint64_t lines = 0;
+        for (std::size_t c = i; c < end; ++c) lines += ll_lines_of(calls[c].bytes, k - 1);
+        return lines <= cap;
+      };
       while (j < calls.size() && j - i < max_segs) {
         const Deferred& e = calls[j];
-        if (e.all != d.all || e.li != d.li || e.root != d.root || e.streams != d.streams || fuse_kind(e) != kind) break;
-        const std::uint64_t more = ll_lines_of(e.bytes, kind - 1);
-        if (lines + more > cap) break;
-        lines += more;
+        if (e.all != d.all || e.li != d.li || e.root != d.root || e.streams != d.streams) break;
+        const int ke = fuse_kind(e);
+        if (ke == 0) break;
+        const int k = std::max(kind, ke);
+        if (!fits(j + 1, k)) break;
+        kind = k;
         ++j;
       }
     }
