@@ -207,6 +207,26 @@ class LocalGroup {
   std::vector<bcl_comm_t> comms_;
 };
 
+// Group fusion (bcl_group_start/end): broadcasts issued while a Group object
+// lives are deferred and fused when the outermost one ends (end() reports
+// errors; the destructor ends an un-ended group and swallows them).
+class Group {
+ public:
+  Group() { check(bcl_group_start()); }
+  ~Group() {
+    if (open_) bcl_group_end();
+  }
+  Group(const Group&) = delete;
+  Group& operator=(const Group&) = delete;
+  void end() {
+    open_ = false;
+    check(bcl_group_end());
+  }
+
+ private:
+  bool open_{true};
+};
+
 // MPI_Bcast-shaped per-rank call: bcast(buf, count, dtype, root, comm).
 inline void bcast(void* buf, std::size_t count, bcl_dtype_t dtype, int root, bcl_comm_t comm,
                   const Config* config = nullptr, void* stream = nullptr) {
