@@ -132,7 +132,7 @@ void set_option(GroupOptions& o, const std::string& key, const std::string& v) {
 constexpr const char* kOptionNames[] = {
     "poll_ns", "window_bytes", "min_slice", "max_ctas", "strict_sys", "sys_scope", "eager_post", "writer_fence",
     "local_fused", "local_ctas", "local_item", "local_claim", "ll", "ll128", "ll128_coop", "ll128_ctas", "protocol", "ll_max", "ll_chain_max", "ll128_max",
-    "host_piece", "stages", "stage_bytes", "nvls", "nvls_strict", "nvls_slot", "nvls_ctas"};
+    "host_piece", "stages", "stage_bytes", "nvls", "nvls_strict", "nvls_slot", "nvls_ctas", "nvls_ll_max"};
 
 }  // namespace
 
@@ -209,6 +209,7 @@ void Group::cache_device_limits(int device) {
   ck(static_cast<cudaError_t>(local_chain_occupancy(&local_chain_occ_)), "occupancy(local chain)");
   ck(static_cast<cudaError_t>(ll128_occupancy(&ll128_occ_)), "occupancy(ll128)");
   ck(static_cast<cudaError_t>(nvls_occupancy(&nvls_occ_)), "occupancy(nvls)");
+  ck(static_cast<cudaError_t>(nvls_ll_occupancy(&nvls_ll_occ_)), "occupancy(nvls ll)");
 }
 
 void Group::upload_peers(LocalRank& r) {
@@ -775,6 +776,43 @@ bool Group::use_nvls(const CallPlan& p, std::uint64_t bytes) const {
 void Group::launch_nvls_group(const std::vector<int>& locals, const std::vector<void*>& bufs, std::uint64_t bytes,
                               int root, cudaStream_t stream) {
   if (bytes == 0) return;  // nothing moves (every rank skips alike)
+  const std::uint64_t ll_max = std::min<std::uint64_t>(opt_.nvls_ll_max, dev::kNvlsLLMaxBytes);
+  if (bytes <= ll_max) {  // NVLS-LL lines: no per-piece release
+    dev::NvlsLLParams L{};
+    L.n_local = static_cast<int>(locals.size());
+    L.lines = static_cast<std::uint32_t>((bytes + 7) / 8);
+    L.bytes = bytes;
+    // ~2 lines per thread, identical on every GPU (the reports count on it);
+    // every CTA of every rank sharing a GPU co-resident (cooperative launch).
+    int per_dev = 1;
+    for (const auto& kv : by_device_) per_dev = std::max(per_dev, static_cast<int>(kv.second.size()));
+    const int cap = std::max(1, std::min(64, sms_ * std::max(nvls_ll_occ_, 1) / per_dev));
+    L.ctas = std::clamp<int>(static_cast<int>((L.lines + 1023) / 1024), 1, cap);
+    const int device = local_[static_cast<std::size_t>(locals[0])].device;
+    std::uint64_t need = 0;
+    const std::uint64_t epoch =
+        nvls_->take_ll(device, static_cast<std::uint64_t>(n_ - 1) * static_cast<std::uint64_t>(L.ctas), &need);
+    L.epoch = static_cast<std::uint32_t>(epoch);
+    L.half = static_cast<std::uint32_t>(epoch & 1u);
+    L.need_done = need;
+    L.timeout_ns = opt_.timeout_ns;
+    L.mc = nvls_->mc(device);
+    L.uc = nvls_->uc(device);
+    const std::size_t S = region_stride();
+    for (std::size_t i = 0; i < locals.size(); ++i) {
+      LocalRank& r = local_[static_cast<std::size_t>(locals[i])];
+      dev::NvlsRank& w = L.ranks[i];
+      w.rank = r.rank;
+      w.is_root = r.rank == root ? 1 : 0;
+      w.buf = static_cast<std::uint8_t*>(bufs[i]);
+      w.err = r.err_dev;
+      w.abort = reinterpret_cast<int*>(r.region + 4 * S + static_cast<std::size_t>(n_));
+      ++r.launches;
+    }
+    DeviceScope ds(device);
+    ck(static_cast<cudaError_t>(launch_nvls_ll(L, stream)), "launch(nvls ll)");
+    return;
+  }
   const std::uint32_t slot = opt_.nvls_slot ? opt_.nvls_slot : dev::kNvlsDefaultSlot;
   const int wave = opt_.nvls_ctas > 0 ? opt_.nvls_ctas : dev::kNvlsDefaultCtas;
   const NvlsGeometry geo = nvls_geometry(bytes, slot, wave);
@@ -1143,7 +1181,9 @@ std::string Group::path(const AlgorithmConfig* cfg, int root, std::uint64_t byte
   if (n_ == 1) return "none";
   std::vector<int> locals;
   for (int i = 0; i < local_count(); ++i) locals.push_back(i);
-  if (use_nvls(p, bytes)) return "nvls_kernel";
+  if (use_nvls(p, bytes)) {
+    return bytes <= std::min<std::uint64_t>(opt_.nvls_ll_max, dev::kNvlsLLMaxBytes) ? "nvls_ll_kernel" : "nvls_kernel";
+  }
   if (p.config.algorithm == Algorithm::Direct && bytes <= ll_max_ && opt_.ll) return "ll_kernel/direct";
   if (const int mode = ll_chain_mode(p, bytes, locals)) return mode == 2 ? "ll128_kernel" : "ll_kernel/chain";
   if (use_local_chain(p, locals)) return "local_chain_kernel";

@@ -117,6 +117,8 @@ struct GroupOptions {
   std::uint32_t nvls_slot = 0;                              // NVLS ring slot bytes (0 = 256 KiB; power of two,
                                                             // 16 KiB .. 8 MiB; identical on every rank)
   int nvls_ctas = 0;                                        // NVLS pieces per wave / CTAs per rank (0 = 148)
+  std::uint64_t nvls_ll_max = 2ull << 20;                   // NVLS messages up to this size travel as multicast
+                                                            // LL lines (0 = never; at most 2 MiB)
   static GroupOptions from_env();                           // BCL_* overrides (tuning runs)
   // "key=value,key=value" with the BCL_* names in lower case (e.g.
   // "stage_bytes=8192,sys_scope=1,protocol=2"); applied over *this.
@@ -331,6 +333,7 @@ class Group {
   int local_chain_occ_{0};      // resident local_chain_kernel CTAs per SM
   int ll128_occ_{0};            // resident ll128_kernel CTAs per SM
   int nvls_occ_{0};             // resident nvls_kernel CTAs per SM
+  int nvls_ll_occ_{0};          // resident nvls_ll_kernel CTAs per SM
   unsigned long long* lc_claim_{nullptr};  // local_chain_kernel item counters [64] (device; zero between uses)
   std::uint64_t lc_launches_{0};
   std::unique_ptr<NvlsTeam> nvls_;  // multicast team (null: NVLS unavailable on this group)

@@ -206,6 +206,100 @@ __global__ void __launch_bounds__(kNvlsThreads) nvls_kernel(const __grid_constan
   }
 }
 
+__device__ __forceinline__ void mc_st_u4(void* p, std::uint32_t a, std::uint32_t b, std::uint32_t c,
+                                         std::uint32_t d) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+
+template <int NL>
+__global__ void __launch_bounds__(512) nvls_ll_kernel(const __grid_constant__ NvlsLLParamsT<NL> P) {
+  __shared__ int ok_sh;
+  const int li = static_cast<int>(blockIdx.x) / P.ctas;
+  const int j = static_cast<int>(blockIdx.x) % P.ctas;
+  if (li >= P.n_local) return;
+  const NvlsRank& R = P.ranks[li];
+  const std::size_t area = (static_cast<std::size_t>(kNvlsCtlBytes) + kNvlsRingBytes) +
+                           static_cast<std::size_t>(P.half) * kNvlsLLLines * 16;
+  const std::uint32_t first = static_cast<std::uint32_t>(j) * blockDim.x + threadIdx.x;
+  const std::uint32_t stride = static_cast<std::uint32_t>(P.ctas) * blockDim.x;
+  const bool aligned = (reinterpret_cast<std::uintptr_t>(R.buf) & 7u) == 0;
+  std::uint64_t* mc_done = reinterpret_cast<std::uint64_t*>(P.mc) + kNvlsLLDone + P.half;
+  const std::uint64_t* uc_done = reinterpret_cast<const std::uint64_t*>(P.uc) + kNvlsLLDone + P.half;
+  if (R.is_root) {
+    // The half was last read two calls ago: every receiver CTA has reported.
+    if (P.need_done > 0 && !cta_wait_geq(R, uc_done, P.need_done, P.timeout_ns, 0, &ok_sh)) return;
+    uint4* dst = reinterpret_cast<uint4*>(P.mc + area);
+    for (std::uint32_t i = first; i < P.lines; i += stride) {
+      const std::uint64_t off = static_cast<std::uint64_t>(i) * 8;
+      std::uint32_t lo = 0, hi = 0;
+      if (aligned && off + 8 <= P.bytes) {
+        const uint2 v = *reinterpret_cast<const uint2*>(R.buf + off);
+        lo = v.x;
+        hi = v.y;
+      } else {
+        for (std::uint32_t b = 0; b < 8 && off + b < P.bytes; ++b) {
+          const std::uint32_t byte = R.buf[off + b];
+          if (b < 4) lo |= byte << (8 * b); else hi |= byte << (8 * (b - 4));
+        }
+      }
+      mc_st_u4(dst + i, lo, P.epoch, hi, P.epoch);
+    }
+    return;
+  }
+  const uint4* src = reinterpret_cast<const uint4*>(P.uc + area);
+  bool ok = true;
+  for (std::uint32_t i = first; i < P.lines && ok; i += stride) {
+    uint4 v;
+    asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(src + i)
+                 : "memory");
+    if (v.y != P.epoch || v.w != P.epoch) {
+      const std::uint64_t t0 = nv_timer();
+      unsigned spins = 0;
+      for (;;) {
+        asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "l"(src + i)
+                     : "memory");
+        if (v.y == P.epoch && v.w == P.epoch) break;
+        if ((++spins & 1023u) == 0) {
+          if (*(volatile int*)R.abort != 0) {
+            ok = false;
+            break;
+          }
+          if (nv_timer() - t0 > P.timeout_ns) {
+            atomicExch(R.abort, 1);
+            if (atomicCAS(&R.err->code, 0, 1) == 0) {
+              R.err->rank = R.rank;
+              R.err->peer = -1;
+              R.err->lane = static_cast<int>(blockIdx.x);
+              R.err->chunk = i;
+              R.err->observed = v.y;
+              R.err->expected = P.epoch;
+              __threadfence_system();
+            }
+            ok = false;
+            break;
+          }
+        }
+      }
+      if (!ok) break;
+    }
+    const std::uint64_t off = static_cast<std::uint64_t>(i) * 8;
+    if (aligned && off + 8 <= P.bytes) {
+      *reinterpret_cast<uint2*>(R.buf + off) = make_uint2(v.x, v.z);
+    } else {
+      for (std::uint32_t b = 0; b < 8 && off + b < P.bytes; ++b) {
+        R.buf[off + b] = static_cast<std::uint8_t>((b < 4 ? v.x >> (8 * b) : v.z >> (8 * (b - 4))) & 0xFFu);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && ok) mc_add_release(mc_done, 1);  // this CTA's lines of the half are read
+}
+
 }  // namespace
 }  // namespace dev
 
@@ -226,6 +320,30 @@ NvlsGeometry nvls_geometry(std::uint64_t bytes, std::uint32_t slot_bytes, int wa
 int nvls_occupancy(int* blocks_per_sm) {
   return static_cast<int>(
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, dev::nvls_kernel<1>, dev::kNvlsThreads, 0));
+}
+
+int nvls_ll_occupancy(int* blocks_per_sm) {
+  return static_cast<int>(
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, dev::nvls_ll_kernel<1>, 512, 0));
+}
+
+int launch_nvls_ll(const dev::NvlsLLParams& p, void* stream) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(p.n_local * p.ctas));
+  cfg.blockDim = dim3(512);
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = p.n_local > 1 ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (p.n_local == 1) {
+    dev::NvlsLLParamsT<1> one;
+    std::memcpy(&one, &p, offsetof(dev::NvlsLLParams, ranks));
+    one.ranks[0] = p.ranks[0];
+    return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::nvls_ll_kernel<1>, one));
+  }
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::nvls_ll_kernel<dev::kMaxLocal>, p));
 }
 
 int launch_nvls(const dev::NvlsParams& p, void* stream) {
@@ -327,7 +445,8 @@ void rt(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string("NVLS: ") + what + ": " + cudaGetErrorString(e));
 }
 
-std::uint64_t bound_bytes() { return static_cast<std::uint64_t>(dev::kNvlsCtlBytes) + dev::kNvlsRingBytes; }
+std::uint64_t ll_area_offset() { return static_cast<std::uint64_t>(dev::kNvlsCtlBytes) + dev::kNvlsRingBytes; }
+std::uint64_t bound_bytes() { return ll_area_offset() + 2 * dev::kNvlsLLLines * 16; }
 
 CUmulticastObjectProp mc_prop(int n_devices, std::uint64_t size, unsigned long long handle_types) {
   CUmulticastObjectProp prop = {};
@@ -500,8 +619,11 @@ void NvlsTeam::bind_device(Binding& b) {
   cu(d.MemAddressReserve(&b.mc, size_, gran_, 0, 0), "cuMemAddressReserve");
   cu(d.MemMap(b.mc, size_, 0, handle_, 0), "cuMemMap(multicast)");
   cu(d.MemSetAccess(b.mc, size_, &acc, 1), "cuMemSetAccess(multicast)");
-  // Counters start at zero (monotone afterwards); the data ring needs no init.
+  // Counters start at zero (monotone afterwards), so do the LL lines' flags
+  // (call epochs start at 1); the data ring needs no init.
   rt(cudaMemset(reinterpret_cast<void*>(b.uc), 0, dev::kNvlsCtlBytes), "cudaMemset(counters)");
+  rt(cudaMemset(reinterpret_cast<void*>(b.uc + ll_area_offset()), 0, 2 * dev::kNvlsLLLines * 16),
+     "cudaMemset(ll area)");
   rt(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
   rt(cudaSetDevice(saved), "cudaSetDevice");
 }
@@ -620,6 +742,19 @@ std::uint64_t NvlsTeam::take(int device, std::uint32_t pieces) {
       const std::uint64_t first = b.seq;
       b.seq += pieces;
       return first;
+    }
+  }
+  throw std::invalid_argument("NVLS: device not in the multicast team");
+}
+
+std::uint64_t NvlsTeam::take_ll(int device, std::uint64_t reports, std::uint64_t* need_done) {
+  for (Binding& b : bindings_) {
+    if (b.device == device) {
+      const std::uint64_t epoch = ++b.ll_calls;
+      std::uint64_t& half = b.ll_reports[epoch & 1u];
+      *need_done = half;
+      half += reports;
+      return epoch;
     }
   }
   throw std::invalid_argument("NVLS: device not in the multicast team");

@@ -33,7 +33,11 @@ namespace dev {
 
 constexpr std::uint64_t kNvlsRingBytes = 64ull << 20;  // staging ring per GPU
 constexpr std::uint32_t kNvlsMaxSlots = 4096;            // ring / slot bytes (slot >= 16 KiB)
-constexpr std::uint32_t kNvlsCtlBytes = 64u << 10;      // ready[kNvlsMaxSlots] | done[kNvlsMaxSlots], then data
+constexpr std::uint32_t kNvlsCtlBytes = 128u << 10;     // ready[kNvlsMaxSlots] | done[kNvlsMaxSlots] | ll_done[2],
+                                                         // then the ring, then the LL area
+constexpr std::uint32_t kNvlsLLDone = 2 * kNvlsMaxSlots;  // word index of ll_done[2]
+constexpr std::uint64_t kNvlsLLMaxBytes = 2ull << 20;     // NVLS-LL: largest message (8-byte payload per 16-byte line)
+constexpr std::uint64_t kNvlsLLLines = kNvlsLLMaxBytes / 8;  // lines per half of the LL area
 constexpr std::uint32_t kNvlsDefaultSlot = 256u << 10;  // 1 GiB at n = 4: 2007 us vs 2350 us with 128 KiB (profiles/round2/nvls)
 constexpr int kNvlsThreads = 512;
 constexpr int kNvlsDefaultCtas = 148;                    // pieces per wave (identical on every rank)
@@ -66,10 +70,33 @@ struct NvlsParamsT {
 };
 using NvlsParams = NvlsParamsT<kMaxLocal>;
 
+// NVLS-LL: small messages as 16-byte LL lines {4 B payload, flag, 4 B
+// payload, flag} written once through the multicast address into every
+// GPU's LL area (half = epoch & 1); receivers poll their own copy, no fence
+// and no per-piece release. ll_done[half] counts receiver CTAs that finished
+// reading that half (multimem.red), so the root reuses it safely.
+template <int NL>
+struct NvlsLLParamsT {
+  int n_local;
+  int ctas;                  // CTAs per local rank (identical on every GPU)
+  std::uint32_t lines;
+  std::uint64_t bytes;
+  std::uint32_t epoch;       // line flag
+  std::uint32_t half;
+  std::uint64_t need_done;   // root: ll_done[half] must reach this first
+  std::uint64_t timeout_ns;
+  std::uint8_t* mc;
+  std::uint8_t* uc;
+  NvlsRank ranks[NL];
+};
+using NvlsLLParams = NvlsLLParamsT<kMaxLocal>;
+
 }  // namespace dev
 
 int launch_nvls(const dev::NvlsParams& p, void* stream);
+int launch_nvls_ll(const dev::NvlsLLParams& p, void* stream);
 int nvls_occupancy(int* blocks_per_sm);
+int nvls_ll_occupancy(int* blocks_per_sm);
 
 // Piece geometry of an M-byte call (identical on every rank, given the same
 // slot size and wave width): about `wave` pieces per wave, each <= one slot.
@@ -108,6 +135,11 @@ class NvlsTeam {
   // returns the first. Every GPU of the team walks the same sequence (one
   // launch per GPU per call).
   std::uint64_t take(int device, std::uint32_t pieces);
+  // NVLS-LL call sequence of `device` (identical on every GPU): returns the
+  // call's epoch (>= 1); *need_done = the receiver-CTA reports its half must
+  // have collected before the root overwrites it (all earlier calls on that
+  // half), then adds this call's `reports`.
+  std::uint64_t take_ll(int device, std::uint64_t reports, std::uint64_t* need_done);
   const std::string& handle_kind() const { return kind_; }
 
  private:
@@ -118,6 +150,8 @@ class NvlsTeam {
     unsigned long long uc{};   // CUdeviceptr
     unsigned long long mc{};
     std::uint64_t seq{0};      // next ring sequence number of this GPU's launches
+    std::uint64_t ll_calls{0};  // NVLS-LL calls issued on this GPU
+    std::uint64_t ll_reports[2]{0, 0};  // receiver-CTA reports expected per half so far
     bool bound{false};
   };
   void bind_device(Binding& b);

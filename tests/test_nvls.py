@@ -57,7 +57,8 @@ def test_nvls_every_schedule_root_and_size():
     comms = _team(devices)
     for c in comms:
         c.set_protocol("nvls")
-    assert comms[0].path(1 << 20, cfg_of("chain_pipelined", 65536)) == "nvls_kernel"
+    assert comms[0].path(1 << 20, cfg_of("chain_pipelined", 65536)) == "nvls_ll_kernel"  # multicast LL lines
+    assert comms[0].path((2 << 20) + 1, cfg_of("chain_pipelined", 65536)) == "nvls_kernel"
     rng = random.Random(41)
     sizes = [1, 15, 16, 17, 4097, (1 << 20) + 3, rng.randrange(1, 9 << 20), (16 << 20) + 5]
     for algo in ("direct", "chain_pipelined", "knomial", "scatter_ring_allgather"):
@@ -79,6 +80,38 @@ def test_nvls_auto_carries_large_direct_and_empty_message():
     assert comms[0].path(8 << 20, cfg_of("chain_pipelined", 1 << 20)) != "nvls_kernel"
     run_group(comms, devices, "direct", 1, (8 << 20) + 1, seed=9)
     run_group(comms, devices, "direct", 0, 0, seed=1)
+
+
+@needs2
+def test_nvls_ll_lines_back_to_back():
+    """Multicast LL lines (messages <= 2 MiB): 300 calls back to back, both
+    halves of the LL area reused every other call, sizes around the 8-byte
+    line payload, misaligned views, rotating roots, every byte checked."""
+    devices = list(range(min(ngpu(), 8)))
+    n = len(devices)
+    comms = _team(devices)
+    for c in comms:
+        c.set_protocol("nvls")
+    rng = random.Random(97)
+    cap = 2 << 20
+    bufs = [torch.empty(cap + 16, dtype=torch.uint8, device=f"cuda:{d}") for d in devices]
+    try:
+        for it in range(300):
+            m = rng.choice([1, 7, 8, 9, 4095, rng.randrange(1, 70000), rng.randrange(70000, cap + 1), cap])
+            off = rng.randrange(0, 9)
+            root = (it * 5) % n
+            src = torch.randint(0, 256, (m,), dtype=torch.uint8, device=f"cuda:{devices[root]}")
+            views = [b[off:off + m] for b in bufs]
+            for r in range(n):
+                (views[r].copy_(src) if r == root else views[r].fill_(it & 0xFF))
+            torch.cuda.synchronize(devices[root])
+            assert comms[0].path(m, cfg_of("direct")) == "nvls_ll_kernel"
+            B.run_bcast(comms, root, views, m, cfg_of("direct"))
+            for r in range(n):
+                assert torch.equal(views[r].cpu(), src.cpu()), (it, m, off, root, r)
+    finally:
+        for c in comms:
+            c.set_protocol("auto")
 
 
 @needs2
