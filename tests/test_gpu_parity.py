@@ -189,6 +189,23 @@ def test_config1_full_size_all_ranks_equal_root():
         assert torch.equal(bufs[r], bufs[0])
 
 
+@pytest.mark.parametrize("root,chunk", [(0, 4 << 20), (3, 65536)])
+def test_one_gibibyte_every_rank_equals_root(root, chunk):
+    """The sweep's largest size (BASELINE 4 B - 1 GiB) on the fused kernel,
+    4 ranks on this GPU: every byte of every rank equals the root's."""
+    n, m = 4, 1 << 30
+    if torch.cuda.get_device_properties(0).total_memory < 6 * m:
+        pytest.skip("needs 6 GiB of device memory")
+    g = torch.Generator(device="cuda:0").manual_seed(root + 11)
+    bufs = [torch.zeros(m, dtype=torch.uint8, device="cuda:0") for _ in range(n)]
+    bufs[root].copy_(torch.randint(0, 256, (m,), dtype=torch.uint8, device="cuda:0", generator=g))
+    B.run_bcast(comms_for(n), root, bufs, m, cfg_of("chain_pipelined", chunk))
+    for r in range(n):
+        assert torch.equal(bufs[r], bufs[root]), r
+    del bufs
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("claim", [1, 0])
 def test_fused_chain_claimed_items_back_to_back_and_two_streams(claim):
     """The fused single-GPU kernel claims items from a per-launch counter that

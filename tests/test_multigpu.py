@@ -320,3 +320,27 @@ def test_group_fusion_across_gpus():
         torch.cuda.synchronize(d)
     for r in range(n):
         assert int(big[r].min()) == 9 == int(big[r].max()) and int(small[r].min()) == 5 == int(small[r].max())
+
+
+@needs2
+def test_one_gibibyte_across_gpus_every_transport():
+    """1 GiB (the sweep's top size) across GPUs on the default transport
+    (LL128 from n = 3, pull at n = 2) and on push; every byte checked."""
+    devices = list(range(min(ngpu(), 4)))
+    n, m = len(devices), 1 << 30
+    comms = B.Comm.local(devices, timeout_s=20)
+    bufs = [torch.zeros(m, dtype=torch.uint8, device=f"cuda:{d}") for d in devices]
+    g = torch.Generator(device=f"cuda:{devices[-1]}").manual_seed(5)
+    src = torch.randint(0, 256, (m,), dtype=torch.uint8, device=f"cuda:{devices[-1]}", generator=g)
+    for proto in ("auto", "push"):
+        for c in comms:
+            c.set_protocol(proto)
+        for r in range(n):
+            (bufs[r].copy_(src) if r == n - 1 else bufs[r].zero_())
+        for d in devices:
+            torch.cuda.synchronize(d)
+        B.run_bcast(comms, n - 1, bufs, m, cfg_of("chain_pipelined", 1 << 20))
+        for r in range(n):
+            assert torch.equal(bufs[r], src.to(f"cuda:{devices[r]}")), (proto, r)
+    for c in comms:
+        c.set_protocol("auto")
