@@ -321,7 +321,7 @@ def flush_l2(torch, flush):
     torch.sum(flush)
 
 
-def time_steps(torch, steps, warmup, prepare, body, verify, stream, align=None):
+def time_steps(torch, steps, warmup, prepare, body, verify, stream, align=None, gate=None):
     """Runs warmup+steps iterations; returns the per-step body times (s).
 
     Per step: prepare (buffer reset, L2 flush) -> a GPU-side gate
@@ -333,7 +333,7 @@ def time_steps(torch, steps, warmup, prepare, body, verify, stream, align=None):
     for it in range(warmup + steps):
         prepare(it)
         with torch.cuda.stream(stream):
-            torch.cuda._sleep(GATE_CYCLES)
+            torch.cuda._sleep(gate or GATE_CYCLES)
         if align is not None:
             align()
         ev0.record(stream)
@@ -722,8 +722,11 @@ def bench_params(args, torch, rank, world):
                 return all(torch.equal(flat[o:o + n], ref[o:o + n]) for o, n in zip(pb.offsets, pb.sizes))
 
             l0 = comm.launches
+            # a gate long enough for the host to enqueue every per-tensor call
+            # (~10 us of host time each) before the GPU reaches them
+            gate = max(GATE_CYCLES, 40_000 * len(pb.msgs))
             times = time_steps(torch, args.steps, args.warmup, prepare, body, verify, stream,
-                               align=lambda: comm.barrier(stream))
+                               align=lambda: comm.barrier(stream), gate=gate)
             if impl == "ours":  # our kernels in the timed steps (the barrier kernels excluded)
                 launches_total += (comm.launches - l0) * args.steps // (args.steps + args.warmup)
             t = torch.tensor(times, dtype=torch.float64, device=dev)
