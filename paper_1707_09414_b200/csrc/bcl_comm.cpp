@@ -1264,7 +1264,7 @@ void Group::bcast(int li, void* buf, std::uint64_t bytes, int root, const Algori
   const AlgorithmConfig c = choose(bytes, cfg);
   const CallPlan p = plan(c, root, bytes);
   if (n_ == 1) return;  // nothing moves (reference: n = 1 leaves the buffer untouched)
-  if (defer(Deferred{false, li, {buf}, bytes, root, p, {stream}})) return;
+  if (defer(Deferred{false, li, {buf}, bytes, root, p, {stream}, opt_.protocol})) return;
   launch_group({li}, {buf}, bytes, root, p, stream);
 }
 
@@ -1288,7 +1288,7 @@ void Group::bcast_all(const std::vector<void*>& bufs, std::uint64_t bytes, int r
     per.push_back(streams.empty() ? local_[static_cast<std::size_t>(first)].stream
                                   : streams[static_cast<std::size_t>(first)]);
   }
-  if (defer(Deferred{true, -1, bufs, bytes, root, p, per})) return;
+  if (defer(Deferred{true, -1, bufs, bytes, root, p, per, opt_.protocol})) return;
   std::size_t d = 0;
   for (const auto& kv : by_device_) {
     std::vector<void*> b;
@@ -1359,9 +1359,16 @@ int Group::fuse_kind(const Deferred& d) {
 void Group::flush_deferred() {
   std::vector<Deferred> calls;
   calls.swap(deferred_);
+  // Each call runs under the protocol that was set when it was issued.
+  struct Restore {
+    int& slot;
+    int saved;
+    ~Restore() { slot = saved; }
+  } restore{opt_.protocol, opt_.protocol};
   std::size_t i = 0;
   while (i < calls.size()) {
     const Deferred& d = calls[i];
+    opt_.protocol = d.protocol;
     int kind = fuse_kind(d);
     // Extend the run: same root, shape and streams, every member on a line
     // protocol; the run travels on its most capable member's protocol (LL128
@@ -1380,7 +1387,10 @@ void Group::flush_deferred() {
       };
       while (j < calls.size() && j - i < max_segs) {
         const Deferred& e = calls[j];
-        if (e.all != d.all || e.li != d.li || e.root != d.root || e.streams != d.streams) break;
+        if (e.all != d.all || e.li != d.li || e.root != d.root || e.streams != d.streams ||
+            e.protocol != d.protocol) {
+          break;
+        }
         const int ke = fuse_kind(e);
         if (ke == 0) break;
         const int k = std::max(kind, ke);

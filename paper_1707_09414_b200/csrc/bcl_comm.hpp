@@ -262,6 +262,7 @@ class Group {
     int root;
     CallPlan plan;
     std::vector<cudaStream_t> streams;  // bcast_all: one per device (by_device_ order)
+    int protocol;                       // set_protocol in effect at the call
   };
   bool defer(Deferred d);
   int fuse_kind(const Deferred& d);
