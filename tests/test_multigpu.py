@@ -235,6 +235,25 @@ def _ipc_worker(rank, world, port, q):
             comm.check()
             ok &= view.cpu().numpy().tobytes() == payload
         comm.set_protocol("auto")
+        # grouped per-rank calls (bcl_group_start/end): every rank fuses alike
+        msgs = [(1, 0), (300, 64), (70000, 1024), ((2 << 20) + 5, 80000), (17, (3 << 20)), ((1 << 20) + 3, 4 << 20)]
+        payloads = []
+        root = world - 1
+        for k, (m, off) in enumerate(msgs):
+            payload = O.payload(400 + k, m)
+            view = plain[off:off + m]
+            (view.copy_(torch.frombuffer(bytearray(payload), dtype=torch.uint8)) if rank == root else view.zero_())
+            payloads.append(payload)
+        torch.cuda.synchronize()
+        dist.barrier()
+        before = comm.launches
+        with B.group():
+            for m, off in msgs:
+                comm.bcast(plain[off:off + m], m, "uint8", root, None)
+        comm.check()
+        ok &= comm.launches - before < len(msgs)
+        for (m, off), payload in zip(msgs, payloads):
+            ok &= plain[off:off + m].cpu().numpy().tobytes() == payload
         # host-buffer entry point (pipelined H2D / broadcast / D2H pieces)
         m = (9 << 20) + 3
         payload = O.payload(99, m)
