@@ -1249,8 +1249,27 @@ void Group::launch_group(const std::vector<int>& locals, const std::vector<void*
   ck(static_cast<cudaError_t>(launch_bcast(P, P.n_local > 1 ? 1 : 0, stream)), "launch(bcast)");
 }
 
+namespace {
+
+// Kernel parameters carry host-side call epochs (and the line protocols'
+// landing-half and credit bookkeeping): a CUDA graph replaying a captured
+// broadcast would reuse them and read stale flags as fresh. Refuse capture.
+void no_capture(cudaStream_t stream) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &st) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  if (st != cudaStreamCaptureStatusNone) {
+    throw std::invalid_argument("broadcasts cannot be captured into a CUDA graph (call epochs live on the host)");
+  }
+}
+
+}  // namespace
+
 void Group::bcast(int li, void* buf, std::uint64_t bytes, int root, const AlgorithmConfig* cfg,
                   cudaStream_t stream) {
+  no_capture(stream);
   if (broken_) throw std::runtime_error("communicator is unusable after a device failure");
   if (!connected_) throw std::invalid_argument("communicator is not connected");
   if (root < 0 || root >= n_) throw std::invalid_argument("root out of range");
@@ -1287,6 +1306,8 @@ void Group::bcast_all(const std::vector<void*>& bufs, std::uint64_t bytes, int r
     const int first = kv.second.front();
     per.push_back(streams.empty() ? local_[static_cast<std::size_t>(first)].stream
                                   : streams[static_cast<std::size_t>(first)]);
+    DeviceScope ds(kv.first);
+    no_capture(per.back());
   }
   if (defer(Deferred{true, -1, bufs, bytes, root, p, per, opt_.protocol})) return;
   std::size_t d = 0;

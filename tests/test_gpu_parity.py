@@ -585,3 +585,19 @@ def test_layerwise_parameter_broadcast_fused(model):
     for r in range(n):
         for off, size in zip(pb.offsets, pb.sizes):
             assert torch.equal(flats[r][off:off + size], flats[root][off:off + size]), (model, r, off)
+
+
+def test_graph_capture_is_refused():
+    """Kernel parameters carry host-side call epochs: a captured broadcast
+    would replay stale epochs, so capture fails loudly instead."""
+    n = 4
+    comms = comms_for(n)
+    bufs = [torch.zeros(4096, dtype=torch.uint8, device="cuda:0") for _ in range(n)]
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with pytest.raises(ValueError, match="CUDA graph"):
+        with torch.cuda.graph(g, stream=s):
+            B.bcast_all(comms, bufs, 4096, "uint8", 0, cfg_of("direct"), streams=[s] * n)
+    torch.cuda.synchronize()
+    B.bcast_all(comms, bufs, 4096, "uint8", 0, cfg_of("direct"))  # the communicator still works
+    torch.cuda.synchronize()
