@@ -180,8 +180,9 @@ AggregateRankError::AggregateRankError(std::vector<RankFailure> failures)
 
 void Group::alloc_rank(LocalRank& r, std::size_t heap_bytes) {
   DeviceScope ds(r.device);
-  // (+ 8 words: the last one is the connect-time agreement word, kCtlWord)
-  r.region_bytes = (ll_offset(lanes_alloc_) + ll_words() + 8) * sizeof(std::uint64_t);
+  // (+ the device-side call state, then 8 words whose last one is the
+  // connect-time agreement word)
+  r.region_bytes = (ll_offset(lanes_alloc_) + ll_words() + dev::kCallStateWords + 8) * sizeof(std::uint64_t);
   ck(cudaMalloc(&r.region, r.region_bytes), "cudaMalloc(region)");
   ck(cudaMemset(r.region, 0, r.region_bytes), "cudaMemset(region)");
   ck(cudaMalloc(&r.d_peers, sizeof(dev::PeerTable)), "cudaMalloc(peers)");
@@ -207,7 +208,8 @@ void Group::cache_device_limits(int device) {
   DeviceScope ds(device);
   ck(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device), "sm count");
   ck(static_cast<cudaError_t>(local_chain_occupancy(&local_chain_occ_)), "occupancy(local chain)");
-  ck(static_cast<cudaError_t>(ll128_occupancy(&ll128_occ_)), "occupancy(ll128)");
+  ck(static_cast<cudaError_t>(ll128_occupancy(&ll128_occ_, 0)), "occupancy(ll128)");
+  ck(static_cast<cudaError_t>(ll128_occupancy(&ll128_occ_shared_, 1)), "occupancy(ll128, shared GPU)");
   ck(static_cast<cudaError_t>(nvls_occupancy(&nvls_occ_)), "occupancy(nvls)");
   ck(static_cast<cudaError_t>(nvls_ll_occupancy(&nvls_ll_occ_)), "occupancy(nvls ll)");
 }
@@ -789,12 +791,7 @@ void Group::launch_nvls_group(const std::vector<int>& locals, const std::vector<
     const int cap = std::max(1, std::min(64, sms_ * std::max(nvls_ll_occ_, 1) / per_dev));
     L.ctas = std::clamp<int>(static_cast<int>((L.lines + 1023) / 1024), 1, cap);
     const int device = local_[static_cast<std::size_t>(locals[0])].device;
-    std::uint64_t need = 0;
-    const std::uint64_t epoch =
-        nvls_->take_ll(device, static_cast<std::uint64_t>(n_ - 1) * static_cast<std::uint64_t>(L.ctas), &need);
-    L.epoch = static_cast<std::uint32_t>(epoch);
-    L.half = static_cast<std::uint32_t>(epoch & 1u);
-    L.need_done = need;
+    L.n_recv = n_ - 1;
     L.timeout_ns = opt_.timeout_ns;
     L.mc = nvls_->mc(device);
     L.uc = nvls_->uc(device);
@@ -807,6 +804,7 @@ void Group::launch_nvls_group(const std::vector<int>& locals, const std::vector<
       w.buf = static_cast<std::uint8_t*>(bufs[i]);
       w.err = r.err_dev;
       w.abort = reinterpret_cast<int*>(r.region + 4 * S + static_cast<std::size_t>(n_));
+      w.state = state_of(r);
       ++r.launches;
     }
     DeviceScope ds(device);
@@ -827,7 +825,6 @@ void Group::launch_nvls_group(const std::vector<int>& locals, const std::vector<
   P.bytes = bytes;
   P.piece_bytes = geo.piece_bytes;
   const int device = local_[static_cast<std::size_t>(locals[0])].device;
-  P.seq_base = nvls_->take(device, geo.pieces);
   P.timeout_ns = opt_.timeout_ns;
   P.strict = opt_.nvls_strict ? 1 : 0;
   P.mc = nvls_->mc(device);
@@ -841,6 +838,7 @@ void Group::launch_nvls_group(const std::vector<int>& locals, const std::vector<
     w.buf = static_cast<std::uint8_t*>(bufs[i]);
     w.err = r.err_dev;
     w.abort = reinterpret_cast<int*>(r.region + 4 * S + static_cast<std::size_t>(n_));
+    w.state = state_of(r);
     ++r.launches;
   }
   DeviceScope ds(device);
@@ -1071,6 +1069,7 @@ void Group::fill_rank_work(dev::RankWork& w, LocalRank& r, const CallPlan& p, vo
   w.prov = r.prov;
   w.trace = r.trace;
   w.trace_cap = r.trace_cap;
+  w.state = state_of(r);
   if (!p.implicit_chain) {
     const auto& ev = p.events[static_cast<std::size_t>(r.rank)];
     std::copy(ev.begin(), ev.end(), w.events);
@@ -1126,7 +1125,8 @@ void Group::launch_ll_segs(const std::vector<int>& locals, const std::vector<std
   if (mode == 2) {  // a warp moves 4 lines per step: ~2 steps per warp, up to 3 CTAs per SM
     const std::uint32_t per_cta = dev::kLLThreads / 32 * 4 * 2;
     // every CTA of every rank co-resident (writers wait on ring credits)
-    int cap = std::max(1, std::min(dev::kLL128MaxCtas, sms_ * std::max(ll128_occ_, 1)) / P.n_local);
+    const int occ = P.n_local > 1 ? ll128_occ_shared_ : ll128_occ_;
+    int cap = std::max(1, std::min(dev::kLL128MaxCtas, sms_ * std::max(occ, 1)) / P.n_local);
     if (opt_.ll128_ctas > 0) cap = std::min(cap, opt_.ll128_ctas);
     P.ctas = std::clamp<int>(static_cast<int>((P.lines + per_cta - 1) / per_cta), 1, cap);
   }
@@ -1136,7 +1136,7 @@ void Group::launch_ll_segs(const std::vector<int>& locals, const std::vector<std
   std::uint64_t epoch = 0;
   for (std::size_t i = 0; i < locals.size(); ++i) {
     LocalRank& r = local_[static_cast<std::size_t>(locals[i])];
-    const std::uint64_t e = ++r.epoch;
+    const std::uint64_t e = ++r.epoch;  // (host count: only checks that local ranks stay in step)
     if (i == 0) epoch = e;
     if (e != epoch) throw std::runtime_error("ranks sharing a GPU drifted apart in call count");
     dev::LLRank& w = P.ranks[i];
@@ -1148,27 +1148,11 @@ void Group::launch_ll_segs(const std::vector<int>& locals, const std::vector<std
     w.peers = r.d_peers;
     w.err = r.err_dev;
     w.abort = reinterpret_cast<int*>(r.region + 4 * S + static_cast<std::size_t>(n_));
-    const std::uint32_t half = static_cast<std::uint32_t>(e & 1u);
-    const int logical = (r.rank - root + n_) % n_;
-    // Writers wait for the credits of the last call of the same kind that
-    // wrote this half (direct: every other rank; chain: the successor).
-    std::uint64_t* last = nullptr;
-    if (mode == 1 && logical + 1 < n_) last = &r.ll_last_chain[half];
-    if (mode == 2 && logical + 1 < n_) last = &r.ll_last_ring;
-    if (!chain && logical == 0) last = &r.ll_last_direct[half];
-    if (last != nullptr) {
-      w.need_credit = *last;
-      *last = e;
-    }
-    if (logical != 0) {
-      w.done = reinterpret_cast<unsigned long long*>(r.region + 4 * S + 2 * static_cast<std::size_t>(n_) + 1);
-      r.ll_done += static_cast<std::uint64_t>(P.ctas);
-      w.done_target = r.ll_done;
-    }
+    // The epoch, the half and the writers' reuse bound (the last call of the
+    // same kind that wrote this half) come from the device-side call state.
+    w.state = state_of(r);
     ++r.launches;
   }
-  P.epoch = epoch;
-  P.half = static_cast<std::uint32_t>(epoch & 1u);
   DeviceScope ds(local_[static_cast<std::size_t>(locals[0])].device);
   ck(static_cast<cudaError_t>(bcl::launch_ll(P, stream)), "launch(ll)");
 }
@@ -1249,27 +1233,8 @@ void Group::launch_group(const std::vector<int>& locals, const std::vector<void*
   ck(static_cast<cudaError_t>(launch_bcast(P, P.n_local > 1 ? 1 : 0, stream)), "launch(bcast)");
 }
 
-namespace {
-
-// Kernel parameters carry host-side call epochs (and the line protocols'
-// landing-half and credit bookkeeping): a CUDA graph replaying a captured
-// broadcast would reuse them and read stale flags as fresh. Refuse capture.
-void no_capture(cudaStream_t stream) {
-  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(stream, &st) != cudaSuccess) {
-    cudaGetLastError();
-    return;
-  }
-  if (st != cudaStreamCaptureStatusNone) {
-    throw std::invalid_argument("broadcasts cannot be captured into a CUDA graph (call epochs live on the host)");
-  }
-}
-
-}  // namespace
-
 void Group::bcast(int li, void* buf, std::uint64_t bytes, int root, const AlgorithmConfig* cfg,
                   cudaStream_t stream) {
-  no_capture(stream);
   if (broken_) throw std::runtime_error("communicator is unusable after a device failure");
   if (!connected_) throw std::invalid_argument("communicator is not connected");
   if (root < 0 || root >= n_) throw std::invalid_argument("root out of range");
@@ -1306,8 +1271,6 @@ void Group::bcast_all(const std::vector<void*>& bufs, std::uint64_t bytes, int r
     const int first = kv.second.front();
     per.push_back(streams.empty() ? local_[static_cast<std::size_t>(first)].stream
                                   : streams[static_cast<std::size_t>(first)]);
-    DeviceScope ds(kv.first);
-    no_capture(per.back());
   }
   if (defer(Deferred{true, -1, bufs, bytes, root, p, per, opt_.protocol})) return;
   std::size_t d = 0;
@@ -1672,8 +1635,8 @@ void Group::barrier(int li, cudaStream_t stream) {
   dev::BarrierParams B{};
   B.n_ranks = n_;
   B.n_local = 1;
-  B.epoch = ++r.bar_epoch;
   B.timeout_ns = opt_.timeout_ns;
+  B.state[0] = state_of(r);
   B.rank[0] = r.rank;
   B.bar[0] = r.region + 4 * region_stride();
   B.peers[0] = r.d_peers;
@@ -1690,7 +1653,7 @@ void Group::barrier_all(const std::vector<cudaStream_t>& streams) {
     B.timeout_ns = opt_.timeout_ns;
     for (std::size_t i = 0; i < kv.second.size(); ++i) {
       LocalRank& r = local_[static_cast<std::size_t>(kv.second[i])];
-      B.epoch = ++r.bar_epoch;
+      B.state[i] = state_of(r);
       B.rank[i] = r.rank;
       B.bar[i] = r.region + 4 * region_stride();
       B.peers[i] = r.d_peers;

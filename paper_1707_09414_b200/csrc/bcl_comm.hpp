@@ -163,10 +163,6 @@ struct LocalRank {
   unsigned long long* trace{};  // optional per-lane event timestamps
   std::uint32_t trace_cap{0};
   std::uint64_t launches{0};
-  std::uint64_t ll_last_direct[2]{0, 0};  // last epoch this rank was a direct LL root, per half
-  std::uint64_t ll_last_chain[2]{0, 0};   // last epoch this rank wrote LL chain lines, per half
-  std::uint64_t ll_last_ring{0};          // last epoch this rank wrote into its successor's LL128 ring
-  std::uint64_t ll_done{0};        // cumulative LL CTA completions expected as a receiver
   std::vector<void*> opened;    // IPC mappings to close
   // Per-process mode: allocations registered for zero-copy broadcasts
   // (bcl_comm_register_*), id = index; peers' bases as mapped here.
@@ -294,6 +290,10 @@ class Group {
   void launch_local_chain(const std::vector<int>& locals, const std::vector<void*>& bufs, std::uint64_t bytes,
                           int root, const CallPlan& p, cudaStream_t stream);
   std::size_t region_stride() const { return static_cast<std::size_t>(n_) * lanes_; }
+  // The rank's device-side call state (after its LL areas; local use only).
+  dev::CallState* state_of(LocalRank& r) const {
+    return reinterpret_cast<dev::CallState*>(r.region + ll_offset(lanes_alloc_) + ll_words());
+  }
   // Offset (in 8-byte words) of the LL landing area for a flag stride of L lanes.
   std::size_t ll_offset(int lanes) const {
     const std::size_t w = 4 * static_cast<std::size_t>(n_) * lanes + 3 * static_cast<std::size_t>(n_) + 2 +
@@ -333,6 +333,7 @@ class Group {
   int sms_{0};                  // SM count of the first device
   int local_chain_occ_{0};      // resident local_chain_kernel CTAs per SM
   int ll128_occ_{0};            // resident ll128_kernel CTAs per SM
+  int ll128_occ_shared_{0};     // the same for the kernel serving ranks that share a GPU
   int nvls_occ_{0};             // resident nvls_kernel CTAs per SM
   int nvls_ll_occ_{0};          // resident nvls_ll_kernel CTAs per SM
   unsigned long long* lc_claim_{nullptr};  // local_chain_kernel item counters [64] (device; zero between uses)

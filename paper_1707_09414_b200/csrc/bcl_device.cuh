@@ -78,6 +78,25 @@ struct PeerTable {
                                        // here (device array), else null
 };
 
+// Per-rank call state, in the rank's own region (device memory). Every
+// kernel reads it when it starts and the last CTA of the rank to finish
+// advances it, so epochs and the line protocols' reuse bookkeeping live on
+// the device: a CUDA graph that replays a captured broadcast sees fresh
+// values on every replay (kernel parameters hold only the call's shape).
+struct CallState {
+  unsigned long long epoch;              // last call epoch (lane executor, LL, LL128)
+  unsigned long long bar_epoch;          // last device barrier
+  unsigned long long ll_last_direct[2];  // LL direct: last epoch this rank wrote each half as the root
+  unsigned long long ll_last_chain[2];   // LL chain: last epoch this rank wrote each half to its successor
+  unsigned long long ll_last_ring;       // LL128: last epoch this rank wrote into its successor's ring
+  unsigned long long finished;           // CTAs of this rank's running launch that finished
+  unsigned long long nvls_seq;           // NVLS ring sequence (identical on every rank)
+  unsigned long long nvls_ll_calls;      // NVLS-LL calls
+  unsigned long long nvls_ll_reports[2]; // NVLS-LL receiver-CTA reports expected per half so far
+  unsigned long long pad[4];
+};
+constexpr int kCallStateWords = sizeof(CallState) / 8;
+
 struct ErrorRecord {  // host-mapped, written by the first failing lane
   int code;           // 0 ok, 1 timeout, 2 aborted
   int rank;
@@ -102,6 +121,7 @@ struct RankWork {
   unsigned long long* prov;      // optional provenance: bytes pulled per [src][chunk]
   unsigned long long* trace;     // optional timeline: [lane][trace_cap][4] globaltimer stamps
   std::uint32_t trace_cap;
+  CallState* state;              // this rank's call state (epoch read at start, advanced at the end)
   std::uint64_t events[kMaxEvents];
 };
 
@@ -121,7 +141,7 @@ struct LaunchParamsT {
   std::uint64_t bytes;
   std::uint64_t chunk_bytes;
   std::uint64_t slice_bytes;  // multiple of 16
-  std::uint64_t epoch;        // >= 1, per call
+  std::uint64_t epoch;        // the call's epoch: filled in on the device from CallState (kernel-side copy)
   std::uint64_t timeout_ns;
   std::uint32_t poll_ns;      // __nanosleep between polls (0 = spin)
   std::uint32_t sys_scope;    // 1: peers on other GPUs; 0: every rank on this GPU
@@ -150,9 +170,7 @@ struct LLRank {
   const PeerTable* peers;
   ErrorRecord* err;
   int* abort;
-  std::uint64_t need_credit;  // writer: its targets must have credited this epoch (0 = no wait)
-  unsigned long long* done;   // receiver: local completion counter (cumulative over calls)
-  unsigned long long done_target;  // receiver: value of *done once every CTA of this call finished
+  CallState* state;           // epoch, the half-reuse bookkeeping and the finished-CTA count
 };
 
 struct LLHeader {
@@ -162,8 +180,6 @@ struct LLHeader {
   int ctas;                   // CTAs per rank
   std::uint32_t lines;        // lines of the launch (every segment's)
   std::uint64_t bytes;        // one segment: its bytes
-  std::uint64_t epoch;
-  std::uint32_t half;
   std::uint32_t area_lines;   // lines per (source, half) landing area of the direct schedule
   std::uint32_t chain;        // 0 direct, 1 pipelined chain on 16-byte LL lines, 2 chain on 128-byte LL128 lines
   std::uint32_t chain_lines;  // lines per half of the chain landing area (after the direct areas)
@@ -213,8 +229,8 @@ struct LocalChainParams {
 struct BarrierParams {
   int n_ranks;
   int n_local;
-  std::uint64_t epoch;
   std::uint64_t timeout_ns;
+  CallState* state[kMaxLocal];          // bar_epoch read and advanced on the device
   int rank[kMaxLocal];
   std::uint64_t* bar[kMaxLocal];        // local barrier slots
   const PeerTable* peers[kMaxLocal];
@@ -230,7 +246,7 @@ int launch_ll(const dev::LLParams& p, void* stream);
 int launch_peer_copy(std::uint8_t* dst, const std::uint8_t* src, std::uint64_t len, void* stream);
 int launch_local_chain(const dev::LocalChainParams& p, int ctas, void* stream);
 int local_chain_occupancy(int* blocks_per_sm);
-int ll128_occupancy(int* blocks_per_sm);
+int ll128_occupancy(int* blocks_per_sm, int shared);  // shared: the kernel for ranks sharing a GPU
 int bcast_kernel_occupancy(int* blocks_per_sm, std::size_t smem);
 std::size_t bcast_smem_bytes(std::uint32_t stages, std::uint32_t stage_bytes);
 int prepare_bcast_kernels(std::size_t smem);

@@ -183,6 +183,7 @@ struct Ctx {
   int ell;             // lane (copy warp) index within the rank
   std::uint32_t tail;  // private copy of sh->tail[warp] (lane 0)
   std::uint8_t* stage; // 2 x stage_bytes of dynamic shared memory (bulk path), or null
+  std::uint64_t epoch; // this call's epoch (from the rank's device-side call state)
 };
 
 // Record the first failure of this rank; every waiting lane then drains out.
@@ -289,7 +290,7 @@ __device__ __forceinline__ void st_mbox(std::uint64_t* slot, std::uint64_t value
 __device__ std::uint64_t read_mbox(const Ctx& c, const std::uint64_t* slot, int peer) {
   unsigned long long value = 0;
   if (c.lane_id == 0) {
-    const std::uint64_t epoch = c.P->epoch;
+    const std::uint64_t epoch = c.epoch;
     const std::uint64_t hi = (epoch & 0xFFFFull) << 48;
     const std::uint64_t t0 = globaltimer();
     unsigned spins = 0;
@@ -646,18 +647,18 @@ __device__ void run_chain_push(Ctx& c, int pipe, int q, int ns) {
   const std::uint32_t K = P.n_chunks;
   if (static_cast<std::uint32_t>(pipe) >= K) return;
   const std::uint32_t mine = (K - 1 - pipe) / ns + 1;
-  const std::uint64_t tag = P.epoch << 32;
+  const std::uint64_t tag = c.epoch << 32;
   const std::size_t slot = static_cast<std::size_t>(me) * L + c.ell;
   const std::uint64_t* arrived = has_prev ? W.flags + static_cast<std::size_t>(prev) * L + c.ell : nullptr;
   if (has_prev) {  // consumer: announce the destination, then "ready"
-    if (c.lane_id == 0) st_mbox(W.peers->mbox[prev] + 2 * slot, W.pub, P.epoch);
-    publish(c, W.peers->acks[prev] + slot, P.epoch);
+    if (c.lane_id == 0) st_mbox(W.peers->mbox[prev] + 2 * slot, W.pub, c.epoch);
+    publish(c, W.peers->acks[prev] + slot, c.epoch);
   }
   if (!has_next) {  // tail: wait until every chunk of this lane has landed
     (void)wait_geq(c, arrived, tag | mine, prev, K);
     return;
   }
-  if (!wait_geq(c, W.acks + static_cast<std::size_t>(next) * L + c.ell, P.epoch, next, 0)) return;
+  if (!wait_geq(c, W.acks + static_cast<std::size_t>(next) * L + c.ell, c.epoch, next, 0)) return;
   auto* dst = reinterpret_cast<std::uint8_t*>(
       peer_addr(W, next, read_mbox(c, W.mbox + 2 * (static_cast<std::size_t>(next) * L + c.ell), next)));
   std::uint64_t* next_flag = W.peers->flags[next] + slot;
@@ -698,10 +699,10 @@ __device__ void run_chain(Ctx& c, int pipe, int q, int ns) {
   const std::uint32_t K = P.n_chunks;
   if (static_cast<std::uint32_t>(pipe) >= K) return;
   const std::uint32_t mine = (K - 1 - pipe) / ns + 1;
-  const std::uint64_t tag = P.epoch << 32;
+  const std::uint64_t tag = c.epoch << 32;
   const std::size_t slot = static_cast<std::size_t>(me) * L + c.ell;
 
-  if (has_next && c.lane_id == 0) st_mbox(W.peers->mbox[next] + 2 * slot, W.pub, P.epoch);
+  if (has_next && c.lane_id == 0) st_mbox(W.peers->mbox[next] + 2 * slot, W.pub, c.epoch);
   if (!has_prev) {
     publish_direct(c, W.peers->flags[next] + slot, tag | mine);  // the head owns every chunk
   } else {
@@ -719,8 +720,8 @@ __device__ void run_chain(Ctx& c, int pipe, int q, int ns) {
                              tag)) {
           return;
         }
-        publish_direct(c, W.peers->acks[prev] + slot, P.epoch);
-        if (has_next) (void)wait_geq(c, W.acks + static_cast<std::size_t>(next) * L + c.ell, P.epoch, next, K);
+        publish_direct(c, W.peers->acks[prev] + slot, c.epoch);
+        if (has_next) (void)wait_geq(c, W.acks + static_cast<std::size_t>(next) * L + c.ell, c.epoch, next, K);
         return;
       }
     }
@@ -736,10 +737,10 @@ __device__ void run_chain(Ctx& c, int pipe, int q, int ns) {
       if (has_next) publish(c, W.peers->flags[next] + slot, tag | (k + 1));  // forward chunk k
       trace_pull(c, k, t_wait, t_ready);
     }
-    publish_direct(c, W.peers->acks[prev] + slot, P.epoch);  // done reading prev's buffer
+    publish_direct(c, W.peers->acks[prev] + slot, c.epoch);  // done reading prev's buffer
   }
   if (has_next) {
-    (void)wait_geq(c, W.acks + static_cast<std::size_t>(next) * L + c.ell, P.epoch, next, K);
+    (void)wait_geq(c, W.acks + static_cast<std::size_t>(next) * L + c.ell, c.epoch, next, K);
   }
 }
 
@@ -750,7 +751,7 @@ __device__ void run_events(Ctx& c, int pipe, int q, int ns) {
   const RankWork& W = *c.W;
   const int L = P.lanes;
   const std::size_t slot = static_cast<std::size_t>(W.rank) * L + c.ell;
-  const std::uint64_t tag = P.epoch << 32;
+  const std::uint64_t tag = c.epoch << 32;
   std::uint64_t sent_mask = 0, recv_mask = 0;
   // Announce our buffer to every peer this lane will serve.
   for (int i = 0; i < W.n_events; ++i) {
@@ -761,7 +762,7 @@ __device__ void run_events(Ctx& c, int pipe, int q, int ns) {
     const int peer = static_cast<int>((ev >> 24) & 0x7F);
     if (!((sent_mask >> peer) & 1u)) {
       sent_mask |= 1ull << peer;
-      if (c.lane_id == 0) st_mbox(W.peers->mbox[peer] + 2 * slot, W.pub, P.epoch);
+      if (c.lane_id == 0) st_mbox(W.peers->mbox[peer] + 2 * slot, W.pub, c.epoch);
     }
   }
   const std::uint8_t* src_of[kMaxRanks];
@@ -790,11 +791,11 @@ __device__ void run_events(Ctx& c, int pipe, int q, int ns) {
     }
   }
   for (std::uint64_t m = recv_mask; m; m &= m - 1) {
-    publish_direct(c, W.peers->acks[__ffsll(static_cast<long long>(m)) - 1] + slot, P.epoch);
+    publish_direct(c, W.peers->acks[__ffsll(static_cast<long long>(m)) - 1] + slot, c.epoch);
   }
   for (std::uint64_t m = sent_mask; m; m &= m - 1) {
     const int peer = __ffsll(static_cast<long long>(m)) - 1;
-    if (!wait_geq(c, W.acks + static_cast<std::size_t>(peer) * L + c.ell, P.epoch, peer, 0)) return;
+    if (!wait_geq(c, W.acks + static_cast<std::size_t>(peer) * L + c.ell, c.epoch, peer, 0)) return;
   }
 }
 
@@ -817,10 +818,27 @@ __global__ void __launch_bounds__(kThreads, NL == 1 ? 1 : BCL_SHARED_MIN_BLOCKS)
     for (std::uint32_t i = 0; i < P.stages; ++i) mbar_init(&sh.full[warp][i]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // The call's epoch comes from the rank's device-side call state (so a
+  // replayed CUDA graph gets a fresh one); every helper takes it from Ctx.
+  __shared__ unsigned long long epoch_sh;
+  __shared__ CallState* state_sh;
+  if (threadIdx.x == 0) {
+    state_sh = P.ranks[local].state;
+    epoch_sh = state_sh->epoch + 1;
+  }
   __syncthreads();
   const auto* hdr = reinterpret_cast<const LaunchParamsT<1>*>(&P);
   if (warp == kWarpsPerCta) {
     run_publisher(*hdr, &sh, P.ranks[local], cta);
+    // The publisher leaves last (after every copy warp of the CTA): the last
+    // CTA of the rank to finish advances the rank's epoch.
+    if ((threadIdx.x & 31) == 0) {
+      CallState* st = state_sh;
+      if (atomicAdd(&st->finished, 1ull) + 1 == static_cast<unsigned long long>(P.ctas_per_rank)) {
+        st->finished = 0;
+        st->epoch = epoch_sh;
+      }
+    }
     return;
   }
   Ctx c;
@@ -830,6 +848,7 @@ __global__ void __launch_bounds__(kThreads, NL == 1 ? 1 : BCL_SHARED_MIN_BLOCKS)
   c.lane_id = static_cast<int>(threadIdx.x & 31);
   c.warp = warp;
   c.ell = cta * kWarpsPerCta + warp;
+  c.epoch = epoch_sh;
   c.tail = 0;
   c.stage = P.stage_bytes ? dyn_smem + static_cast<std::size_t>(warp) * P.stages * P.stage_bytes : nullptr;
   if (c.ell < P.lanes) {
@@ -973,26 +992,32 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ 
   const std::uint32_t cta = NL == 1 ? blockIdx.x : blockIdx.x % P.ctas;
   const std::uint32_t first = cta * blockDim.x + threadIdx.x;
   const std::uint32_t stride = static_cast<std::uint32_t>(P.ctas) * blockDim.x;
-  const std::uint32_t flag = static_cast<std::uint32_t>(P.epoch);
+  __shared__ unsigned long long s_epoch;
+  if (threadIdx.x == 0) s_epoch = R.state->epoch + 1;  // the call's epoch (device-side call state)
+  __syncthreads();
+  const unsigned long long epoch = s_epoch;
+  const std::uint32_t half = static_cast<std::uint32_t>(epoch & 1u);
+  const std::uint32_t flag = static_cast<std::uint32_t>(epoch);
   const int n = P.n_ranks;
   const int logical = (R.rank - P.root + n) % n;
   const int next = (R.rank + 1) % n;
   const bool chain = P.chain != 0;
   const bool writer = chain ? logical + 1 < n : logical == 0;
   const std::size_t area =
-      chain ? static_cast<std::size_t>(n) * 2 * P.area_lines + static_cast<std::size_t>(P.half) * P.chain_lines
-            : (static_cast<std::size_t>(P.root) * 2 + P.half) * P.area_lines;
+      chain ? static_cast<std::size_t>(n) * 2 * P.area_lines + static_cast<std::size_t>(half) * P.chain_lines
+            : (static_cast<std::size_t>(P.root) * 2 + half) * P.area_lines;
   if (writer) {
     // The half we are about to overwrite was last written (same kind) in
-    // epoch need_credit: wait until the targets have read it (normally long ago).
+    // epoch need: wait until the targets have read it (normally long ago).
+    const std::uint64_t need = chain ? R.state->ll_last_chain[half] : R.state->ll_last_direct[half];
     const int t = static_cast<int>(threadIdx.x);
-    if (R.need_credit > 0 && (chain ? t == next : (t < n && t != P.root))) {
+    if (need > 0 && (chain ? t == next : (t < n && t != P.root))) {
       const std::uint64_t* cr = R.credit + t;
       const std::uint64_t t0 = globaltimer();
       std::uint64_t v;
-      while ((v = ld_relaxed_sys(cr)) < R.need_credit) {
+      while ((v = ld_relaxed_sys(cr)) < need) {
         if (globaltimer() - t0 > P.timeout_ns) {
-          ll_fail(R, t, 0, v, R.need_credit);
+          ll_fail(R, t, 0, v, need);
           break;
         }
       }
@@ -1024,14 +1049,13 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ 
         }
       }
     }
-    return;
   }
   // Receiver: poll our landing lines, forward (chain, not the tail), copy out.
   const uint4* src = R.ll + area;
   uint4* fwd = chain && writer ? R.peers->ll[next] + area : nullptr;
   const int source = chain ? (R.rank + n - 1) % n : P.root;
   bool ok = true;
-  for (std::uint32_t i = first; i < P.lines && ok; i += stride) {
+  for (std::uint32_t i = logical == 0 ? P.lines : first; i < P.lines && ok; i += stride) {
     uint4 v = ld_volatile_v4(src + i);
     if (v.y != flag || v.w != flag) {
       const std::uint64_t t0 = globaltimer();
@@ -1062,11 +1086,18 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ 
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0 && ok) {
-    // The last CTA to finish tells the source every line of this epoch has
-    // been read, so the source may reuse the half.
-    if (atomicAdd(R.done, 1ull) + 1 == R.done_target) {
-      st_relaxed_sys(R.peers->credit[source] + (chain ? n + 1 : 0) + R.rank, P.epoch);
+  if (threadIdx.x == 0) {
+    // The rank's last CTA to finish advances its call state and, as a
+    // receiver, tells the source every line of this epoch has been read, so
+    // the source may reuse the half.
+    CallState* st = R.state;
+    if (atomicAdd(&st->finished, 1ull) + 1 == static_cast<unsigned long long>(P.ctas)) {
+      st->finished = 0;
+      st->epoch = epoch;
+      if (writer) (chain ? st->ll_last_chain : st->ll_last_direct)[half] = epoch;
+      if (logical != 0 && *(volatile int*)R.abort == 0) {
+        st_relaxed_sys(R.peers->credit[source] + (chain ? n + 1 : 0) + R.rank, epoch);
+      }
     }
   }
 }
@@ -1113,8 +1144,10 @@ __device__ __forceinline__ void ll128_put(std::uint8_t* buf, std::uint64_t off, 
 }
 
 // NL > 1: ranks sharing one GPU (cooperative launch, P.ctas CTAs per rank).
+// (3 CTAs per SM for one rank per GPU; the 16-rank block, for ranks sharing a
+// GPU, is compiled for 2 so it does not spill at 42 registers.)
 template <int NL, int NS>
-__global__ void __launch_bounds__(kLLThreads, 3) ll128_kernel(const __grid_constant__ LLParamsT<NL, NS> P) {
+__global__ void __launch_bounds__(kLLThreads, NL == 1 ? 3 : 2) ll128_kernel(const __grid_constant__ LLParamsT<NL, NS> P) {
   const int li = NL == 1 ? 0 : static_cast<int>(blockIdx.x) / P.ctas;
   const LLRank& R = P.ranks[li];
   const std::uint32_t cta = NL == 1 ? blockIdx.x : blockIdx.x % P.ctas;
@@ -1123,19 +1156,27 @@ __global__ void __launch_bounds__(kLLThreads, 3) ll128_kernel(const __grid_const
   const int sub = lane >> 3;  // line within the warp's group of four
   const std::uint32_t warp = (cta * blockDim.x + threadIdx.x) >> 5;
   const std::uint32_t warps = (static_cast<std::uint32_t>(P.ctas) * blockDim.x) >> 5;
-  const unsigned long long epoch = P.epoch;
+  __shared__ unsigned long long s_epoch;
+  __shared__ CallState* s_state;
+  if (threadIdx.x == 0) {
+    s_state = R.state;
+    s_epoch = s_state->epoch + 1;  // the call's epoch (device-side call state)
+  }
+  __syncthreads();
+  const unsigned long long& epoch = s_epoch;  // (read from shared where used: LL128 runs at 42 registers)
   const int n = P.n_ranks;
   const int logical = (R.rank - P.root + n) % n;
   const int next = (R.rank + 1) % n;
   const int source = (R.rank + n - 1) % n;
   const bool writer = logical + 1 < n;
   if (writer) {  // the successor finished reading our previous LL128 call (ring reuse across calls)
-    if (R.need_credit > 0 && static_cast<int>(threadIdx.x) == next) {
+    const std::uint64_t need = s_state->ll_last_ring;
+    if (need > 0 && static_cast<int>(threadIdx.x) == next) {
       const std::uint64_t t0 = globaltimer();
       std::uint64_t v;
-      while ((v = ld_relaxed_sys(R.credit + next)) < R.need_credit) {
+      while ((v = ld_relaxed_sys(R.credit + next)) < need) {
         if (globaltimer() - t0 > P.timeout_ns) {
-          ll_fail(R, next, 0, v, R.need_credit);
+          ll_fail(R, next, 0, v, need);
           break;
         }
       }
@@ -1198,7 +1239,7 @@ __global__ void __launch_bounds__(kLLThreads, 3) ll128_kernel(const __grid_const
   if (logical == 0) {
     std::uint32_t k = 0;
     for (std::uint32_t g = warp; g * 4 < P.lines; g += warps, ++k) {
-      if (!room(k)) return;
+      if (!room(k)) break;
       const std::uint32_t line = g * 4 + sub;
       if (line >= P.lines) continue;
       const LineSeg sg = seg_of(P, li, line);
@@ -1210,11 +1251,10 @@ __global__ void __launch_bounds__(kLLThreads, 3) ll128_kernel(const __grid_const
       const unsigned long long b = part == 7 ? flag_of(k) : ll128_get(sg.buf, off + 8, l1, aligned);
       st_volatile_v2u64(ring_next + at(k), a, b);
     }
-    return;
   }
   bool ok = true;
   std::uint32_t k = 0;
-  for (std::uint32_t g = warp; g * 4 < P.lines && ok; g += warps, ++k) {
+  for (std::uint32_t g = logical == 0 ? P.lines : warp; g * 4 < P.lines && ok; g += warps, ++k) {
     const std::uint32_t line = g * 4 + sub;
     const bool active = line < P.lines;
     const unsigned long long flag = flag_of(k);
@@ -1259,8 +1299,14 @@ __global__ void __launch_bounds__(kLLThreads, 3) ll128_kernel(const __grid_const
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0 && ok) {
-    if (atomicAdd(R.done, 1ull) + 1 == R.done_target) st_relaxed_sys(R.peers->credit[source] + n + 1 + R.rank, P.epoch);
+  if (threadIdx.x == 0) {  // the rank's last CTA: advance the call state, credit the predecessor
+    CallState* st = s_state;
+    if (atomicAdd(&st->finished, 1ull) + 1 == static_cast<unsigned long long>(P.ctas)) {
+      st->finished = 0;
+      st->epoch = epoch;
+      if (writer) st->ll_last_ring = epoch;
+      if (logical != 0 && *(volatile int*)R.abort == 0) st_relaxed_sys(R.peers->credit[source] + n + 1 + R.rank, epoch);
+    }
   }
 }
 
@@ -1271,22 +1317,26 @@ __global__ void barrier_kernel(const __grid_constant__ BarrierParams B) {
   const int t = threadIdx.x;
   const int me = B.rank[local];
   const PeerTable* peers = B.peers[local];
+  __shared__ unsigned long long s_epoch;
+  if (t == 0) s_epoch = B.state[local]->bar_epoch + 1;  // one CTA per rank: read, then advanced below
+  __syncthreads();
+  const unsigned long long epoch = s_epoch;
   if (t < B.n_ranks && t != me) {
     fence_acq_rel_sys();
-    st_relaxed_sys(peers->bar[t] + me, B.epoch);
+    st_relaxed_sys(peers->bar[t] + me, epoch);
   }
   __syncthreads();
   if (t < B.n_ranks && t != me) {
     const std::uint64_t* slot = B.bar[local] + t;
     const std::uint64_t t0 = globaltimer();
-    while (ld_relaxed_sys(slot) < B.epoch) {
+    while (ld_relaxed_sys(slot) < epoch) {
       if (globaltimer() - t0 > B.timeout_ns) {
         ErrorRecord* e = B.err[local];
         if (atomicCAS(&e->code, 0, 1) == 0) {
           e->rank = me;
           e->peer = t;
           e->lane = -1;
-          e->expected = B.epoch;
+          e->expected = epoch;
           __threadfence_system();
         }
         break;
@@ -1295,6 +1345,7 @@ __global__ void barrier_kernel(const __grid_constant__ BarrierParams B) {
     (void)ld_acquire_sys(slot);
   }
   __syncthreads();
+  if (t == 0) B.state[local]->bar_epoch = epoch;
 }
 
 // Plain copy of one message slab (the DeviceFabric transport, bcl_fabric.cpp):
@@ -1386,7 +1437,11 @@ int local_chain_occupancy(int* blocks_per_sm) {
   return static_cast<int>(cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, dev::local_chain_kernel, 256, 0));
 }
 
-int ll128_occupancy(int* blocks_per_sm) {
+int ll128_occupancy(int* blocks_per_sm, int shared) {
+  if (shared) {
+    return static_cast<int>(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        blocks_per_sm, dev::ll128_kernel<dev::kMaxLocal, 1>, dev::kLLThreads, 0));
+  }
   return static_cast<int>(
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, dev::ll128_kernel<1, 1>, dev::kLLThreads, 0));
 }

@@ -115,13 +115,27 @@ __device__ __forceinline__ uint4 gather16(const std::uint8_t* s, std::uint32_t n
   return v;
 }
 
+// The rank's last CTA to finish: advance its call state (`advance` runs once).
+template <class F>
+__device__ void nvls_finish(const NvlsRank& R, int ctas, F advance) {
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(&R.state->finished, 1ull) + 1 == static_cast<unsigned long long>(ctas)) {
+    R.state->finished = 0;
+    advance(R.state);
+  }
+}
+
 template <int NL>
 __global__ void __launch_bounds__(kNvlsThreads) nvls_kernel(const __grid_constant__ NvlsParamsT<NL> P) {
   __shared__ int ok_sh;
+  __shared__ unsigned long long seq_sh;
   const int li = static_cast<int>(blockIdx.x) / P.ctas;
   const int j = static_cast<int>(blockIdx.x) % P.ctas;
   if (li >= P.n_local) return;
   const NvlsRank& R = P.ranks[li];
+  if (threadIdx.x == 0) seq_sh = R.state->nvls_seq;  // this call's first ring sequence number
+  __syncthreads();
+  const unsigned long long seq_base = seq_sh;
   std::uint64_t* mc_ready = reinterpret_cast<std::uint64_t*>(P.mc);
   std::uint64_t* mc_done = mc_ready + kNvlsMaxSlots;
   const std::uint64_t* uc_ready = reinterpret_cast<const std::uint64_t*>(P.uc);
@@ -129,7 +143,7 @@ __global__ void __launch_bounds__(kNvlsThreads) nvls_kernel(const __grid_constan
   const unsigned T = blockDim.x;
   const unsigned tid = threadIdx.x;
   for (std::uint32_t k = static_cast<std::uint32_t>(j); k < P.pieces; k += static_cast<std::uint32_t>(P.ctas)) {
-    const std::uint64_t seq = P.seq_base + k;
+    const std::uint64_t seq = seq_base + k;
     const std::uint32_t slot = static_cast<std::uint32_t>(seq % P.slots);
     const std::uint64_t round = seq / P.slots;
     const std::uint64_t off = static_cast<std::uint64_t>(k) * P.piece_bytes;
@@ -141,7 +155,7 @@ __global__ void __launch_bounds__(kNvlsThreads) nvls_kernel(const __grid_constan
       // The slot's previous occupant must be consumed by every receiver.
       if (round > 0 && !cta_wait_geq(R, uc_done + slot, static_cast<std::uint64_t>(P.n_recv) * round, P.timeout_ns, k,
                                      &ok_sh)) {
-        return;
+        break;
       }
       const std::uint8_t* src = R.buf + off;
       uint4* dst = reinterpret_cast<uint4*>(P.mc + data_off);
@@ -167,7 +181,7 @@ __global__ void __launch_bounds__(kNvlsThreads) nvls_kernel(const __grid_constan
         mc_add_release(mc_ready + slot, 1);
       }
     } else {
-      if (!cta_wait_geq(R, uc_ready + slot, round + 1, P.timeout_ns, k, &ok_sh)) return;
+      if (!cta_wait_geq(R, uc_ready + slot, round + 1, P.timeout_ns, k, &ok_sh)) break;
       const uint4* src = reinterpret_cast<const uint4*>(P.uc + data_off);
       std::uint8_t* dst = R.buf + off;
       if ((reinterpret_cast<std::uintptr_t>(dst) & 15u) == 0) {
@@ -204,6 +218,8 @@ __global__ void __launch_bounds__(kNvlsThreads) nvls_kernel(const __grid_constan
       }
     }
   }
+  const std::uint32_t pieces = P.pieces;
+  nvls_finish(R, P.ctas, [&](CallState* st) { st->nvls_seq = seq_base + pieces; });
 }
 
 __device__ __forceinline__ void mc_st_u4(void* p, std::uint32_t a, std::uint32_t b, std::uint32_t c,
@@ -219,16 +235,33 @@ __global__ void __launch_bounds__(512) nvls_ll_kernel(const __grid_constant__ Nv
   const int j = static_cast<int>(blockIdx.x) % P.ctas;
   if (li >= P.n_local) return;
   const NvlsRank& R = P.ranks[li];
+  __shared__ unsigned long long epoch_sh, need_sh;
+  if (threadIdx.x == 0) {  // the call's epoch and its half's reuse bound (device-side call state)
+    epoch_sh = R.state->nvls_ll_calls + 1;
+    need_sh = R.state->nvls_ll_reports[epoch_sh & 1u];
+  }
+  __syncthreads();
+  const unsigned long long epoch = epoch_sh;
+  const std::uint32_t half = static_cast<std::uint32_t>(epoch & 1u);
+  const std::uint32_t flag = static_cast<std::uint32_t>(epoch);
   const std::size_t area = (static_cast<std::size_t>(kNvlsCtlBytes) + kNvlsRingBytes) +
-                           static_cast<std::size_t>(P.half) * kNvlsLLLines * 16;
+                           static_cast<std::size_t>(half) * kNvlsLLLines * 16;
   const std::uint32_t first = static_cast<std::uint32_t>(j) * blockDim.x + threadIdx.x;
   const std::uint32_t stride = static_cast<std::uint32_t>(P.ctas) * blockDim.x;
   const bool aligned = (reinterpret_cast<std::uintptr_t>(R.buf) & 7u) == 0;
-  std::uint64_t* mc_done = reinterpret_cast<std::uint64_t*>(P.mc) + kNvlsLLDone + P.half;
-  const std::uint64_t* uc_done = reinterpret_cast<const std::uint64_t*>(P.uc) + kNvlsLLDone + P.half;
+  std::uint64_t* mc_done = reinterpret_cast<std::uint64_t*>(P.mc) + kNvlsLLDone + half;
+  const std::uint64_t* uc_done = reinterpret_cast<const std::uint64_t*>(P.uc) + kNvlsLLDone + half;
+  const unsigned long long reports = static_cast<unsigned long long>(P.n_recv) * static_cast<unsigned long long>(P.ctas);
+  auto advance = [&](CallState* st) {
+    st->nvls_ll_calls = epoch;
+    st->nvls_ll_reports[half] += reports;
+  };
   if (R.is_root) {
     // The half was last read two calls ago: every receiver CTA has reported.
-    if (P.need_done > 0 && !cta_wait_geq(R, uc_done, P.need_done, P.timeout_ns, 0, &ok_sh)) return;
+    if (need_sh > 0 && !cta_wait_geq(R, uc_done, need_sh, P.timeout_ns, 0, &ok_sh)) {
+      nvls_finish(R, P.ctas, advance);
+      return;
+    }
     uint4* dst = reinterpret_cast<uint4*>(P.mc + area);
     for (std::uint32_t i = first; i < P.lines; i += stride) {
       const std::uint64_t off = static_cast<std::uint64_t>(i) * 8;
@@ -243,8 +276,9 @@ __global__ void __launch_bounds__(512) nvls_ll_kernel(const __grid_constant__ Nv
           if (b < 4) lo |= byte << (8 * b); else hi |= byte << (8 * (b - 4));
         }
       }
-      mc_st_u4(dst + i, lo, P.epoch, hi, P.epoch);
+      mc_st_u4(dst + i, lo, flag, hi, flag);
     }
+    nvls_finish(R, P.ctas, advance);
     return;
   }
   const uint4* src = reinterpret_cast<const uint4*>(P.uc + area);
@@ -255,7 +289,7 @@ __global__ void __launch_bounds__(512) nvls_ll_kernel(const __grid_constant__ Nv
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                  : "l"(src + i)
                  : "memory");
-    if (v.y != P.epoch || v.w != P.epoch) {
+    if (v.y != flag || v.w != flag) {
       const std::uint64_t t0 = nv_timer();
       unsigned spins = 0;
       for (;;) {
@@ -263,7 +297,7 @@ __global__ void __launch_bounds__(512) nvls_ll_kernel(const __grid_constant__ Nv
                      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                      : "l"(src + i)
                      : "memory");
-        if (v.y == P.epoch && v.w == P.epoch) break;
+        if (v.y == flag && v.w == flag) break;
         if ((++spins & 1023u) == 0) {
           if (*(volatile int*)R.abort != 0) {
             ok = false;
@@ -277,7 +311,7 @@ __global__ void __launch_bounds__(512) nvls_ll_kernel(const __grid_constant__ Nv
               R.err->lane = static_cast<int>(blockIdx.x);
               R.err->chunk = i;
               R.err->observed = v.y;
-              R.err->expected = P.epoch;
+              R.err->expected = flag;
               __threadfence_system();
             }
             ok = false;
@@ -298,6 +332,7 @@ __global__ void __launch_bounds__(512) nvls_ll_kernel(const __grid_constant__ Nv
   }
   __syncthreads();
   if (threadIdx.x == 0 && ok) mc_add_release(mc_done, 1);  // this CTA's lines of the half are read
+  nvls_finish(R, P.ctas, advance);
 }
 
 }  // namespace
@@ -645,7 +680,7 @@ std::unique_ptr<NvlsTeam> NvlsTeam::create_local(const std::vector<int>& devices
     CUdevice cdev{};
     cu(d.DeviceGet(&cdev, dv), "cuDeviceGet");
     cu(d.MulticastAddDevice(t->handle_, cdev), "cuMulticastAddDevice");
-    t->bindings_.push_back(Binding{dv, 0, 0, 0, 0, false});
+    t->bindings_.push_back(Binding{dv, 0, 0, 0, false});
   }
   for (Binding& b : t->bindings_) t->bind_device(b);
   return t;
@@ -655,7 +690,7 @@ std::unique_ptr<NvlsTeam> NvlsTeam::create_owner(int n_devices, int device) {
   const Driver& d = drv();
   std::unique_ptr<NvlsTeam> t(new NvlsTeam());
   t->n_devices_ = n_devices;
-  t->bindings_.push_back(Binding{device, 0, 0, 0, 0, false});
+  t->bindings_.push_back(Binding{device, 0, 0, 0, false});
   // The POSIX descriptor of the object is handed to each importer over an
   // abstract Unix socket (SCM_RIGHTS). (Fabric handles would travel as bytes
   // but need an IMEX channel; exporting one without it fails with an unknown
@@ -707,7 +742,7 @@ std::unique_ptr<NvlsTeam> NvlsTeam::import(const std::uint8_t blob[kBlobBytes], 
   std::unique_ptr<NvlsTeam> t(new NvlsTeam());
   t->n_devices_ = b.n_devices;
   t->size_ = b.size;
-  t->bindings_.push_back(Binding{device, 0, 0, 0, 0, false});
+  t->bindings_.push_back(Binding{device, 0, 0, 0, false});
   CUmulticastObjectProp prop = mc_prop(b.n_devices, b.size, 0);
   std::size_t gran = 0;
   cu(d.MulticastGetGranularity(&gran, &prop, CU_MULTICAST_GRANULARITY_RECOMMENDED), "cuMulticastGetGranularity");
@@ -735,30 +770,6 @@ void NvlsTeam::add_device() {
 }
 
 void NvlsTeam::bind_and_map() { bind_device(bindings_.front()); }
-
-std::uint64_t NvlsTeam::take(int device, std::uint32_t pieces) {
-  for (Binding& b : bindings_) {
-    if (b.device == device) {
-      const std::uint64_t first = b.seq;
-      b.seq += pieces;
-      return first;
-    }
-  }
-  throw std::invalid_argument("NVLS: device not in the multicast team");
-}
-
-std::uint64_t NvlsTeam::take_ll(int device, std::uint64_t reports, std::uint64_t* need_done) {
-  for (Binding& b : bindings_) {
-    if (b.device == device) {
-      const std::uint64_t epoch = ++b.ll_calls;
-      std::uint64_t& half = b.ll_reports[epoch & 1u];
-      *need_done = half;
-      half += reports;
-      return epoch;
-    }
-  }
-  throw std::invalid_argument("NVLS: device not in the multicast team");
-}
 
 std::uint8_t* NvlsTeam::mc(int device) const {
   for (const Binding& b : bindings_) {

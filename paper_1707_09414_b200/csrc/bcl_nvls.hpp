@@ -14,7 +14,9 @@
 // Ring geometry: a 64 MiB ring of `slots` slots (slot size: the nvls_slot
 // option); the message is cut into pieces (<= one slot) identically on every
 // rank; piece k of a call occupies global sequence number seq_base + k,
-// slot = seq % slots, round = seq / slots.
+// slot = seq % slots, round = seq / slots. The sequence lives in each rank's
+// device-side call state (CallState::nvls_seq), advanced by the rank's last
+// CTA, identical on every rank.
 // Writers wait for done[slot] >= n_recv * round, readers for
 // ready[slot] >= round + 1 (monotone counters: never reset).
 #pragma once
@@ -49,6 +51,7 @@ struct NvlsRank {
   std::uint8_t* buf;
   ErrorRecord* err;
   int* abort;
+  CallState* state;         // nvls_seq / nvls_ll_* read at start, advanced by the rank's last CTA
 };
 
 template <int NL>
@@ -59,7 +62,6 @@ struct NvlsParamsT {
   std::uint32_t pieces;
   std::uint64_t bytes;
   std::uint64_t piece_bytes;
-  std::uint64_t seq_base;
   std::uint32_t slots;      // ring slots (kNvlsRingBytes / slot_bytes)
   std::uint32_t slot_bytes;
   std::uint64_t timeout_ns;
@@ -79,11 +81,9 @@ template <int NL>
 struct NvlsLLParamsT {
   int n_local;
   int ctas;                  // CTAs per local rank (identical on every GPU)
+  int n_recv;                // receiving ranks (each reports `ctas` CTAs per call)
   std::uint32_t lines;
   std::uint64_t bytes;
-  std::uint32_t epoch;       // line flag
-  std::uint32_t half;
-  std::uint64_t need_done;   // root: ll_done[half] must reach this first
   std::uint64_t timeout_ns;
   std::uint8_t* mc;
   std::uint8_t* uc;
@@ -131,15 +131,7 @@ class NvlsTeam {
   std::uint8_t* mc(int device) const;
   std::uint8_t* uc(int device) const;
   std::uint64_t size() const { return size_; }
-  // Reserve `pieces` ring sequence numbers for the next call on `device`;
-  // returns the first. Every GPU of the team walks the same sequence (one
-  // launch per GPU per call).
-  std::uint64_t take(int device, std::uint32_t pieces);
-  // NVLS-LL call sequence of `device` (identical on every GPU): returns the
-  // call's epoch (>= 1); *need_done = the receiver-CTA reports its half must
-  // have collected before the root overwrites it (all earlier calls on that
-  // half), then adds this call's `reports`.
-  std::uint64_t take_ll(int device, std::uint64_t reports, std::uint64_t* need_done);
+
   const std::string& handle_kind() const { return kind_; }
 
  private:
@@ -149,9 +141,6 @@ class NvlsTeam {
     unsigned long long mem{};  // CUmemGenericAllocationHandle
     unsigned long long uc{};   // CUdeviceptr
     unsigned long long mc{};
-    std::uint64_t seq{0};      // next ring sequence number of this GPU's launches
-    std::uint64_t ll_calls{0};  // NVLS-LL calls issued on this GPU
-    std::uint64_t ll_reports[2]{0, 0};  // receiver-CTA reports expected per half so far
     bool bound{false};
   };
   void bind_device(Binding& b);

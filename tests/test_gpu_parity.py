@@ -587,17 +587,60 @@ def test_layerwise_parameter_broadcast_fused(model):
             assert torch.equal(flats[r][off:off + size], flats[root][off:off + size]), (model, r, off)
 
 
-def test_graph_capture_is_refused():
-    """Kernel parameters carry host-side call epochs: a captured broadcast
-    would replay stale epochs, so capture fails loudly instead."""
-    n = 4
-    comms = comms_for(n)
-    bufs = [torch.zeros(4096, dtype=torch.uint8, device="cuda:0") for _ in range(n)]
-    s = torch.cuda.Stream()
-    g = torch.cuda.CUDAGraph()
-    with pytest.raises(ValueError, match="CUDA graph"):
+@pytest.mark.parametrize("variant", ["auto", "pull", "ll", "xpull", "xpush", "ll128"])
+def test_graph_capture_replays_fresh_epochs(variant):
+    """Epochs and the line protocols' reuse bookkeeping live on the device
+    (CallState), so a CUDA graph of broadcasts replays correctly: a captured
+    sequence (a chain call on the variant's path, a small direct call, a
+    device barrier, a grouped pair) replayed 6 times with a fresh payload
+    each time, interleaved with eager calls, every byte checked."""
+    n, m = 4, (1 << 20) + 3
+    options, proto = VARIANTS[variant]
+    comms = comms_for(n, options)
+    for c in comms:
+        c.set_protocol(proto)
+    try:
+        bufs = [torch.zeros(m, dtype=torch.uint8, device="cuda:0") for _ in range(n)]
+        small = [torch.zeros(777, dtype=torch.uint8, device="cuda:0") for _ in range(n)]
+        pair = [[torch.zeros(k, dtype=torch.uint8, device="cuda:0") for _ in range(n)] for k in (100, 5000)]
+        s = torch.cuda.Stream()
+        chain = cfg_of("chain_pipelined", 65536)
+
+        def body():
+            B.bcast_all(comms, bufs, m, "uint8", 1, chain, streams=[s] * n)
+            B.bcast_all(comms, small, 777, "uint8", 2, cfg_of("direct"), streams=[s] * n)
+            B.barrier_all(comms, streams=[s] * n)
+            with B.group():
+                for p in pair:
+                    B.bcast_all(comms, p, p[0].numel(), "uint8", 3, cfg_of("direct"), streams=[s] * n)
+
+        with torch.cuda.stream(s):
+            body()  # warm-up outside capture (lazy allocations happen here)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
-            B.bcast_all(comms, bufs, 4096, "uint8", 0, cfg_of("direct"), streams=[s] * n)
-    torch.cuda.synchronize()
-    B.bcast_all(comms, bufs, 4096, "uint8", 0, cfg_of("direct"))  # the communicator still works
-    torch.cuda.synchronize()
+            body()
+        torch.cuda.synchronize()
+        for rep in range(6):
+            vals = [(rep * 4 + k) % 251 + 1 for k in range(4)]
+            for r in range(n):
+                bufs[r].fill_(vals[0] if r == 1 else 0)
+                small[r].fill_(vals[1] if r == 2 else 0)
+                for k, p in enumerate(pair):
+                    p[r].fill_(vals[2 + k] if r == 3 else 0)
+            torch.cuda.synchronize()
+            with torch.cuda.stream(s):  # (calls on one communicator must be ordered: one stream)
+                g.replay()
+                if rep % 2:  # eager calls between replays keep the device state moving
+                    B.bcast_all(comms, small, 777, "uint8", 2, cfg_of("direct"), streams=[s] * n)
+            torch.cuda.synchronize()
+            for r in range(n):
+                assert int(bufs[r].min()) == vals[0] == int(bufs[r].max()), (variant, rep, r)
+                assert int(small[r].min()) == vals[1] == int(small[r].max()), (variant, rep, r)
+                for k, p in enumerate(pair):
+                    assert int(p[r].min()) == vals[2 + k] == int(p[r].max()), (variant, rep, k, r)
+        for c in comms:
+            c.check()
+    finally:
+        for c in comms:
+            c.set_protocol("auto")

@@ -363,3 +363,65 @@ def test_one_gibibyte_across_gpus_every_transport():
             assert torch.equal(bufs[r], src.to(f"cuda:{devices[r]}")), (proto, r)
     for c in comms:
         c.set_protocol("auto")
+
+
+@needs2
+@pytest.mark.parametrize("proto", ["auto", "pull", "push", "nvls"])
+def test_graph_capture_replays_across_gpus(proto):
+    """Captured broadcasts across GPUs (LL128 / pull / push / NVLS): the
+    device-side call state gives every replay a fresh epoch and ring
+    position; 5 replays with fresh payloads, every byte checked."""
+    devices = list(range(min(ngpu(), 4)))
+    n = len(devices)
+    comms = B.Comm.local(devices, timeout_s=10)
+    if proto == "nvls" and not comms[0].nvls()[0]:
+        pytest.skip("no multicast team")
+    for c in comms:
+        c.set_protocol(proto)
+    sizes = [(8 << 20) + 5, 3000]
+    bufs = [[torch.zeros(m, dtype=torch.uint8, device=f"cuda:{d}") for d in devices] for m in sizes]
+    streams = [torch.cuda.Stream(device=f"cuda:{d}") for d in devices]
+
+    def body():
+        for k, m in enumerate(sizes):
+            B.bcast_all(comms, bufs[k], m, "uint8", (k + 1) % n, cfg_of("chain_pipelined", 262144), streams=streams)
+
+    body()  # warm-up outside capture
+    for d in devices:
+        torch.cuda.synchronize(d)
+    # one process, several GPUs: capture every GPU's stream into one graph
+    # (the other streams join the capturing stream through events)
+    g = torch.cuda.CUDAGraph()
+    cap = streams[0]
+    ev = [torch.cuda.Event() for _ in devices]
+    with torch.cuda.graph(g, stream=cap):
+        start = torch.cuda.Event()
+        start.record(cap)
+        for i, st in enumerate(streams[1:], 1):
+            st.wait_event(start)
+        body()
+        for i, st in enumerate(streams[1:], 1):
+            ev[i].record(st)
+            cap.wait_event(ev[i])
+    for d in devices:
+        torch.cuda.synchronize(d)
+    try:
+        for rep in range(5):
+            vals = [(rep * 2 + k) % 250 + 3 for k in range(2)]
+            for k in range(2):
+                for r in range(n):
+                    bufs[k][r].fill_(vals[k] if r == (k + 1) % n else 0)
+            for d in devices:
+                torch.cuda.synchronize(d)
+            with torch.cuda.stream(cap):
+                g.replay()
+            for d in devices:
+                torch.cuda.synchronize(d)
+            for k in range(2):
+                for r in range(n):
+                    assert int(bufs[k][r].min()) == vals[k] == int(bufs[k][r].max()), (proto, rep, k, r)
+        for c in comms:
+            c.check()
+    finally:
+        for c in comms:
+            c.set_protocol("auto")
