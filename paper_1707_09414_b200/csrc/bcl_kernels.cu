@@ -47,6 +47,15 @@ namespace {
 
 constexpr int kRing = 16;  // pending publishes per copy warp
 
+// Whether this CTA is the last of its rank's `ctas` to finish (a single-CTA
+// launch is, without the round trip of the counter).
+__device__ __forceinline__ bool last_cta(CallState* st, int ctas) {
+  if (ctas == 1) return true;
+  if (atomicAdd(&st->finished, 1ull) + 1 != static_cast<unsigned long long>(ctas)) return false;
+  st->finished = 0;
+  return true;
+}
+
 __device__ __forceinline__ std::uint64_t ld_relaxed_sys(const std::uint64_t* p) {
   std::uint64_t v;
   asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -834,10 +843,7 @@ __global__ void __launch_bounds__(kThreads, NL == 1 ? 1 : BCL_SHARED_MIN_BLOCKS)
     // CTA of the rank to finish advances the rank's epoch.
     if ((threadIdx.x & 31) == 0) {
       CallState* st = state_sh;
-      if (atomicAdd(&st->finished, 1ull) + 1 == static_cast<unsigned long long>(P.ctas_per_rank)) {
-        st->finished = 0;
-        st->epoch = epoch_sh;
-      }
+      if (last_cta(st, P.ctas_per_rank)) st->epoch = epoch_sh;
     }
     return;
   }
@@ -1091,8 +1097,7 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ 
     // receiver, tells the source every line of this epoch has been read, so
     // the source may reuse the half.
     CallState* st = R.state;
-    if (atomicAdd(&st->finished, 1ull) + 1 == static_cast<unsigned long long>(P.ctas)) {
-      st->finished = 0;
+    if (last_cta(st, P.ctas)) {
       st->epoch = epoch;
       if (writer) (chain ? st->ll_last_chain : st->ll_last_direct)[half] = epoch;
       if (logical != 0 && *(volatile int*)R.abort == 0) {
@@ -1301,8 +1306,7 @@ __global__ void __launch_bounds__(kLLThreads, NL == 1 ? 3 : 2) ll128_kernel(cons
   __syncthreads();
   if (threadIdx.x == 0) {  // the rank's last CTA: advance the call state, credit the predecessor
     CallState* st = s_state;
-    if (atomicAdd(&st->finished, 1ull) + 1 == static_cast<unsigned long long>(P.ctas)) {
-      st->finished = 0;
+    if (last_cta(st, P.ctas)) {
       st->epoch = epoch;
       if (writer) st->ll_last_ring = epoch;
       if (logical != 0 && *(volatile int*)R.abort == 0) st_relaxed_sys(R.peers->credit[source] + n + 1 + R.rank, epoch);

@@ -119,7 +119,8 @@ __device__ __forceinline__ uint4 gather16(const std::uint8_t* s, std::uint32_t n
 template <class F>
 __device__ void nvls_finish(const NvlsRank& R, int ctas, F advance) {
   __syncthreads();
-  if (threadIdx.x == 0 && atomicAdd(&R.state->finished, 1ull) + 1 == static_cast<unsigned long long>(ctas)) {
+  if (threadIdx.x == 0 &&
+      (ctas == 1 || atomicAdd(&R.state->finished, 1ull) + 1 == static_cast<unsigned long long>(ctas))) {
     R.state->finished = 0;
     advance(R.state);
   }
