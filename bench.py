@@ -273,6 +273,9 @@ def main():
     ap.add_argument("--bucket", type=int, default=0, help="parameter workloads: coalesce tensors into >= this")
     ap.add_argument("--fused", action="store_true",
                     help="parameter workloads: issue the per-tensor broadcasts inside one bcl_group_start/end")
+    ap.add_argument("--graph", action="store_true",
+                    help="parameter workloads: capture one iteration's broadcasts (ours and NCCL's) in a CUDA graph "
+                         "and replay it per step")
     ap.add_argument("--csv", default=None, help="N>1: write the sweep as the reference bench CSV here")
     ap.add_argument("--fixed-chunk", dest="tuned", action="store_false",
                     help="N>1: pipelined chain with --chunk instead of the tuned selection")
@@ -711,12 +714,34 @@ def bench_params(args, torch, rank, world):
                     stream.synchronize()
                     dist.barrier(device_ids=[local])
 
-            def body(it):
+            def issue():
                 if impl == "ours":
                     pb.bcast(comm, flat, root, stream)
                 else:
                     for v in views:
                         nccl_direct.bcast(v, v.numel(), root, stream)
+
+            graph = None
+            per_iter = None
+            if args.graph:  # one eager iteration (lazy setup), then capture one
+                l_eager = comm.launches
+                with torch.cuda.stream(stream):
+                    issue()
+                per_iter = comm.launches - l_eager  # our kernels per replayed iteration
+                stream.synchronize()
+                dist.barrier(device_ids=[local])
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, stream=stream):
+                    issue()
+                stream.synchronize()
+                dist.barrier(device_ids=[local])
+
+            def body(it):
+                if graph is None:
+                    issue()
+                else:
+                    with torch.cuda.stream(stream):
+                        graph.replay()
 
             def verify(it):
                 return all(torch.equal(flat[o:o + n], ref[o:o + n]) for o, n in zip(pb.offsets, pb.sizes))
@@ -727,8 +752,15 @@ def bench_params(args, torch, rank, world):
             gate = max(GATE_CYCLES, 40_000 * len(pb.msgs))
             times = time_steps(torch, args.steps, args.warmup, prepare, body, verify, stream,
                                align=lambda: comm.barrier(stream), gate=gate)
+            if graph is not None:  # destroy it now: NCCL's communicator cannot go while a graph holds its work
+                stream.synchronize()
+                graph = None
+                torch.cuda.synchronize()
             if impl == "ours":  # our kernels in the timed steps (the barrier kernels excluded)
-                launches_total += (comm.launches - l0) * args.steps // (args.steps + args.warmup)
+                if per_iter is not None:
+                    launches_total += per_iter * args.steps
+                else:
+                    launches_total += (comm.launches - l0) * args.steps // (args.steps + args.warmup)
             t = torch.tensor(times, dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             results[(root, impl)] = statistics.mean(t.cpu().tolist())
@@ -742,7 +774,8 @@ def bench_params(args, torch, rank, world):
                 "data": "synthetic parameters (random bytes), torchvision layer shapes",
                 "config": {"workload": f"{args.workload}: {len(pb.sizes)} tensors, {sum(pb.sizes)} bytes, "
                                        f"{len(pb.msgs)} broadcasts per iteration (bucket {args.bucket} B"
-                                       f"{', grouped: bcl_group_start/end' if args.fused else ''}), roots {roots}",
+                                       f"{', grouped: bcl_group_start/end' if args.fused else ''}"
+                                       f"{', CUDA graph replay (ours and NCCL)' if args.graph else ''}), roots {roots}",
                            "tensors": len(pb.sizes), "bytes": sum(pb.sizes), "messages": len(pb.msgs)},
                 "per_root_ms": {str(r): {"ours": round(results[(r, 'ours')] * 1e3, 4),
                                          "nccl": round(results[(r, 'nccl')] * 1e3, 4)} for r in roots},
