@@ -252,3 +252,18 @@ def test_call_overhead_extends_the_reference_model():
         assert b.predicted_cost_s == pytest.approx(a.predicted_cost_s + a0, rel=1e-9)
     with pytest.raises(ValueError):
         B.cost_for(cands[0], 4, 100, call_overhead_s=-1.0)
+
+
+def test_group_calls_without_a_gpu():
+    """bcl_group_start/end are host bookkeeping: nesting works, an end without
+    a start is a contract error, an empty group flushes nothing."""
+    from paper_1707_09414_b200 import _lib
+    lib = B.lib()
+    assert lib.bcl_group_start() == 0
+    assert lib.bcl_group_start() == 0
+    assert lib.bcl_group_end() == 0
+    assert lib.bcl_group_end() == 0
+    with pytest.raises(ValueError, match="group_end without group_start"):
+        _lib._check(lib.bcl_group_end())
+    with B.group():
+        pass
