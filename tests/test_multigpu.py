@@ -425,3 +425,16 @@ def test_graph_capture_replays_across_gpus(proto):
     finally:
         for c in comms:
             c.set_protocol("auto")
+
+
+@needs2
+def test_soak_every_transport_groups_and_graphs():
+    """tools/r2/soak.py, short: random calls across every transport, schedule,
+    root and size, grouped runs, barriers and a replayed CUDA graph, every
+    byte checked after each step."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "tools", "r2", "soak.py"), "150", "11"],
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "soak ok" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
