@@ -282,7 +282,9 @@ bcl_status_t bcl_mem_reset(bcl_comm_t c);
  * count*size(dtype)), n, root, M), rank, buf, fabric) (runtime.hpp:134-138).
  * In place on a device buffer, enqueued on `stream` (cudaStream_t, NULL =
  * legacy default stream); config NULL = tuned. Asynchronous: device errors
- * surface from bcl_comm_check(). */
+ * surface from bcl_comm_check(). Capturable into a CUDA graph (call epochs
+ * live on the device; issue the call once before capturing so lazy
+ * allocations are done); calls on one communicator must be stream-ordered. */
 bcl_status_t bcl_bcast(void* buf, size_t count, bcl_dtype_t dtype, int root,
                        bcl_comm_t comm, const bcl_config_t* config, void* stream);
 /* Same with a HOST buffer: H2D at the root, device broadcast, D2H elsewhere. */
