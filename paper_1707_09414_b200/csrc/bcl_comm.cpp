@@ -872,7 +872,7 @@ void Group::launch_local_chain(const std::vector<int>& locals, const std::vector
     P.buf[logical] = static_cast<std::uint8_t*>(bufs[i]);
     P.rank[logical] = r.rank;
     P.prov[logical] = r.prov;
-    const std::uint64_t e = ++r.epoch;  // keep call counts aligned with the other paths
+    const std::uint64_t e = ++r.epoch;  // (host count: only checks that local ranks stay in step)
     if (i == 0) epoch = e;
     if (e != epoch) throw std::runtime_error("ranks sharing a GPU drifted apart in call count");
     ++r.launches;
@@ -1228,7 +1228,7 @@ void Group::launch_group(const std::vector<int>& locals, const std::vector<void*
     fill_rank_work(P.ranks[i], r, p, bufs[i], bytes);
     ++r.launches;
   }
-  P.epoch = epoch;
+  P.epoch = epoch;  // (informational: the kernel takes the call's epoch from the device-side call state)
   DeviceScope ds(local_[static_cast<std::size_t>(locals[0])].device);
   ck(static_cast<cudaError_t>(launch_bcast(P, P.n_local > 1 ? 1 : 0, stream)), "launch(bcast)");
 }

@@ -2,8 +2,10 @@
 // run_bcast / execute_rank boundary (proj/include/bcastlab/runtime.hpp:20-143).
 //
 //   Group         owns the device state of the ranks this process drives:
-//                 per-rank flag/ack/mailbox region, the peer table, the call
-//                 epoch and host-mapped error records. Two ways to build one:
+//                 per-rank flag/ack/mailbox region (with the device-side call
+//                 state: epochs advance on the device, so captured CUDA graphs
+//                 replay correctly), the peer table and host-mapped error
+//                 records. Two ways to build one:
 //                 * create_local(devices): one process drives every rank, one
 //                   rank per entry of `devices` (UVA + peer access; several
 //                   ranks may share a GPU — they then run in one launch);
@@ -147,8 +149,7 @@ struct LocalRank {
   dev::PeerTable h_peers{};
   dev::ErrorRecord* err_host{};
   dev::ErrorRecord* err_dev{};
-  std::uint64_t epoch{0};
-  std::uint64_t bar_epoch{0};
+  std::uint64_t epoch{0};        // host call count (local-rank lockstep check; kernels use the device CallState)
   std::uint8_t* heap{};
   std::size_t heap_bytes{};
   std::size_t heap_used{};
