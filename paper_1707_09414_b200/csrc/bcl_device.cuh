@@ -240,6 +240,9 @@ struct BarrierParams {
 }  // namespace dev
 
 // Launchers (bcl_kernels.cu). Return cudaError_t as int.
+// Fills attr[] (room for 2) for a launch: cooperative, or programmatic stream
+// serialization; returns the count. (cudaLaunchAttribute from cuda_runtime.h.)
+int fill_launch_attrs(struct cudaLaunchAttribute_st* attr, int cooperative);
 int launch_bcast(const dev::LaunchParams& p, int cooperative, void* stream);
 int launch_barrier(const dev::BarrierParams& p, void* stream);
 int launch_ll(const dev::LLParams& p, void* stream);

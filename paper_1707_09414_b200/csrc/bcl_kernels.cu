@@ -24,6 +24,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -46,6 +47,12 @@ namespace dev {
 namespace {
 
 constexpr int kRing = 16;  // pending publishes per copy warp
+
+// Programmatic dependent launch: with the stream-serialization attribute a
+// kernel may be scheduled before the previous kernel of its stream has
+// finished; everything it reads (the call state, user buffers) may be that
+// kernel's output, so it waits here first (a no-op without the attribute).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // Whether this CTA is the last of its rank's `ctas` to finish (a single-CTA
 // launch is, without the round trip of the counter).
@@ -813,6 +820,7 @@ __device__ void run_events(Ctx& c, int pipe, int q, int ns) {
 // no spills; the 3-CTA bound spilled 224 bytes).
 template <int NL>
 __global__ void __launch_bounds__(kThreads, NL == 1 ? 1 : BCL_SHARED_MIN_BLOCKS) bcast_kernel(const __grid_constant__ LaunchParamsT<NL> P) {
+  pdl_wait();
   __shared__ CtaShared sh;
   const int local = NL == 1 ? 0 : static_cast<int>(blockIdx.x) / P.ctas_per_rank;
   const int cta = NL == 1 ? static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x) % P.ctas_per_rank;
@@ -993,6 +1001,7 @@ __device__ __forceinline__ LineSeg seg_of(const LLParamsT<NL, NS>& P, int li, st
 
 template <int NL, int NS>
 __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ LLParamsT<NL, NS> P) {
+  pdl_wait();
   const int li = NL == 1 ? 0 : static_cast<int>(blockIdx.x) / P.ctas;
   const LLRank& R = P.ranks[li];
   const std::uint32_t cta = NL == 1 ? blockIdx.x : blockIdx.x % P.ctas;
@@ -1153,6 +1162,7 @@ __device__ __forceinline__ void ll128_put(std::uint8_t* buf, std::uint64_t off, 
 // GPU, is compiled for 2 so it does not spill at 42 registers.)
 template <int NL, int NS>
 __global__ void __launch_bounds__(kLLThreads, NL == 1 ? 3 : 2) ll128_kernel(const __grid_constant__ LLParamsT<NL, NS> P) {
+  pdl_wait();
   const int li = NL == 1 ? 0 : static_cast<int>(blockIdx.x) / P.ctas;
   const LLRank& R = P.ranks[li];
   const std::uint32_t cta = NL == 1 ? blockIdx.x : blockIdx.x % P.ctas;
@@ -1317,6 +1327,7 @@ __global__ void __launch_bounds__(kLLThreads, NL == 1 ? 3 : 2) ll128_kernel(cons
 // All-ranks barrier: rank r bumps slot [r] in every peer, then waits for
 // every peer's bump in its own slots.
 __global__ void barrier_kernel(const __grid_constant__ BarrierParams B) {
+  pdl_wait();
   const int local = blockIdx.x;
   const int t = threadIdx.x;
   const int me = B.rank[local];
@@ -1377,6 +1388,28 @@ __global__ void __launch_bounds__(512) peer_copy_kernel(std::uint8_t* __restrict
 }  // namespace
 }  // namespace dev
 
+// Launch attributes shared by the launchers: cooperative when asked, else
+// programmatic stream serialization, so a broadcast kernel is scheduled while
+// the previous kernel of its stream drains and starts the moment it is done
+// (back to back, N = 2: 5.2 -> 3.2 us per small broadcast;
+// profiles/round2/pdl/). BCL_PDL=0 turns it off.
+int fill_launch_attrs(cudaLaunchAttribute_st* attr, int cooperative) {
+  static const bool pdl = [] {
+    const char* v = std::getenv("BCL_PDL");
+    return v == nullptr || std::atoi(v) != 0;
+  }();
+  int k = 0;
+  attr[k].id = cudaLaunchAttributeCooperative;
+  attr[k].val.cooperative = cooperative ? 1 : 0;
+  ++k;
+  if (!cooperative && pdl) {
+    attr[k].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[k].val.programmaticStreamSerializationAllowed = 1;
+    ++k;
+  }
+  return k;
+}
+
 int launch_peer_copy(std::uint8_t* dst, const std::uint8_t* src, std::uint64_t len, void* stream) {
   const std::uint64_t nvec = (len + 15) / 16;
   const unsigned blocks = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(296, (nvec + 511) / 512)));
@@ -1424,11 +1457,9 @@ int launch_bcast(const dev::LaunchParams& p, int cooperative, void* stream) {
   cfg.blockDim = dim3(dev::kThreads);
   cfg.dynamicSmemBytes = p.stage_bytes ? bcast_smem_bytes(p.stages, p.stage_bytes) : 0;
   cfg.stream = static_cast<cudaStream_t>(stream);
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = cooperative ? 1 : 0;
+  cudaLaunchAttribute attr[2];
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = static_cast<unsigned>(fill_launch_attrs(attr, cooperative));
   // Same header layout: copy the header and the ranks into the smallest
   // parameter block that holds them (a 10 KB block for 16 ranks costs launch
   // latency; 4 ranks sharing a GPU is the emulated bench shape).
@@ -1460,11 +1491,9 @@ int launch_barrier(const dev::BarrierParams& p, void* stream) {
   cfg.gridDim = dim3(static_cast<unsigned>(p.n_local));
   cfg.blockDim = dim3(dev::kMaxRanks);
   cfg.stream = static_cast<cudaStream_t>(stream);
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = p.n_local > 1 ? 1 : 0;
+  cudaLaunchAttribute attr[2];
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = static_cast<unsigned>(fill_launch_attrs(attr, p.n_local > 1 ? 1 : 0));
   return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::barrier_kernel, p));
 }
 
@@ -1498,13 +1527,11 @@ int launch_ll(const dev::LLParams& p, void* stream) {
   cfg.gridDim = dim3(static_cast<unsigned>(p.n_local * p.ctas));
   cfg.blockDim = dim3(dev::kLLThreads);
   cfg.stream = static_cast<cudaStream_t>(stream);
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
+  cudaLaunchAttribute attr[2];
+  cfg.attrs = attr;
   // LL128 writers wait on ring credits from the successor's CTAs: co-residency
   // is required even for one rank per GPU (the successor's warp w may be any CTA).
-  attr[0].val.cooperative = (p.n_local > 1 || (p.chain == 2 && p.coop)) ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = static_cast<unsigned>(fill_launch_attrs(attr, (p.n_local > 1 || (p.chain == 2 && p.coop)) ? 1 : 0));
   if (p.n_seg < 1 || p.n_seg > dev::max_segs(p.n_local)) return static_cast<int>(cudaErrorInvalidValue);
   const bool fused = p.n_seg > 1;
   if (p.n_local == 1) return fused ? launch_ll_as<1, dev::kMaxSegs>(cfg, p) : launch_ll_as<1, 1>(cfg, p);

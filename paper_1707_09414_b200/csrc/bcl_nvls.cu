@@ -128,6 +128,7 @@ __device__ void nvls_finish(const NvlsRank& R, int ctas, F advance) {
 
 template <int NL>
 __global__ void __launch_bounds__(kNvlsThreads) nvls_kernel(const __grid_constant__ NvlsParamsT<NL> P) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (programmatic dependent launch: see bcl_kernels.cu)
   __shared__ int ok_sh;
   __shared__ unsigned long long seq_sh;
   const int li = static_cast<int>(blockIdx.x) / P.ctas;
@@ -231,6 +232,7 @@ __device__ __forceinline__ void mc_st_u4(void* p, std::uint32_t a, std::uint32_t
 
 template <int NL>
 __global__ void __launch_bounds__(512) nvls_ll_kernel(const __grid_constant__ NvlsLLParamsT<NL> P) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __shared__ int ok_sh;
   const int li = static_cast<int>(blockIdx.x) / P.ctas;
   const int j = static_cast<int>(blockIdx.x) % P.ctas;
@@ -368,11 +370,9 @@ int launch_nvls_ll(const dev::NvlsLLParams& p, void* stream) {
   cfg.gridDim = dim3(static_cast<unsigned>(p.n_local * p.ctas));
   cfg.blockDim = dim3(512);
   cfg.stream = static_cast<cudaStream_t>(stream);
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = p.n_local > 1 ? 1 : 0;
+  cudaLaunchAttribute attr[2];
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = static_cast<unsigned>(fill_launch_attrs(attr, p.n_local > 1 ? 1 : 0));
   if (p.n_local == 1) {
     dev::NvlsLLParamsT<1> one;
     std::memcpy(&one, &p, offsetof(dev::NvlsLLParams, ranks));
@@ -387,12 +387,10 @@ int launch_nvls(const dev::NvlsParams& p, void* stream) {
   cfg.gridDim = dim3(static_cast<unsigned>(p.n_local * p.ctas));
   cfg.blockDim = dim3(dev::kNvlsThreads);
   cfg.stream = static_cast<cudaStream_t>(stream);
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  // The root and the receivers sharing its GPU wait on one another.
-  attr[0].val.cooperative = p.n_local > 1 ? 1 : 0;
+  cudaLaunchAttribute attr[2];
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  // The root and the receivers sharing its GPU wait on one another.
+  cfg.numAttrs = static_cast<unsigned>(fill_launch_attrs(attr, p.n_local > 1 ? 1 : 0));
   if (p.n_local == 1) {
     dev::NvlsParamsT<1> one;
     std::memcpy(&one, &p, offsetof(dev::NvlsParams, ranks));
