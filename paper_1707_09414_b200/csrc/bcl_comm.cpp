@@ -1144,6 +1144,8 @@ void Group::launch_ll_segs(const std::vector<int>& locals, const std::vector<std
     w.buf = static_cast<std::uint8_t*>(seg_bufs.front()[i]);
     w.credit = r.region + 4 * S + static_cast<std::size_t>(n_) + 1 + (chain ? static_cast<std::size_t>(n_) + 1 : 0);
     w.wcredit = r.region + 4 * S + 3 * static_cast<std::size_t>(n_) + 2;
+    w.wseq = w.wcredit + dev::kLL128WarpsMax;
+    w.rseq = w.wseq + dev::kLL128WarpsMax;
     w.ll = reinterpret_cast<uint4*>(r.region + ll_offset(lanes_));
     w.peers = r.d_peers;
     w.err = r.err_dev;

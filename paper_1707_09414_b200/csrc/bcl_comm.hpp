@@ -298,7 +298,7 @@ class Group {
   // Offset (in 8-byte words) of the LL landing area for a flag stride of L lanes.
   std::size_t ll_offset(int lanes) const {
     const std::size_t w = 4 * static_cast<std::size_t>(n_) * lanes + 3 * static_cast<std::size_t>(n_) + 2 +
-                          static_cast<std::size_t>(dev::kLL128WarpsMax);
+                          3 * static_cast<std::size_t>(dev::kLL128WarpsMax);  // wcredit | wseq | rseq
     return (w + 31) / 32 * 32;  // 256-byte aligned: warp stores of LL lines cover whole 128-byte lines
   }
   std::uint64_t ll_max_{dev::kLLMaxBytes};  // LL protocol threshold (bytes), direct schedule

@@ -62,7 +62,8 @@ enum ChunkMode : std::uint32_t {
 
 // Addresses of every peer's state as mapped in *this* rank's address space.
 // Region layout of a rank (8-byte words): flags[n][L] | acks[n][L] | mbox[n][L][2]
-// | bar[n] | abort | credit[n] | ll_done | chain_credit[n] | wcredit[kLL128WarpsMax] | pad to 256 B
+// | bar[n] | abort | credit[n] | ll_done | chain_credit[n] | wcredit[kLL128WarpsMax]
+// | wseq[kLL128WarpsMax] | rseq[kLL128WarpsMax] | pad to 256 B
 // | ll[n][2][ll_lines] (16-byte lines, ll_lines = the group's LL cap / 8) | chain LL [2][chain_lines]
 // | LL128 ring [kLL128RingLines] (128-byte lines).
 struct PeerTable {
@@ -167,6 +168,8 @@ struct LLRank {
   uint4* ll;                  // local landing area base
   std::uint64_t* credit;      // local credit array [n] of this call's kind (direct, or chain: LL and LL128)
   std::uint64_t* wcredit;     // local LL128 per-warp ring credits [kLL128WarpsMax] (written by the successor)
+  std::uint64_t* wseq;        // local: groups each warp has written into the successor's ring, all calls
+  std::uint64_t* rseq;        // local: groups each warp has read from this rank's ring, all calls
   const PeerTable* peers;
   ErrorRecord* err;
   int* abort;

@@ -1184,20 +1184,14 @@ __global__ void __launch_bounds__(kLLThreads, NL == 1 ? 3 : 2) ll128_kernel(cons
   const int next = (R.rank + 1) % n;
   const int source = (R.rank + n - 1) % n;
   const bool writer = logical + 1 < n;
-  if (writer) {  // the successor finished reading our previous LL128 call (ring reuse across calls)
-    const std::uint64_t need = s_state->ll_last_ring;
-    if (need > 0 && static_cast<int>(threadIdx.x) == next) {
-      const std::uint64_t t0 = globaltimer();
-      std::uint64_t v;
-      while ((v = ld_relaxed_sys(R.credit + next)) < need) {
-        if (globaltimer() - t0 > P.timeout_ns) {
-          ll_fail(R, next, 0, v, need);
-          break;
-        }
-      }
-    }
-    __syncthreads();
-  }
+  // Ring positions continue across calls: warp w's groups into its
+  // successor's ring are numbered by wseq[w] (this rank's count of groups it
+  // wrote there, over every call) and read back by the successor's warp w by
+  // its rseq[w] (the same count). A call therefore never waits for the
+  // previous call to drain: only each slot's own credit gates its reuse.
+  // (32-bit positions, compared modulo 2^32: the registers LL128 can spare)
+  const std::uint32_t wbase = writer ? static_cast<std::uint32_t>(R.wseq[warp]) : 0u;
+  const std::uint32_t rbase = logical > 0 ? static_cast<std::uint32_t>(R.rseq[warp]) : 0u;
   // `line` counts from its segment's first line; `bytes` = the segment's.
   auto piece = [&](std::uint32_t line, std::uint64_t bytes, std::uint64_t* off, std::uint32_t* len0,
                    std::uint32_t* len1) {
@@ -1213,33 +1207,37 @@ __global__ void __launch_bounds__(kLLThreads, NL == 1 ? 3 : 2) ll128_kernel(cons
   ulonglong2* ring_next = writer ? reinterpret_cast<ulonglong2*>(R.peers->ll[next] + P.chain128_area) : nullptr;
   const std::uint64_t* my_credit = R.wcredit + warp;  // our successor's consumption of our groups
   std::uint64_t* prev_credit = logical > 0 ? R.peers->wcredit[source] + warp : nullptr;
-  const unsigned long long ctag = epoch << 32;
-  auto at = [&](std::uint32_t k) -> std::size_t {  // this thread's 16-byte word of group k's slot
-    return ((static_cast<std::size_t>(warp) * kLL128Depth + k % kLL128Depth) * 4 + sub) * 8 + part;
+  // This thread's 16-byte word of the slot of ring position q, and the flag
+  // a line at position q carries (its lap + 1: a slot's previous content is
+  // one lap older, a zeroed ring matches nothing).
+  auto at = [&](std::uint32_t q) -> std::size_t {
+    return ((static_cast<std::size_t>(warp) * kLL128Depth + q % kLL128Depth) * 4 + sub) * 8 + part;
   };
-  auto flag_of = [&](std::uint32_t k) -> unsigned long long { return (epoch << 20) | (k / kLL128Depth); };
-  // Warp-collective: the successor has consumed our group k - D (its slot is
-  // free). The last credit seen is cached (warp-uniform), so the local credit
-  // word is polled about once per D / 2 groups. Like NCCL's LL128 credits the
-  // overwrite is ordered after the poll by its control dependency (no acquire:
-  // an acquire invalidates L1 on every call, ~6% at 64 MiB, n = 4).
-  unsigned long long seen = 0;
-  auto room = [&](std::uint32_t k) -> bool {
-    if (k < static_cast<std::uint32_t>(kLL128Depth)) return true;
-    const unsigned long long want = ctag | (k - kLL128Depth + 1);
-    if (seen >= want) return true;
+  auto flag_of = [&](std::uint32_t q) -> unsigned long long { return q / kLL128Depth + 1u; };
+  // Warp-collective: the successor has consumed our position q - D (its slot
+  // is free); credits count positions consumed, over every call. The last
+  // credit seen is cached (warp-uniform), so the local credit word is polled
+  // about once per D / 2 groups. Like NCCL's LL128 credits the overwrite is
+  // ordered after the poll by its control dependency (no acquire: an acquire
+  // invalidates L1 on every call, ~6% at 64 MiB, n = 4).
+  std::uint32_t seen = 0;
+  bool seen_any = false;
+  auto room = [&](std::uint32_t q) -> bool {
+    const std::uint32_t want = q - kLL128Depth + 1;  // consumed positions needed (modulo 2^32)
+    if (q + 1 <= static_cast<std::uint32_t>(kLL128Depth) && wbase == 0) return true;  // the ring's first lap
+    if (seen_any && static_cast<std::int32_t>(seen - want) >= 0) return true;
     int ok = 1;
-    unsigned long long v = 0;
+    std::uint32_t v = 0;
     if (lane == 0) {
-      v = ld_volatile_u64(my_credit);
-      if (v < want) {
+      v = static_cast<std::uint32_t>(ld_volatile_u64(my_credit));
+      if (static_cast<std::int32_t>(v - want) < 0) {
         const std::uint64_t t0 = globaltimer();
         unsigned spins = 0;
-        while ((v = ld_volatile_u64(my_credit)) < want) {
+        while (static_cast<std::int32_t>((v = static_cast<std::uint32_t>(ld_volatile_u64(my_credit))) - want) < 0) {
           if ((++spins & 1023u) == 0) {
             if (*(volatile int*)R.abort != 0) { ok = 0; break; }
             if (globaltimer() - t0 > P.timeout_ns) {
-              ll_fail(R, next, k, v, want);
+              ll_fail(R, next, q, v, want);
               ok = 0;
               break;
             }
@@ -1249,12 +1247,13 @@ __global__ void __launch_bounds__(kLLThreads, NL == 1 ? 3 : 2) ll128_kernel(cons
     }
     ok = __shfl_sync(0xffffffffu, ok, 0);
     seen = __shfl_sync(0xffffffffu, v, 0);
+    seen_any = true;
     return ok != 0;
   };
+  std::uint32_t k = 0;  // groups this warp moved in this call
   if (logical == 0) {
-    std::uint32_t k = 0;
     for (std::uint32_t g = warp; g * 4 < P.lines; g += warps, ++k) {
-      if (!room(k)) break;
+      if (!room(wbase + k)) break;
       const std::uint32_t line = g * 4 + sub;
       if (line >= P.lines) continue;
       const LineSeg sg = seg_of(P, li, line);
@@ -1263,21 +1262,20 @@ __global__ void __launch_bounds__(kLLThreads, NL == 1 ? 3 : 2) ll128_kernel(cons
       std::uint32_t l0, l1;
       piece(line - sg.line0, sg.bytes, &off, &l0, &l1);
       const unsigned long long a = ll128_get(sg.buf, off, l0, aligned);
-      const unsigned long long b = part == 7 ? flag_of(k) : ll128_get(sg.buf, off + 8, l1, aligned);
-      st_volatile_v2u64(ring_next + at(k), a, b);
+      const unsigned long long b = part == 7 ? flag_of(wbase + k) : ll128_get(sg.buf, off + 8, l1, aligned);
+      st_volatile_v2u64(ring_next + at(wbase + k), a, b);
     }
   }
   bool ok = true;
-  std::uint32_t k = 0;
   for (std::uint32_t g = logical == 0 ? P.lines : warp; g * 4 < P.lines && ok; g += warps, ++k) {
     const std::uint32_t line = g * 4 + sub;
     const bool active = line < P.lines;
-    const unsigned long long flag = flag_of(k);
+    const unsigned long long flag = flag_of(rbase + k);
     ulonglong2 v = make_ulonglong2(0, 0);
     const std::uint64_t t0 = globaltimer();
     unsigned spins = 0;
     while (true) {
-      if (active) v = ld_volatile_v2u64(ring_self + at(k));
+      if (active) v = ld_volatile_v2u64(ring_self + at(rbase + k));
       const bool stale = active && part == 7 && v.y != flag;
       if (!__any_sync(0xffffffffu, stale)) break;
       if ((++spins & 1023u) == 0) {
@@ -1290,12 +1288,12 @@ __global__ void __launch_bounds__(kLLThreads, NL == 1 ? 3 : 2) ll128_kernel(cons
       }
     }
     if (!ok) break;
-    if (writer) {  // forward the very same line into the successor's ring
-      if (!room(k)) {
+    if (writer) {  // forward the same line into the successor's ring (at our position, with its flag)
+      if (!room(wbase + k)) {
         ok = false;
         break;
       }
-      if (active) st_volatile_v2u64(ring_next + at(k), v.x, v.y);
+      if (active) st_volatile_v2u64(ring_next + at(wbase + k), v.x, part == 7 ? flag_of(wbase + k) : v.y);
     }
     if (active) {
       const LineSeg sg = seg_of(P, li, line);
@@ -1306,22 +1304,20 @@ __global__ void __launch_bounds__(kLLThreads, NL == 1 ? 3 : 2) ll128_kernel(cons
       ll128_put(sg.buf, off, l0, aligned, v.x);
       if (part != 7) ll128_put(sg.buf, off + 8, l1, aligned, v.y);
     }
-    if ((k + 1) % (kLL128Depth / 2) == 0) {
+    if ((rbase + k + 1) % (kLL128Depth / 2) == 0) {
       // Every lane's loads of these groups have returned (their values were
       // stored above), so the predecessor may overwrite the slots.
       __syncwarp();
-      if (lane == 0) st_relaxed_sys(prev_credit, ctag | (k + 1));
+      if (lane == 0) st_relaxed_sys(prev_credit, rbase + k + 1);
     }
+  }
+  // The warp's ring positions after this call (warp-private counters).
+  if (lane == 0 && ok) {
+    if (writer) R.wseq[warp] = wbase + k;
+    if (logical > 0) R.rseq[warp] = rbase + k;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {  // the rank's last CTA: advance the call state, credit the predecessor
-    CallState* st = s_state;
-    if (last_cta(st, P.ctas)) {
-      st->epoch = epoch;
-      if (writer) st->ll_last_ring = epoch;
-      if (logical != 0 && *(volatile int*)R.abort == 0) st_relaxed_sys(R.peers->credit[source] + n + 1 + R.rank, epoch);
-    }
-  }
+  if (threadIdx.x == 0 && last_cta(s_state, P.ctas)) s_state->epoch = epoch;  // the rank's last CTA
 }
 
 // All-ranks barrier: rank r bumps slot [r] in every peer, then waits for
