@@ -266,6 +266,8 @@ def main():
     ap.add_argument("--bytes", type=int, default=64 << 20)
     ap.add_argument("--chunk", type=int, default=512 << 10)
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--b2b-max", type=int, default=1 << 20,
+                    help="N>1 sweep: also time 50 back-to-back calls up to this size")
     ap.add_argument("--sweep-max", type=int, default=1 << 30)
     ap.add_argument("--cpu-iters", type=int, default=12)
     ap.add_argument("--workload", default="config1", choices=["config1", "vgg16", "alexnet", "resnet50", "lenet"],
@@ -580,7 +582,7 @@ def bench_multi(args, torch, rank, world):
             theirs = run(size, steps, 3, False, None, flush=False)
             to, tn = statistics.median(ours), statistics.median(theirs)
             b2b = None
-            if size <= (1 << 20):  # CUDA events tick every ~2 us here: average 50 back-to-back calls too
+            if size <= args.b2b_max:  # CUDA events tick every ~2 us here: average 50 back-to-back calls too
                 bo, bn = back_to_back(size, True), back_to_back(size, False)
                 b2b = {"ours_us": round(bo * 1e6, 3), "nccl_us": round(bn * 1e6, 3), "vs_nccl": verdict(bo, bn)}
             nv = None

@@ -1171,14 +1171,6 @@ __global__ void __launch_bounds__(kLLThreads, NL == 1 ? 3 : 2) ll128_kernel(cons
   const int sub = lane >> 3;  // line within the warp's group of four
   const std::uint32_t warp = (cta * blockDim.x + threadIdx.x) >> 5;
   const std::uint32_t warps = (static_cast<std::uint32_t>(P.ctas) * blockDim.x) >> 5;
-  __shared__ unsigned long long s_epoch;
-  __shared__ CallState* s_state;
-  if (threadIdx.x == 0) {
-    s_state = R.state;
-    s_epoch = s_state->epoch + 1;  // the call's epoch (device-side call state)
-  }
-  __syncthreads();
-  const unsigned long long& epoch = s_epoch;  // (read from shared where used: LL128 runs at 42 registers)
   const int n = P.n_ranks;
   const int logical = (R.rank - P.root + n) % n;
   const int next = (R.rank + 1) % n;
@@ -1189,9 +1181,12 @@ __global__ void __launch_bounds__(kLLThreads, NL == 1 ? 3 : 2) ll128_kernel(cons
   // wrote there, over every call) and read back by the successor's warp w by
   // its rseq[w] (the same count). A call therefore never waits for the
   // previous call to drain: only each slot's own credit gates its reuse.
-  // (32-bit positions, compared modulo 2^32: the registers LL128 can spare)
+  // (32-bit positions, compared modulo 2^32: the registers LL128 can spare.
+  // Loaded before the call-state barrier so the loads overlap.)
   const std::uint32_t wbase = writer ? static_cast<std::uint32_t>(R.wseq[warp]) : 0u;
   const std::uint32_t rbase = logical > 0 ? static_cast<std::uint32_t>(R.rseq[warp]) : 0u;
+  // (LL128 needs no call epoch while it runs: its lines carry ring laps; the
+  // rank's last CTA just advances the epoch at the end.)
   // `line` counts from its segment's first line; `bytes` = the segment's.
   auto piece = [&](std::uint32_t line, std::uint64_t bytes, std::uint64_t* off, std::uint32_t* len0,
                    std::uint32_t* len1) {
@@ -1220,50 +1215,46 @@ __global__ void __launch_bounds__(kLLThreads, NL == 1 ? 3 : 2) ll128_kernel(cons
   // about once per D / 2 groups. Like NCCL's LL128 credits the overwrite is
   // ordered after the poll by its control dependency (no acquire: an acquire
   // invalidates L1 on every call, ~6% at 64 MiB, n = 4).
+  // Lane 0 caches the last credit it saw; the first value is loaded when the
+  // kernel starts, so its latency overlaps the first payload loads / polls.
   std::uint32_t seen = 0;
-  bool seen_any = false;
+  if (writer && lane == 0) seen = static_cast<std::uint32_t>(ld_volatile_u64(my_credit));
   auto room = [&](std::uint32_t q) -> bool {
     const std::uint32_t want = q - kLL128Depth + 1;  // consumed positions needed (modulo 2^32)
-    if (q + 1 <= static_cast<std::uint32_t>(kLL128Depth) && wbase == 0) return true;  // the ring's first lap
-    if (seen_any && static_cast<std::int32_t>(seen - want) >= 0) return true;
     int ok = 1;
-    std::uint32_t v = 0;
-    if (lane == 0) {
-      v = static_cast<std::uint32_t>(ld_volatile_u64(my_credit));
-      if (static_cast<std::int32_t>(v - want) < 0) {
-        const std::uint64_t t0 = globaltimer();
-        unsigned spins = 0;
-        while (static_cast<std::int32_t>((v = static_cast<std::uint32_t>(ld_volatile_u64(my_credit))) - want) < 0) {
-          if ((++spins & 1023u) == 0) {
-            if (*(volatile int*)R.abort != 0) { ok = 0; break; }
-            if (globaltimer() - t0 > P.timeout_ns) {
-              ll_fail(R, next, q, v, want);
-              ok = 0;
-              break;
-            }
+    if (lane == 0 && static_cast<std::int32_t>(seen - want) < 0) {
+      const std::uint64_t t0 = globaltimer();
+      unsigned spins = 0;
+      while (static_cast<std::int32_t>((seen = static_cast<std::uint32_t>(ld_volatile_u64(my_credit))) - want) < 0) {
+        if ((++spins & 1023u) == 0) {
+          if (*(volatile int*)R.abort != 0) { ok = 0; break; }
+          if (globaltimer() - t0 > P.timeout_ns) {
+            ll_fail(R, next, q, seen, want);
+            ok = 0;
+            break;
           }
         }
       }
     }
-    ok = __shfl_sync(0xffffffffu, ok, 0);
-    seen = __shfl_sync(0xffffffffu, v, 0);
-    seen_any = true;
-    return ok != 0;
+    return __shfl_sync(0xffffffffu, ok, 0) != 0;
   };
   std::uint32_t k = 0;  // groups this warp moved in this call
   if (logical == 0) {
     for (std::uint32_t g = warp; g * 4 < P.lines; g += warps, ++k) {
-      if (!room(wbase + k)) break;
       const std::uint32_t line = g * 4 + sub;
-      if (line >= P.lines) continue;
-      const LineSeg sg = seg_of(P, li, line);
-      const bool aligned = (reinterpret_cast<std::uintptr_t>(sg.buf) & 7u) == 0;
-      std::uint64_t off;
-      std::uint32_t l0, l1;
-      piece(line - sg.line0, sg.bytes, &off, &l0, &l1);
-      const unsigned long long a = ll128_get(sg.buf, off, l0, aligned);
-      const unsigned long long b = part == 7 ? flag_of(wbase + k) : ll128_get(sg.buf, off + 8, l1, aligned);
-      st_volatile_v2u64(ring_next + at(wbase + k), a, b);
+      const bool active = line < P.lines;
+      unsigned long long a = 0, b = 0;
+      if (active) {  // payload first: its load overlaps the credit check
+        const LineSeg sg = seg_of(P, li, line);
+        const bool aligned = (reinterpret_cast<std::uintptr_t>(sg.buf) & 7u) == 0;
+        std::uint64_t off;
+        std::uint32_t l0, l1;
+        piece(line - sg.line0, sg.bytes, &off, &l0, &l1);
+        a = ll128_get(sg.buf, off, l0, aligned);
+        b = part == 7 ? flag_of(wbase + k) : ll128_get(sg.buf, off + 8, l1, aligned);
+      }
+      if (!room(wbase + k)) break;
+      if (active) st_volatile_v2u64(ring_next + at(wbase + k), a, b);
     }
   }
   bool ok = true;
@@ -1317,7 +1308,7 @@ __global__ void __launch_bounds__(kLLThreads, NL == 1 ? 3 : 2) ll128_kernel(cons
     if (logical > 0) R.rseq[warp] = rbase + k;
   }
   __syncthreads();
-  if (threadIdx.x == 0 && last_cta(s_state, P.ctas)) s_state->epoch = epoch;  // the rank's last CTA
+  if (threadIdx.x == 0 && last_cta(R.state, P.ctas)) R.state->epoch += 1;  // the rank's last CTA
 }
 
 // All-ranks barrier: rank r bumps slot [r] in every peer, then waits for
