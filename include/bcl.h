@@ -261,7 +261,8 @@ bcl_status_t bcl_comm_set_protocol(bcl_comm_t c, int protocol);
  * ranks share a GPU) on the run's most capable protocol (LL128 chain > LL
  * chain > LL direct), everything else launches as usual, in call order.
  * Every rank must issue the same calls between the same start/end (MPI
- * semantics); host-buffer and synchronous run_bcast calls cannot be grouped
+ * semantics), switching streams at the same calls (a stream change ends a
+ * run); host-buffer and synchronous run_bcast calls cannot be grouped
  * (BCL_ERR_INVALID_ARGUMENT). The paper's caller broadcasts every layer of a
  * model (configs 4/5): grouped, ResNet-50's 161 per-tensor broadcasts run in
  * ~10 launches. New on B200; no reference counterpart. */
