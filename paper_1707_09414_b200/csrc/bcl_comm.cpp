@@ -33,6 +33,7 @@ struct ExportInfo {
   std::uint64_t ll_max;        // LL landing-area geometry must agree across ranks
   std::uint64_t ll_chain_max;
   std::uint64_t ll128_max;
+  std::uint64_t d128_min;
   cudaUUID_t uuid;             // physical GPU identity (ordinals differ between processes)
   cudaIpcMemHandle_t region;
   cudaIpcMemHandle_t heap;
@@ -107,6 +108,7 @@ void set_option(GroupOptions& o, const std::string& key, const std::string& v) {
   else if (key == "ll128") o.ll128 = i32();
   else if (key == "ll128_coop") o.ll128_coop = i32() != 0;
   else if (key == "ll128_ctas") o.ll128_ctas = std::clamp(i32(), 0, dev::kLL128MaxCtas);
+  else if (key == "ll128_direct_min") o.ll128_direct_min = u64();
   else if (key == "protocol") {
     o.protocol = i32();
     if (o.protocol < 0 || o.protocol > 5) throw std::invalid_argument("protocol must be 0..5");
@@ -131,7 +133,7 @@ void set_option(GroupOptions& o, const std::string& key, const std::string& v) {
 
 constexpr const char* kOptionNames[] = {
     "poll_ns", "window_bytes", "min_slice", "max_ctas", "strict_sys", "sys_scope", "eager_post", "writer_fence",
-    "local_fused", "local_ctas", "local_item", "local_claim", "ll", "ll128", "ll128_coop", "ll128_ctas", "protocol", "ll_max", "ll_chain_max", "ll128_max",
+    "local_fused", "local_ctas", "local_item", "local_claim", "ll", "ll128", "ll128_coop", "ll128_ctas", "ll128_direct_min", "protocol", "ll_max", "ll_chain_max", "ll128_max",
     "host_piece", "stages", "stage_bytes", "nvls", "nvls_strict", "nvls_slot", "nvls_ctas", "nvls_ll_max"};
 
 }  // namespace
@@ -269,6 +271,15 @@ constexpr std::uint64_t kNoLimit = 1ull << 62;
 std::uint64_t ll128_cap(const GroupOptions& opt) {
   return opt.ll128_max_bytes < 0 ? kNoLimit : static_cast<std::uint64_t>(opt.ll128_max_bytes);
 }
+// LL128 direct threshold X (a multiple of 64, at most 0.45 of the LL cap):
+// 16-byte LL lines of messages below X fill at most the first 2X bytes of a
+// direct area, and the 128-byte lines of one up to the cap (at most
+// cap x 128/120 bytes) fit behind them, 128-byte aligned.
+std::uint64_t d128_cap(std::uint64_t ll_max, const GroupOptions& opt) {
+  if (opt.ll128_direct_min == 0 || ll_max % 64 != 0) return 0;
+  const std::uint64_t x = std::min<std::uint64_t>(opt.ll128_direct_min, ll_max * 45 / 100);
+  return std::max<std::uint64_t>(64, x / 64 * 64);
+}
 
 }  // namespace
 
@@ -325,6 +336,7 @@ std::shared_ptr<Group> Group::create_local(const std::vector<int>& devices, cons
   g->ll_chain_max_ = ll_chain_cap(opt);
   g->ll128_max_ = g->ll128_ok_ ? ll128_cap(opt) : 0;  // no LL128 ring without LL128
   g->ll128_ok_ = g->ll128_ok_ && g->ll128_max_ > 0;
+  g->d128_min_ = d128_cap(g->ll_max_, opt);
   g->cache_device_limits(devices[0]);
   g->local_.resize(static_cast<std::size_t>(n));
   for (int r = 0; r < n; ++r) {
@@ -391,6 +403,7 @@ std::shared_ptr<Group> Group::create_rank(int n, int rank, int device, std::size
   g->ll_max_ = ll_cap(n, opt);
   g->ll_chain_max_ = ll_chain_cap(opt);
   g->ll128_max_ = opt.ll128 != 0 ? ll128_cap(opt) : 0;
+  g->d128_min_ = d128_cap(g->ll_max_, opt);
   g->cache_device_limits(device);
   g->local_.resize(1);
   g->local_[0].rank = rank;
@@ -429,6 +442,7 @@ std::vector<std::uint8_t> Group::export_info() const {
   info.ll_max = ll_max_;
   info.ll_chain_max = ll_chain_max_;
   info.ll128_max = ll128_max_;
+  info.d128_min = d128_min_;
   {
     cudaDeviceProp prop{};
     ck(cudaGetDeviceProperties(&prop, r.device), "cudaGetDeviceProperties");
@@ -551,8 +565,10 @@ void Group::connect(const std::vector<std::vector<std::uint8_t>>& infos) {
     if (all[i].magic != kInfoMagic || all[i].n != n_ || all[i].rank != static_cast<int>(i)) {
       throw std::invalid_argument("info blobs must be ordered by rank and belong to this group");
     }
-    if (all[i].ll_max != ll_max_ || all[i].ll_chain_max != ll_chain_max_ || all[i].ll128_max != ll128_max_) {
-      throw std::invalid_argument("ranks disagree on the LL landing areas (BCL_LL_MAX / _CHAIN_MAX / LL128_MAX)");
+    if (all[i].ll_max != ll_max_ || all[i].ll_chain_max != ll_chain_max_ || all[i].ll128_max != ll128_max_ ||
+        all[i].d128_min != d128_min_) {
+      throw std::invalid_argument(
+          "ranks disagree on the LL landing areas (BCL_LL_MAX / _CHAIN_MAX / LL128_MAX / LL128_DIRECT_MIN)");
     }
     lanes = std::min(lanes, static_cast<int>(all[i].lanes));
   }
@@ -773,6 +789,15 @@ bool Group::use_nvls(const CallPlan& p, std::uint64_t bytes) const {
   }
   if (opt_.protocol != 0 || !nvls_ || bytes == 0) return false;
   return p.config.algorithm == Algorithm::Direct && !(bytes <= ll_max_ && opt_.ll);
+}
+
+// LL128 lines for the `direct` schedule: every rank on its own GPU, from
+// d128_min_ up to the LL threshold, whatever the protocol (like the 16-byte
+// LL direct lines it replaces there: 16-byte lines never land at or past the
+// LL128 lines' offset, so neither format ever reads the other's bytes).
+bool Group::use_ll128_direct(const CallPlan& p, std::uint64_t bytes) const {
+  if (!d128_min_ || !ll128_ok_ || single_device_ || !opt_.ll) return false;
+  return p.config.algorithm == Algorithm::Direct && bytes >= d128_min_ && bytes <= ll_max_;
 }
 
 void Group::launch_nvls_group(const std::vector<int>& locals, const std::vector<void*>& bufs, std::uint64_t bytes,
@@ -1082,14 +1107,14 @@ void Group::launch_ll(const std::vector<int>& locals, const std::vector<void*>& 
 }
 
 std::uint64_t Group::ll_lines_of(std::uint64_t bytes, int mode) {
-  return mode == 2 ? (bytes + dev::kLL128Payload - 1) / dev::kLL128Payload : (bytes + 7) / 8;
+  return mode >= 2 ? (bytes + dev::kLL128Payload - 1) / dev::kLL128Payload : (bytes + 7) / 8;
 }
 
 // One launch of a line protocol carrying one or more messages (segments):
 // seg_bufs[s][i] is local rank i's buffer of message s.
 void Group::launch_ll_segs(const std::vector<int>& locals, const std::vector<std::vector<void*>>& seg_bufs,
                            const std::vector<std::uint64_t>& seg_bytes, int root, cudaStream_t stream, int mode) {
-  const bool chain = mode != 0;
+  const bool chain = mode == 1 || mode == 2;
   dev::LLParams P{};
   P.n_ranks = n_;
   P.root = root;
@@ -1116,6 +1141,7 @@ void Group::launch_ll_segs(const std::vector<int>& locals, const std::vector<std
   P.chain_lines = static_cast<std::uint32_t>(ll_chain_max_ / 8);
   P.chain128_lines = ll128_lines();
   P.chain128_area = ll128_area();
+  P.d128_off = static_cast<std::uint32_t>(d128_min_ / 8);
   // ~4 lines per thread, at most kLLMaxCtas CTAs per rank
   // ~2 lines per thread; ranks sharing a GPU must stay co-resident
   // (cooperative launch): at most 4 LL CTAs per SM in total.
@@ -1129,6 +1155,10 @@ void Group::launch_ll_segs(const std::vector<int>& locals, const std::vector<std
     int cap = std::max(1, std::min(dev::kLL128MaxCtas, sms_ * std::max(occ, 1)) / P.n_local);
     if (opt_.ll128_ctas > 0) cap = std::min(cap, opt_.ll128_ctas);
     P.ctas = std::clamp<int>(static_cast<int>((P.lines + per_cta - 1) / per_cta), 1, cap);
+  }
+  if (mode == 3) {  // LL128 direct: a warp moves 4 lines per step, ~2 steps per warp; no co-residency needed
+    const std::uint32_t per_cta = dev::kLLThreads / 32 * 4 * 2;
+    P.ctas = std::clamp<int>(static_cast<int>((P.lines + per_cta - 1) / per_cta), 1, dev::kLLMaxCtas);
   }
   P.timeout_ns = opt_.timeout_ns;
   P.coop = opt_.ll128_coop ? 1 : 0;
@@ -1170,6 +1200,7 @@ std::string Group::path(const AlgorithmConfig* cfg, int root, std::uint64_t byte
   if (use_nvls(p, bytes)) {
     return bytes <= std::min<std::uint64_t>(opt_.nvls_ll_max, dev::kNvlsLLMaxBytes) ? "nvls_ll_kernel" : "nvls_kernel";
   }
+  if (use_ll128_direct(p, bytes)) return "ll128_kernel/direct";
   if (p.config.algorithm == Algorithm::Direct && bytes <= ll_max_ && opt_.ll) return "ll_kernel/direct";
   if (const int mode = ll_chain_mode(p, bytes, locals)) return mode == 2 ? "ll128_kernel" : "ll_kernel/chain";
   if (use_local_chain(p, locals)) return "local_chain_kernel";
@@ -1183,6 +1214,10 @@ void Group::launch_group(const std::vector<int>& locals, const std::vector<void*
                          std::uint64_t bytes, int root, const CallPlan& p, cudaStream_t stream) {
   if (use_nvls(p, bytes)) {
     launch_nvls_group(locals, bufs, bytes, root, stream);
+    return;
+  }
+  if (use_ll128_direct(p, bytes)) {
+    launch_ll(locals, bufs, bytes, root, stream, 3);
     return;
   }
   if (p.config.algorithm == Algorithm::Direct && bytes <= ll_max_ && opt_.ll) {
@@ -1329,7 +1364,7 @@ int Group::fuse_kind(const Deferred& d) {
   } else {
     locals.push_back(d.li);
   }
-  if (use_nvls(p, d.bytes)) return 0;
+  if (use_nvls(p, d.bytes) || use_ll128_direct(p, d.bytes)) return 0;  // (one message per launch)
   if (p.config.algorithm == Algorithm::Direct && d.bytes <= ll_max_ && opt_.ll) return 1;
   const int mode = ll_chain_mode(p, d.bytes, locals);
   if (mode == 1) return 2;
@@ -1366,7 +1401,8 @@ void Group::flush_deferred() {
       for (const auto& kv : by_device_) per_dev = std::max(per_dev, static_cast<int>(kv.second.size()));
       const std::size_t max_segs = static_cast<std::size_t>(dev::max_segs(d.all ? per_dev : 1));
       auto fits = [&](std::size_t end, int k) {
-        const std::uint64_t cap = k == 1 ? ll_max_ / 8 : k == 2 ? ll_chain_max_ / 8 : (1ull << 31) - 1;
+        // (LL direct lines stay below the LL128 direct lines' offset)
+        const std::uint64_t cap = k == 1 ? (d128_min_ ? d128_min_ / 8 : ll_max_ / 8) : k == 2 ? ll_chain_max_ / 8 : (1ull << 31) - 1;
         std::uint64_t lines = 0;
         for (std::size_t c = i; c < end; ++c) lines += ll_lines_of(calls[c].bytes, k - 1);
         return lines <= cap;

@@ -1311,6 +1311,114 @@ __global__ void __launch_bounds__(kLLThreads, NL == 1 ? 3 : 2) ll128_kernel(cons
   if (threadIdx.x == 0 && last_cta(R.state, P.ctas)) R.state->epoch += 1;  // the rank's last CTA
 }
 
+// LL128 lines for the `direct` schedule (chain == 3): the root writes each
+// 128-byte line (120 payload bytes, flag = the call's epoch in the last 8)
+// into every receiver's direct landing area for that source -- the area of
+// the 16-byte LL direct lines, from d128_off on, so that stale lines of the
+// other format never sit where a reader looks -- and receivers poll their
+// own copy line by line: half the root's egress of 16-byte LL lines. The
+// halves, the credits and the reuse rule are the LL direct ones (the same
+// memory). One call's lines fit the area: no ring, no co-residency needed.
+template <int NL>
+__global__ void __launch_bounds__(kLLThreads) ll128_direct_kernel(const __grid_constant__ LLParamsT<NL, 1> P) {
+  pdl_wait();
+  const int li = NL == 1 ? 0 : static_cast<int>(blockIdx.x) / P.ctas;
+  const LLRank& R = P.ranks[li];
+  const std::uint32_t cta = NL == 1 ? blockIdx.x : blockIdx.x % P.ctas;
+  const int lane = static_cast<int>(threadIdx.x & 31);
+  const int part = lane & 7;
+  const int sub = lane >> 3;
+  const std::uint32_t warp = (cta * blockDim.x + threadIdx.x) >> 5;
+  const std::uint32_t warps = (static_cast<std::uint32_t>(P.ctas) * blockDim.x) >> 5;
+  __shared__ unsigned long long s_epoch;
+  if (threadIdx.x == 0) s_epoch = R.state->epoch + 1;
+  __syncthreads();
+  const unsigned long long epoch = s_epoch;
+  const std::uint32_t half = static_cast<std::uint32_t>(epoch & 1u);
+  const int n = P.n_ranks;
+  const bool root = R.rank == P.root;
+  const std::size_t area = (static_cast<std::size_t>(P.root) * 2 + half) * P.area_lines + P.d128_off;
+  const bool aligned = (reinterpret_cast<std::uintptr_t>(R.buf) & 7u) == 0;
+  auto piece = [&](std::uint32_t line, std::uint64_t* off, std::uint32_t* len0, std::uint32_t* len1) {
+    *off = static_cast<std::uint64_t>(line) * kLL128Payload + static_cast<std::uint64_t>(part) * 16;
+    const std::uint64_t end = static_cast<std::uint64_t>(line) * kLL128Payload + kLL128Payload;
+    const std::uint64_t lim = end < P.bytes ? end : P.bytes;
+    auto clip = [&](std::uint64_t a) -> std::uint32_t { return a >= lim ? 0u : static_cast<std::uint32_t>(lim - a < 8 ? lim - a : 8); };
+    *len0 = clip(*off);
+    *len1 = part == 7 ? 0u : clip(*off + 8);
+  };
+  if (root) {
+    // The half was last written (LL or LL128 direct) in epoch need: its
+    // receivers must have read it.
+    const std::uint64_t need = R.state->ll_last_direct[half];
+    const int t = static_cast<int>(threadIdx.x);
+    if (need > 0 && t < n && t != P.root) {
+      const std::uint64_t t0 = globaltimer();
+      std::uint64_t v;
+      while ((v = ld_relaxed_sys(R.credit + t)) < need) {
+        if (globaltimer() - t0 > P.timeout_ns) {
+          ll_fail(R, t, 0, v, need);
+          break;
+        }
+      }
+    }
+    __syncthreads();
+    for (std::uint32_t g = warp; g * 4 < P.lines; g += warps) {
+      const std::uint32_t line = g * 4 + sub;
+      if (line >= P.lines) continue;
+      std::uint64_t off;
+      std::uint32_t l0, l1;
+      piece(line, &off, &l0, &l1);
+      const unsigned long long a = ll128_get(R.buf, off, l0, aligned);
+      const unsigned long long b = part == 7 ? epoch : ll128_get(R.buf, off + 8, l1, aligned);
+      const std::size_t at = area + static_cast<std::size_t>(line) * 8 + part;
+      for (int d = 0; d < n; ++d) {
+        if (d != P.root) st_volatile_v2u64(reinterpret_cast<ulonglong2*>(R.peers->ll[d] + at), a, b);
+      }
+    }
+  } else {
+    bool ok = true;
+    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(R.ll + area);
+    for (std::uint32_t g = warp; g * 4 < P.lines && ok; g += warps) {
+      const std::uint32_t line = g * 4 + sub;
+      const bool active = line < P.lines;
+      ulonglong2 v = make_ulonglong2(0, 0);
+      const std::uint64_t t0 = globaltimer();
+      unsigned spins = 0;
+      while (true) {
+        if (active) v = ld_volatile_v2u64(src + static_cast<std::size_t>(line) * 8 + part);
+        const bool stale = active && part == 7 && v.y != epoch;
+        if (!__any_sync(0xffffffffu, stale)) break;
+        if ((++spins & 1023u) == 0) {
+          const int give_up = (*(volatile int*)R.abort != 0 || globaltimer() - t0 > P.timeout_ns) ? 1 : 0;
+          if (__any_sync(0xffffffffu, give_up)) {
+            if (lane == 0 && *(volatile int*)R.abort == 0) ll_fail(R, P.root, line, 0, epoch);
+            ok = false;
+            break;
+          }
+        }
+      }
+      if (!ok) break;
+      if (active) {
+        std::uint64_t off;
+        std::uint32_t l0, l1;
+        piece(line, &off, &l0, &l1);
+        ll128_put(R.buf, off, l0, aligned, v.x);
+        if (part != 7) ll128_put(R.buf, off + 8, l1, aligned, v.y);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    CallState* st = R.state;
+    if (last_cta(st, P.ctas)) {
+      st->epoch = epoch;
+      if (root) st->ll_last_direct[half] = epoch;
+      else if (*(volatile int*)R.abort == 0) st_relaxed_sys(R.peers->credit[P.root] + R.rank, epoch);
+    }
+  }
+}
+
 // All-ranks barrier: rank r bumps slot [r] in every peer, then waits for
 // every peer's bump in its own slots.
 __global__ void barrier_kernel(const __grid_constant__ BarrierParams B) {
@@ -1497,6 +1605,10 @@ int launch_ll_as(cudaLaunchConfig_t& cfg, const dev::LLParams& p) {
   for (int i = 0; i < p.n_local; ++i) {
     q.ranks[i] = p.ranks[i];
     for (int s = 0; s < NS && s < p.n_seg; ++s) q.seg_buf[i][s] = p.seg_buf[i][s];
+  }
+  if (p.chain == 3) {  // LL128 direct: one message per launch
+    if constexpr (NS > 1) return static_cast<int>(cudaErrorInvalidValue);
+    else return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::ll128_direct_kernel<NL>, q));
   }
   if (p.chain == 2) {
     // (LL128 groups are not fused for ranks sharing a GPU: the 16-rank fused

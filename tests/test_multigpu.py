@@ -120,6 +120,69 @@ def test_ll128_chain_back_to_back_stress():
 
 
 @needs2
+def test_ll128_direct_lines():
+    """`direct` calls from ll128_direct_min up to the LL threshold travel as
+    128-byte LL128 lines behind the 16-byte LL lines of smaller calls in the
+    same landing areas: sizes around both thresholds and the 120-byte line
+    payload, every root, misaligned views, the two formats interleaved back to
+    back on the same halves (each result checked before the next call), a
+    grouped run (LL lines fused, LL128 direct lines one launch each)."""
+    devices = list(range(min(ngpu(), 8)))
+    n = len(devices)
+    comms = B.Comm.local(devices, timeout_s=10, ll128_direct_min=65536)
+    d = cfg_of("direct")
+    ll_max = comms[0].protocol_caps()["ll_direct"]
+    assert comms[0].path(65535, d) == "ll_kernel/direct"
+    assert comms[0].path(65536, d) == comms[0].path(ll_max, d) == "ll128_kernel/direct"
+    assert comms[0].path(ll_max + 1, d) != "ll128_kernel/direct"
+    for root in range(n):
+        for m in (65535, 65536, 65537, 120 * 600, 120 * 600 + 1, 1 << 20, ll_max - 1, ll_max, ll_max + 1):
+            run_group(comms, devices, "direct", root, m, seed=m + root)
+    rng = random.Random(29)
+    cap = ll_max + 64
+    bufs = [torch.empty(cap, dtype=torch.uint8, device=f"cuda:{x}") for x in devices]
+    for it in range(80):
+        m = rng.choice([rng.randrange(1, 65536), rng.randrange(65536, ll_max + 1)])
+        off = rng.randrange(0, 16) if it % 3 == 0 else 0
+        root = rng.randrange(n)
+        src = torch.randint(0, 256, (m,), dtype=torch.uint8, device=f"cuda:{devices[root]}")
+        views = [b[off:off + m] for b in bufs]
+        for r in range(n):
+            (views[r].copy_(src) if r == root else views[r].fill_(it & 0xFF))
+        torch.cuda.synchronize(devices[root])
+        B.run_bcast(comms, root, views, m, d)
+        for r in range(n):
+            assert torch.equal(views[r].cpu(), src.cpu()), (it, m, off, root, r)
+    sizes = [5000, 300000, 777, 70000, 40000, 2 << 20 if ll_max >= 2 << 20 else ll_max]
+    views, srcs, at = [], [], 0
+    for k, m in enumerate(sizes):
+        views.append([b[at:at + m] for b in bufs] if at + m <= cap else None)
+        at += m
+    views = [v for v in views if v is not None]
+    streams = [torch.cuda.Stream(device=f"cuda:{x}") for x in devices]
+    for k, v in enumerate(views):
+        src = torch.randint(0, 256, (v[0].numel(),), dtype=torch.uint8, device=f"cuda:{devices[k % n]}")
+        for r in range(n):
+            (v[r].copy_(src) if r == k % n else v[r].zero_())
+        srcs.append(src)
+    for x in devices:
+        torch.cuda.synchronize(x)
+    with B.group():
+        for k, v in enumerate(views):
+            B.bcast_all(comms, v, v[0].numel(), "uint8", k % n, d, streams=streams)
+    for x in devices:
+        torch.cuda.synchronize(x)
+    for k, (v, src) in enumerate(zip(views, srcs)):
+        for r in range(n):
+            assert torch.equal(v[r].cpu(), src.cpu()), ("group", k, r)
+    for c in comms:
+        c.check()
+    off = B.Comm.local(devices, timeout_s=10, ll128_direct_min=0)
+    assert off[0].path(1 << 20, d) == "ll_kernel/direct"
+    run_group(off, devices, "direct", n - 1, (1 << 20) + 3, seed=3)
+
+
+@needs2
 def test_pull_flag_ordering_litmus():
     """The default pull path publishes a slice after a gpu-scope fence of the
     producing warp (DESIGN.md §5 "Memory ordering": the producer's L2 is the

@@ -1,7 +1,9 @@
 #!/usr/bin/env python3
 """Dev A/B (torchrun, one process per GPU): device time of the pipelined
 chain per transport variant and size (GPU gate, device barrier, CUDA events,
-median of K, max over ranks). VARIANTS: ';'-separated "protocol[:k=v,...]"."""
+median of K, max over ranks). VARIANTS: ';'-separated "protocol[:k=v,...]";
+ALGO: the schedule (chain_pipelined, direct, ..., or "table": the tuned
+choice); B2B: calls per timed region (back to back, one event pair)."""
 import os, statistics, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch, torch.distributed as dist
@@ -16,6 +18,8 @@ sizes = [int(x) for x in os.environ.get("SIZES", "8388608,67108864,268435456,107
 chunk = int(os.environ.get("CHUNK", 65536))
 K = int(os.environ.get("ITERS", 10))
 variants = os.environ.get("VARIANTS", "ll128;ll128:ll128_coop=0;pull;push").split(";")
+B2B = int(os.environ.get("B2B", 1))
+ALGO = os.environ.get("ALGO", "chain_pipelined")
 mx = max(sizes)
 s = torch.cuda.Stream(device=dev)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -29,7 +33,8 @@ for v in variants:
     torch.cuda.synchronize()
     res = []
     for m in sizes:
-        cfg = B.AlgorithmConfig(B.Algorithm.chain_pipelined, 0, chunk)
+        cfg = None if ALGO == "table" else B.AlgorithmConfig(
+            B.Algorithm[ALGO], 2 if ALGO == "knomial" else 0, chunk if ALGO == "chain_pipelined" else 0)
         ts = []
         for it in range(3 + K):
             with torch.cuda.stream(s):
@@ -37,20 +42,21 @@ for v in variants:
                 torch.cuda._sleep(1_000_000)
             comm.barrier(s)
             e0.record(s)
-            comm.bcast(buf, m, "uint8", 0, cfg, stream=s)
+            for _ in range(B2B):
+                comm.bcast(buf, m, "uint8", 0, cfg, stream=s)
             e1.record(s)
             e1.synchronize()
             if it >= 3:
-                ts.append(e0.elapsed_time(e1) * 1e-3)
+                ts.append(e0.elapsed_time(e1) * 1e-3 / B2B)
         ok = torch.equal(buf[:m], ref[:m])
         t = torch.tensor(ts, dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         okt = torch.tensor([1.0 if ok else 0.0], device=dev)
         dist.all_reduce(okt, op=dist.ReduceOp.MIN)
         med = statistics.median(t.cpu().tolist())
-        res.append(f"{m >> 20}MiB {med * 1e6:.1f}us {m / med / 1e9:.0f}GB/s{'' if okt.item() else ' MISMATCH'}")
+        res.append(f"{m >> 10}KiB {med * 1e6:.1f}us {m / med / 1e9:.0f}GB/s{'' if okt.item() else ' MISMATCH'}")
     if rank == 0:
-        print(f"N={world} {v} [{comm.path(sizes[-1], cfg)}]: " + " | ".join(res), flush=True)
+        print(f"N={world} {v} {ALGO} b2b={B2B} [{comm.path(sizes[-1], cfg)}]: " + " | ".join(res), flush=True)
     comm.close()
 dist.barrier(device_ids=[local])
 dist.destroy_process_group()

@@ -26,8 +26,8 @@ from paper_1707_09414_b200.comm import DevicePtr  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--out", required=True)
-ap.add_argument("--min", type=int, default=4)
-ap.add_argument("--max", type=int, default=1 << 30)
+ap.add_argument("--min", "--min-bytes", dest="min", type=int, default=4)
+ap.add_argument("--max", "--max-bytes", dest="max", type=int, default=1 << 30)  # (--max-bytes under torchrun)
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--chunks", default="65536,131072,262144,524288,1048576,2097152,4194304")
 ap.add_argument("--cands", default="direct,knomial,scatter_ring_allgather,chain_pipelined")
