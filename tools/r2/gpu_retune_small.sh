@@ -2,6 +2,7 @@
 # Re-tune the n = 2 / n = 4 tables below 4 MiB with LL128 direct on (default),
 # raw latencies kept; spliced into the builtin table by hand (rows < 2965821).
 out=gpurun_out/retune_small; mkdir -p $out
+(cd paper_1707_09414_b200 && make -s >/dev/null)
 for n in 4 2; do
   devs=$( [ $n = 2 ] && echo 0,1 || echo 0,1,2,3 )
   CUDA_VISIBLE_DEVICES=$devs timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
