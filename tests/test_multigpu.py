@@ -441,13 +441,14 @@ def test_graph_capture_replays_across_gpus(proto):
         pytest.skip("no multicast team")
     for c in comms:
         c.set_protocol(proto)
-    sizes = [(8 << 20) + 5, 3000]
+    sizes = [(8 << 20) + 5, 3000, (1 << 20) + 9]  # the last one on the `direct` schedule (LL128 direct lines)
     bufs = [[torch.zeros(m, dtype=torch.uint8, device=f"cuda:{d}") for d in devices] for m in sizes]
     streams = [torch.cuda.Stream(device=f"cuda:{d}") for d in devices]
 
     def body():
         for k, m in enumerate(sizes):
-            B.bcast_all(comms, bufs[k], m, "uint8", (k + 1) % n, cfg_of("chain_pipelined", 262144), streams=streams)
+            cfg = cfg_of("direct") if k == 2 else cfg_of("chain_pipelined", 262144)
+            B.bcast_all(comms, bufs[k], m, "uint8", (k + 1) % n, cfg, streams=streams)
 
     body()  # warm-up outside capture
     for d in devices:
@@ -470,8 +471,8 @@ def test_graph_capture_replays_across_gpus(proto):
         torch.cuda.synchronize(d)
     try:
         for rep in range(5):
-            vals = [(rep * 2 + k) % 250 + 3 for k in range(2)]
-            for k in range(2):
+            vals = [(rep * 2 + k) % 250 + 3 for k in range(len(sizes))]
+            for k in range(len(sizes)):
                 for r in range(n):
                     bufs[k][r].fill_(vals[k] if r == (k + 1) % n else 0)
             for d in devices:
@@ -480,7 +481,7 @@ def test_graph_capture_replays_across_gpus(proto):
                 g.replay()
             for d in devices:
                 torch.cuda.synchronize(d)
-            for k in range(2):
+            for k in range(len(sizes)):
                 for r in range(n):
                     assert int(bufs[k][r].min()) == vals[k] == int(bufs[k][r].max()), (proto, rep, k, r)
         for c in comms:

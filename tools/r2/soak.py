@@ -34,7 +34,7 @@ def main():
     bufs = [torch.empty(cap + 64, dtype=torch.uint8, device=f"cuda:{d}") for d in devices]
     streams = [torch.cuda.Stream(device=f"cuda:{d}") for d in devices]
     # a captured graph: two broadcasts on fixed views, replayed between steps
-    gviews = [[torch.zeros(m, dtype=torch.uint8, device=f"cuda:{d}") for d in devices] for m in (3000, (2 << 20) + 7)]
+    gviews = [[torch.zeros(m, dtype=torch.uint8, device=f"cuda:{d}") for d in devices] for m in (3000, (2 << 20) + 7, (1 << 20) + 5)]
 
     def graph_body():
         for k, v in enumerate(gviews):
