@@ -271,14 +271,9 @@ constexpr std::uint64_t kNoLimit = 1ull << 62;
 std::uint64_t ll128_cap(const GroupOptions& opt) {
   return opt.ll128_max_bytes < 0 ? kNoLimit : static_cast<std::uint64_t>(opt.ll128_max_bytes);
 }
-// LL128 direct threshold X (a multiple of 64, at most 0.45 of the LL cap):
-// 16-byte LL lines of messages below X fill at most the first 2X bytes of a
-// direct area, and the 128-byte lines of one up to the cap (at most
-// cap x 128/120 bytes) fit behind them, 128-byte aligned.
+// LL128 direct threshold (0 = off: no LL128 direct landing areas either).
 std::uint64_t d128_cap(std::uint64_t ll_max, const GroupOptions& opt) {
-  if (opt.ll128_direct_min == 0 || ll_max % 64 != 0) return 0;
-  const std::uint64_t x = std::min<std::uint64_t>(opt.ll128_direct_min, ll_max * 45 / 100);
-  return std::max<std::uint64_t>(64, x / 64 * 64);
+  return opt.ll128_direct_min == 0 || opt.ll128_direct_min > ll_max ? 0 : opt.ll128_direct_min;
 }
 
 }  // namespace
@@ -793,8 +788,8 @@ bool Group::use_nvls(const CallPlan& p, std::uint64_t bytes) const {
 
 // LL128 lines for the `direct` schedule: every rank on its own GPU, from
 // d128_min_ up to the LL threshold, whatever the protocol (like the 16-byte
-// LL direct lines it replaces there: 16-byte lines never land at or past the
-// LL128 lines' offset, so neither format ever reads the other's bytes).
+// LL direct lines it replaces there). Inside a group such calls stay on
+// fused 16-byte LL lines (fuse_kind): one launch for many small messages.
 bool Group::use_ll128_direct(const CallPlan& p, std::uint64_t bytes) const {
   if (!d128_min_ || !ll128_ok_ || single_device_ || !opt_.ll) return false;
   return p.config.algorithm == Algorithm::Direct && bytes >= d128_min_ && bytes <= ll_max_;
@@ -1141,7 +1136,8 @@ void Group::launch_ll_segs(const std::vector<int>& locals, const std::vector<std
   P.chain_lines = static_cast<std::uint32_t>(ll_chain_max_ / 8);
   P.chain128_lines = ll128_lines();
   P.chain128_area = ll128_area();
-  P.d128_off = static_cast<std::uint32_t>(d128_min_ / 8);
+  P.d128_area = d128_area();
+  P.d128_lines = d128_lines();
   // ~4 lines per thread, at most kLLMaxCtas CTAs per rank
   // ~2 lines per thread; ranks sharing a GPU must stay co-resident
   // (cooperative launch): at most 4 LL CTAs per SM in total.
@@ -1364,7 +1360,9 @@ int Group::fuse_kind(const Deferred& d) {
   } else {
     locals.push_back(d.li);
   }
-  if (use_nvls(p, d.bytes) || use_ll128_direct(p, d.bytes)) return 0;  // (one message per launch)
+  if (use_nvls(p, d.bytes)) return 0;
+  // (LL128 direct calls too: grouped small messages are launch-bound, one
+  // fused launch of 16-byte lines beats a launch each)
   if (p.config.algorithm == Algorithm::Direct && d.bytes <= ll_max_ && opt_.ll) return 1;
   const int mode = ll_chain_mode(p, d.bytes, locals);
   if (mode == 1) return 2;
@@ -1401,8 +1399,7 @@ void Group::flush_deferred() {
       for (const auto& kv : by_device_) per_dev = std::max(per_dev, static_cast<int>(kv.second.size()));
       const std::size_t max_segs = static_cast<std::size_t>(dev::max_segs(d.all ? per_dev : 1));
       auto fits = [&](std::size_t end, int k) {
-        // (LL direct lines stay below the LL128 direct lines' offset)
-        const std::uint64_t cap = k == 1 ? (d128_min_ ? d128_min_ / 8 : ll_max_ / 8) : k == 2 ? ll_chain_max_ / 8 : (1ull << 31) - 1;
+        const std::uint64_t cap = k == 1 ? ll_max_ / 8 : k == 2 ? ll_chain_max_ / 8 : (1ull << 31) - 1;
         std::uint64_t lines = 0;
         for (std::size_t c = i; c < end; ++c) lines += ll_lines_of(calls[c].bytes, k - 1);
         return lines <= cap;

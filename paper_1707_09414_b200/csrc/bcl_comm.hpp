@@ -105,7 +105,7 @@ struct GroupOptions {
   bool ll = true;                                           // LL push protocol for small `direct` calls
   std::uint64_t ll128_direct_min = 128ull << 10;            // `direct` calls from this size up to the LL threshold
                                                             // travel as 128-byte LL128 lines (every rank on its own
-                                                            // GPU; 0 = never; at most 0.45 x the LL threshold):
+                                                            // GPU; 0 = never, no landing areas for them either):
                                                             // n = 4, 8 back to back, 1 MiB: 11.4 vs 15.4 us
   int protocol = 0;                                         // chain: 0 auto (table), 1 pull, 2 push
   std::uint64_t ll_max_bytes = 0;                           // LL threshold (0 = 2 MiB, lowered for many ranks)
@@ -309,8 +309,7 @@ class Group {
   std::uint64_t ll_chain_max_{0};           // LL pipelined chain up to this size (0 = off)
   std::uint64_t ll128_max_{0};              // LL128 pipelined chain up to this size (0 = off; the ring is bounded)
   bool ll128_ok_{false};                    // every rank on its own GPU (LL128 needs NVLink hops)
-  std::uint64_t d128_min_{0};               // LL128 direct from this size (0 = off); its lines start at 2 x this
-                                            // many bytes into the direct area, past any 16-byte LL line
+  std::uint64_t d128_min_{0};               // LL128 direct from this size (0 = off)
   bool use_ll128_direct(const CallPlan& p, std::uint64_t bytes) const;
   std::uint32_t ll128_lines() const { return ll128_max_ > 0 ? dev::kLL128RingLines : 0; }
   // LL128 area offset from the LL base (16-byte units), 128-byte aligned given
@@ -320,9 +319,15 @@ class Group {
     const std::size_t base_bytes = ll_offset(lanes_) * 8 + units * 16;
     return static_cast<std::uint32_t>(units + ((128 - base_bytes % 128) % 128) / 16);
   }
+  // LL128 direct landing areas [n sources][2 halves][d128_lines()] 128-byte
+  // lines, behind the LL128 ring (128-byte aligned like it).
+  std::uint32_t d128_lines() const {
+    return d128_min_ > 0 && ll128_lines() > 0 ? static_cast<std::uint32_t>((ll_max_ + 119) / 120) : 0;
+  }
+  std::uint32_t d128_area() const { return ll128_area() + ll128_lines() * 8; }
   std::size_t ll_words() const {            // 8-byte words of LL landing areas per rank (+ alignment pad)
     return (static_cast<std::size_t>(n_) * 2 * (ll_max_ / 8) + 2 * (ll_chain_max_ / 8)) * 2 +
-           static_cast<std::size_t>(ll128_lines()) * 16 + 16;
+           static_cast<std::size_t>(ll128_lines()) * 16 + static_cast<std::size_t>(n_) * 2 * d128_lines() * 16 + 16;
   }
 
   int n_{0};

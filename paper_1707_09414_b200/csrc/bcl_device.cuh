@@ -185,11 +185,12 @@ struct LLHeader {
   std::uint64_t bytes;        // one segment: its bytes
   std::uint32_t area_lines;   // lines per (source, half) landing area of the direct schedule
   std::uint32_t chain;        // 0 direct, 1 pipelined chain on 16-byte LL lines, 2 chain on 128-byte LL128 lines,
-                              // 3 direct on 128-byte LL128 lines (in the LL direct area, from d128_off)
+                              // 3 direct on 128-byte LL128 lines (in the LL128 direct areas)
   std::uint32_t chain_lines;  // lines per half of the chain landing area (after the direct areas)
   std::uint32_t chain128_lines;  // 128-byte lines of the LL128 ring (kLL128RingLines)
   std::uint32_t chain128_area;   // its offset from the LL base in 16-byte units (128-byte aligned)
-  std::uint32_t d128_off;        // LL128 direct: offset inside each (source, half) direct area, 16-byte units
+  std::uint32_t d128_area;       // LL128 direct areas [n][2][d128_lines]: offset from the LL base, 16-byte units
+  std::uint32_t d128_lines;      // 128-byte lines per (source, half)
   std::uint64_t timeout_ns;
   std::uint32_t coop;            // LL128, one rank per GPU: cooperative launch (co-residency guaranteed)
   int n_seg;                     // messages fused into this launch (bcl_group_*); 1 = an ordinary call

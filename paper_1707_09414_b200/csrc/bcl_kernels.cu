@@ -1313,12 +1313,12 @@ __global__ void __launch_bounds__(kLLThreads, NL == 1 ? 3 : 2) ll128_kernel(cons
 
 // LL128 lines for the `direct` schedule (chain == 3): the root writes each
 // 128-byte line (120 payload bytes, flag = the call's epoch in the last 8)
-// into every receiver's direct landing area for that source -- the area of
-// the 16-byte LL direct lines, from d128_off on, so that stale lines of the
-// other format never sit where a reader looks -- and receivers poll their
-// own copy line by line: half the root's egress of 16-byte LL lines. The
-// halves, the credits and the reuse rule are the LL direct ones (the same
-// memory). One call's lines fit the area: no ring, no co-residency needed.
+// into every receiver's LL128 direct landing area for that source and half,
+// and receivers poll their own copy line by line: half the root's egress of
+// 16-byte LL lines. The halves, the credits and the reuse rule are the LL
+// direct ones (a half is reused once its receivers credited the last call of
+// either format that wrote it). One call's lines fit the area: no ring, no
+// co-residency needed.
 template <int NL>
 __global__ void __launch_bounds__(kLLThreads) ll128_direct_kernel(const __grid_constant__ LLParamsT<NL, 1> P) {
   pdl_wait();
@@ -1337,7 +1337,7 @@ __global__ void __launch_bounds__(kLLThreads) ll128_direct_kernel(const __grid_c
   const std::uint32_t half = static_cast<std::uint32_t>(epoch & 1u);
   const int n = P.n_ranks;
   const bool root = R.rank == P.root;
-  const std::size_t area = (static_cast<std::size_t>(P.root) * 2 + half) * P.area_lines + P.d128_off;
+  const std::size_t area = P.d128_area + (static_cast<std::size_t>(P.root) * 2 + half) * P.d128_lines * 8;
   const bool aligned = (reinterpret_cast<std::uintptr_t>(R.buf) & 7u) == 0;
   auto piece = [&](std::uint32_t line, std::uint64_t* off, std::uint32_t* len0, std::uint32_t* len1) {
     *off = static_cast<std::uint64_t>(line) * kLL128Payload + static_cast<std::uint64_t>(part) * 16;

@@ -122,11 +122,11 @@ def test_ll128_chain_back_to_back_stress():
 @needs2
 def test_ll128_direct_lines():
     """`direct` calls from ll128_direct_min up to the LL threshold travel as
-    128-byte LL128 lines behind the 16-byte LL lines of smaller calls in the
-    same landing areas: sizes around both thresholds and the 120-byte line
-    payload, every root, misaligned views, the two formats interleaved back to
-    back on the same halves (each result checked before the next call), a
-    grouped run (LL lines fused, LL128 direct lines one launch each)."""
+    128-byte LL128 lines (their own landing areas, the LL direct halves and
+    credits): sizes around both thresholds and the 120-byte line payload,
+    every root, misaligned views, the two formats interleaved back to back on
+    the same halves (each result checked before the next call), a grouped run
+    (every message on fused 16-byte LL lines)."""
     devices = list(range(min(ngpu(), 8)))
     n = len(devices)
     comms = B.Comm.local(devices, timeout_s=10, ll128_direct_min=65536)
