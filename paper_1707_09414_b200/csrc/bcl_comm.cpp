@@ -786,12 +786,13 @@ bool Group::use_nvls(const CallPlan& p, std::uint64_t bytes) const {
   return p.config.algorithm == Algorithm::Direct && !(bytes <= ll_max_ && opt_.ll);
 }
 
-// LL128 lines for the `direct` schedule: every rank on its own GPU, from
-// d128_min_ up to the LL threshold, whatever the protocol (like the 16-byte
-// LL direct lines it replaces there). Inside a group such calls stay on
+// LL128 lines for the `direct` schedule: every rank on its own GPU (or, with
+// the ll128=1 option, ranks sharing one: the cross-GPU kernel through L2, one
+// cooperative launch), from d128_min_ up to the LL threshold, whatever the
+// protocol (like the 16-byte LL direct lines it replaces there). Inside a group such calls stay on
 // fused 16-byte LL lines (fuse_kind): one launch for many small messages.
 bool Group::use_ll128_direct(const CallPlan& p, std::uint64_t bytes) const {
-  if (!d128_min_ || !ll128_ok_ || single_device_ || !opt_.ll) return false;
+  if (!d128_min_ || !ll128_ok_ || !opt_.ll) return false;
   return p.config.algorithm == Algorithm::Direct && bytes >= d128_min_ && bytes <= ll_max_;
 }
 

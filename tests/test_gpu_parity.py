@@ -273,6 +273,35 @@ def test_back_to_back_calls_change_payload_and_root(variant):
             c.set_protocol("auto")
 
 
+@pytest.mark.parametrize("n", [2, 4, 7])
+def test_ll128_direct_lines_one_gpu(n):
+    """LL128 lines for the `direct` schedule (what runs across GPUs from 128
+    KiB up to the LL threshold), here through L2 with the ll128=1 option:
+    sizes around the threshold and the 120-byte line payload, every root,
+    misaligned views against the oracle, then back-to-back calls alternating
+    with 16-byte LL direct lines on the same halves."""
+    comms = comms_for(n, VARIANTS["ll128"][0])
+    d = cfg_of("direct")
+    assert comms[0].path(128 << 10, d) == comms[0].path(2 << 20, d) == "ll128_kernel/direct"
+    assert comms[0].path((128 << 10) - 1, d) == "ll_kernel/direct"
+    for root in range(n):
+        for m in ((128 << 10), 120 * 1200 + 1, (1 << 20) + 3, 2 << 20):
+            run_case("direct", n, root, m, seed=m + root, protocol="ll128")
+    run_case("direct", n, n - 1, (700 << 10) + 5, seed=3, offsets=[(5 * r) % 16 for r in range(n)], protocol="ll128")
+    bufs = [torch.zeros(2 << 20, dtype=torch.uint8, device="cuda:0") for _ in range(n)]
+    for it in range(30):
+        m = [(1 << 20) + it, 5000 + it, (2 << 20) - it, 131072 + 120 * it][it % 4]
+        root = (it * 3) % n
+        for r in range(n):
+            bufs[r][:m].fill_(it + 1 if r == root else 0)
+        B.bcast_all(comms, [b[:m] for b in bufs], m, "uint8", root, d)
+        torch.cuda.synchronize()
+        for r in range(n):
+            assert int(bufs[r][:m].min()) == it + 1 == int(bufs[r][:m].max()), (it, m, root, r)
+    for c in comms:
+        c.check()
+
+
 def test_provenance_matches_schedule_sends():
     """Schedule fidelity (test_runtime.cpp:121-161): every (src, dst, chunk)
     pull happened once and moved exactly the chunk's bytes."""
