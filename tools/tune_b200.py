@@ -32,6 +32,9 @@ ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--chunks", default="65536,131072,262144,524288,1048576,2097152,4194304")
 ap.add_argument("--cands", default="direct,knomial,scatter_ring_allgather,chain_pipelined")
 ap.add_argument("--raw", default="", help="also write every measurement (config, n, bytes, seconds) here")
+ap.add_argument("--b2b", type=int, default=1,
+                help="cost = mean of this many calls issued back to back (what a training step issues; resolves "
+                     "differences below the ~2 us event tick); 1 = single gated calls")
 a = ap.parse_args()
 
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -74,13 +77,14 @@ def cost(cfg, n, m):
         comm.barrier(stream)
         ev0.record(stream)
         try:
-            comm.bcast(buf, m, "uint8", 0, cfg, stream=stream)
+            for _ in range(a.b2b if m <= (16 << 20) else 1):
+                comm.bcast(buf, m, "uint8", 0, cfg, stream=stream)
         except Exception as e:
             raise RuntimeError(f"bcast {cfg} M={m} protocol={proto_now[0]} failed: {e}") from e
         ev1.record(stream)
         ev1.synchronize()
         if it >= 2:
-            times.append(ev0.elapsed_time(ev1) * 1e-3)
+            times.append(ev0.elapsed_time(ev1) * 1e-3 / (a.b2b if m <= (16 << 20) else 1))
     t = torch.tensor(times, dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     med = float(statistics.median(t.cpu().tolist()))
@@ -108,7 +112,8 @@ chunks = [int(x) for x in a.chunks.split(",")]
 t0 = time.time()
 table = B.tune_measured([world], sizes, cands, chunks, cost,
                         provenance=f"B200 x{world}, NVLink (LL128 lines, P2P pulls or pushes per rule), median of {a.iters}-{4 * a.iters} "
-                                   f"device-timed runs (max over ranks, 2 significant digits), "
+                                   f"device-timed runs (max over ranks, 2 significant digits"
+                                   f"{f'; mean of {a.b2b} back-to-back calls up to 16 MiB' if a.b2b > 1 else ''}), "
                                    f"{time.strftime('%Y-%m-%d')}")
 comm.check(stream)
 
