@@ -197,8 +197,9 @@ bcl_status_t bcl_comm_init_rank(int n, int rank, int device, size_t heap_bytes,
  *                  ranks sharing a GPU;  ll128_max, ll_chain_max, ll_max caps
  *   ll128_direct_min  `direct` calls from this size up to ll_max travel as
  *                  128-byte LL128 lines (every rank on its own GPU; 0 off,
- *                  without their landing areas either; default 131072;
- *                  grouped calls stay on fused 16-byte LL lines)
+ *                  without their landing areas either; default 131072; a
+ *                  group's `direct` run holding such a call travels on
+ *                  fused LL128 lines)
  *   nvls           NVLS multicast team: -1 auto (ranks on two or more GPUs with
  *                  multicast support), 0 off, 1 required (init fails without);
  *                  nvls_strict 1: system-scope fence before every counter bump

@@ -789,8 +789,8 @@ bool Group::use_nvls(const CallPlan& p, std::uint64_t bytes) const {
 // LL128 lines for the `direct` schedule: every rank on its own GPU (or, with
 // the ll128=1 option, ranks sharing one: the cross-GPU kernel through L2, one
 // cooperative launch), from d128_min_ up to the LL threshold, whatever the
-// protocol (like the 16-byte LL direct lines it replaces there). Inside a group such calls stay on
-// fused 16-byte LL lines (fuse_kind): one launch for many small messages.
+// protocol (like the 16-byte LL direct lines it replaces there). In a group
+// the run carries every member on LL128 direct lines (fuse_kind).
 bool Group::use_ll128_direct(const CallPlan& p, std::uint64_t bytes) const {
   if (!d128_min_ || !ll128_ok_ || !opt_.ll) return false;
   return p.config.algorithm == Algorithm::Direct && bytes >= d128_min_ && bytes <= ll_max_;
@@ -1351,7 +1351,9 @@ bool Group::defer(Deferred d) {
   return true;
 }
 
-// The line protocol a call takes (1 LL direct, 2 LL chain, 3 LL128 chain),
+// The line protocol a call takes (1 LL direct, 2 LL128 direct, 3 LL chain,
+// 4 LL128 chain: a run travels on its highest member's; mode_of_kind maps
+// them to launch_ll_segs modes),
 // or 0 when it cannot be fused -- the decisions of launch_group.
 int Group::fuse_kind(const Deferred& d) {
   const CallPlan& p = d.plan;
@@ -1362,16 +1364,15 @@ int Group::fuse_kind(const Deferred& d) {
     locals.push_back(d.li);
   }
   if (use_nvls(p, d.bytes)) return 0;
-  // (LL128 direct calls too: grouped small messages are launch-bound, one
-  // fused launch of 16-byte lines beats a launch each)
+  if (use_ll128_direct(p, d.bytes)) return 2;
   if (p.config.algorithm == Algorithm::Direct && d.bytes <= ll_max_ && opt_.ll) return 1;
   const int mode = ll_chain_mode(p, d.bytes, locals);
-  if (mode == 1) return 2;
+  if (mode == 1) return 3;
   if (mode == 2) {
     for (const auto& kv : by_device_) {
-      if (kv.second.size() > 1) return 0;  // no fused LL128 for ranks sharing a GPU
+      if (kv.second.size() > 1) return 0;  // no fused LL128 chain for ranks sharing a GPU
     }
-    return 3;
+    return 4;
   }
   return 0;
 }
@@ -1400,9 +1401,12 @@ void Group::flush_deferred() {
       for (const auto& kv : by_device_) per_dev = std::max(per_dev, static_cast<int>(kv.second.size()));
       const std::size_t max_segs = static_cast<std::size_t>(dev::max_segs(d.all ? per_dev : 1));
       auto fits = [&](std::size_t end, int k) {
-        const std::uint64_t cap = k == 1 ? ll_max_ / 8 : k == 2 ? ll_chain_max_ / 8 : (1ull << 31) - 1;
+        const std::uint64_t cap = k == 1   ? ll_max_ / 8
+                                  : k == 2 ? d128_lines()
+                                  : k == 3 ? ll_chain_max_ / 8
+                                           : (1ull << 31) - 1;
         std::uint64_t lines = 0;
-        for (std::size_t c = i; c < end; ++c) lines += ll_lines_of(calls[c].bytes, k - 1);
+        for (std::size_t c = i; c < end; ++c) lines += ll_lines_of(calls[c].bytes, mode_of_kind(k));
         return lines <= cap;
       };
       while (j < calls.size() && j - i < max_segs) {
@@ -1442,12 +1446,12 @@ void Group::flush_deferred() {
             for (int li : kv.second) b.push_back(calls[c].bufs[static_cast<std::size_t>(li)]);
             seg_bufs.push_back(std::move(b));
           }
-          launch_ll_segs(kv.second, seg_bufs, seg_bytes, d.root, d.streams[k++], kind - 1);
+          launch_ll_segs(kv.second, seg_bufs, seg_bytes, d.root, d.streams[k++], mode_of_kind(kind));
         }
       } else {
         std::vector<std::vector<void*>> seg_bufs;
         for (std::size_t c = i; c < j; ++c) seg_bufs.push_back({calls[c].bufs.front()});
-        launch_ll_segs({d.li}, seg_bufs, seg_bytes, d.root, d.streams.front(), kind - 1);
+        launch_ll_segs({d.li}, seg_bufs, seg_bytes, d.root, d.streams.front(), mode_of_kind(kind));
       }
     }
     i = j;

@@ -267,6 +267,7 @@ class Group {
   };
   bool defer(Deferred d);
   int fuse_kind(const Deferred& d);
+  static int mode_of_kind(int kind) { return kind == 1 ? 0 : kind == 2 ? 3 : kind == 3 ? 1 : 2; }
   void flush_deferred();
   std::vector<Deferred> deferred_;
   void alloc_rank(LocalRank& r, std::size_t heap_bytes);

@@ -1319,8 +1319,8 @@ __global__ void __launch_bounds__(kLLThreads, NL == 1 ? 3 : 2) ll128_kernel(cons
 // direct ones (a half is reused once its receivers credited the last call of
 // either format that wrote it). One call's lines fit the area: no ring, no
 // co-residency needed.
-template <int NL>
-__global__ void __launch_bounds__(kLLThreads) ll128_direct_kernel(const __grid_constant__ LLParamsT<NL, 1> P) {
+template <int NL, int NS>
+__global__ void __launch_bounds__(kLLThreads) ll128_direct_kernel(const __grid_constant__ LLParamsT<NL, NS> P) {
   pdl_wait();
   const int li = NL == 1 ? 0 : static_cast<int>(blockIdx.x) / P.ctas;
   const LLRank& R = P.ranks[li];
@@ -1338,11 +1338,13 @@ __global__ void __launch_bounds__(kLLThreads) ll128_direct_kernel(const __grid_c
   const int n = P.n_ranks;
   const bool root = R.rank == P.root;
   const std::size_t area = P.d128_area + (static_cast<std::size_t>(P.root) * 2 + half) * P.d128_lines * 8;
-  const bool aligned = (reinterpret_cast<std::uintptr_t>(R.buf) & 7u) == 0;
-  auto piece = [&](std::uint32_t line, std::uint64_t* off, std::uint32_t* len0, std::uint32_t* len1) {
+  // (a group's messages are segments: a line belongs to one, its payload
+  // offset counts from the segment's first line)
+  auto piece = [&](std::uint32_t line, std::uint64_t bytes, std::uint64_t* off, std::uint32_t* len0,
+                   std::uint32_t* len1) {
     *off = static_cast<std::uint64_t>(line) * kLL128Payload + static_cast<std::uint64_t>(part) * 16;
     const std::uint64_t end = static_cast<std::uint64_t>(line) * kLL128Payload + kLL128Payload;
-    const std::uint64_t lim = end < P.bytes ? end : P.bytes;
+    const std::uint64_t lim = end < bytes ? end : bytes;
     auto clip = [&](std::uint64_t a) -> std::uint32_t { return a >= lim ? 0u : static_cast<std::uint32_t>(lim - a < 8 ? lim - a : 8); };
     *len0 = clip(*off);
     *len1 = part == 7 ? 0u : clip(*off + 8);
@@ -1366,11 +1368,13 @@ __global__ void __launch_bounds__(kLLThreads) ll128_direct_kernel(const __grid_c
     for (std::uint32_t g = warp; g * 4 < P.lines; g += warps) {
       const std::uint32_t line = g * 4 + sub;
       if (line >= P.lines) continue;
+      const LineSeg sg = seg_of(P, li, line);
+      const bool aligned = (reinterpret_cast<std::uintptr_t>(sg.buf) & 7u) == 0;
       std::uint64_t off;
       std::uint32_t l0, l1;
-      piece(line, &off, &l0, &l1);
-      const unsigned long long a = ll128_get(R.buf, off, l0, aligned);
-      const unsigned long long b = part == 7 ? epoch : ll128_get(R.buf, off + 8, l1, aligned);
+      piece(line - sg.line0, sg.bytes, &off, &l0, &l1);
+      const unsigned long long a = ll128_get(sg.buf, off, l0, aligned);
+      const unsigned long long b = part == 7 ? epoch : ll128_get(sg.buf, off + 8, l1, aligned);
       const std::size_t at = area + static_cast<std::size_t>(line) * 8 + part;
       for (int d = 0; d < n; ++d) {
         if (d != P.root) st_volatile_v2u64(reinterpret_cast<ulonglong2*>(R.peers->ll[d] + at), a, b);
@@ -1400,11 +1404,13 @@ __global__ void __launch_bounds__(kLLThreads) ll128_direct_kernel(const __grid_c
       }
       if (!ok) break;
       if (active) {
+        const LineSeg sg = seg_of(P, li, line);
+        const bool aligned = (reinterpret_cast<std::uintptr_t>(sg.buf) & 7u) == 0;
         std::uint64_t off;
         std::uint32_t l0, l1;
-        piece(line, &off, &l0, &l1);
-        ll128_put(R.buf, off, l0, aligned, v.x);
-        if (part != 7) ll128_put(R.buf, off + 8, l1, aligned, v.y);
+        piece(line - sg.line0, sg.bytes, &off, &l0, &l1);
+        ll128_put(sg.buf, off, l0, aligned, v.x);
+        if (part != 7) ll128_put(sg.buf, off + 8, l1, aligned, v.y);
       }
     }
   }
@@ -1606,10 +1612,7 @@ int launch_ll_as(cudaLaunchConfig_t& cfg, const dev::LLParams& p) {
     q.ranks[i] = p.ranks[i];
     for (int s = 0; s < NS && s < p.n_seg; ++s) q.seg_buf[i][s] = p.seg_buf[i][s];
   }
-  if (p.chain == 3) {  // LL128 direct: one message per launch
-    if constexpr (NS > 1) return static_cast<int>(cudaErrorInvalidValue);
-    else return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::ll128_direct_kernel<NL>, q));
-  }
+  if (p.chain == 3) return static_cast<int>(cudaLaunchKernelEx(&cfg, dev::ll128_direct_kernel<NL, NS>, q));
   if (p.chain == 2) {
     // (LL128 groups are not fused for ranks sharing a GPU: the 16-rank fused
     // block would spill at LL128's 42-register budget; the host never asks.)

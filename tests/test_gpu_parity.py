@@ -579,6 +579,30 @@ def test_group_fuses_line_protocol_calls():
             c.set_protocol("auto")
 
 
+@pytest.mark.parametrize("n", [2, 4])
+def test_group_fuses_ll128_direct_lines(n):
+    """A group whose `direct` run holds a message >= ll128_direct_min travels
+    on LL128 direct lines, every member a segment (small and large, odd
+    sizes, misaligned, an empty one): one launch per run, bit-exact; a run of
+    small messages only stays on 16-byte LL lines."""
+    comms = comms_for(n, VARIANTS["ll128"][0])
+    bufs = [torch.zeros(4 << 20, dtype=torch.uint8, device="cuda:0") for _ in range(n)]
+    rng = random.Random(5 + n)
+    sizes = [1, 119, 120, 121, 300000, 0, 4096 + 7, 131072]  # (ranks sharing a GPU: <= 8 messages per launch)
+    before = comms[0].launches
+    _grouped_round(comms, bufs, sizes, n - 1, "direct", offs=[rng.randrange(0, 8) for _ in sizes])
+    assert comms[0].launches - before == 1
+    before = comms[0].launches
+    _grouped_round(comms, bufs, [(700 << 10) + 3, 5, (900 << 10) + 1], 0, "direct", offs=[3, 0, 1])
+    assert comms[0].launches - before == 1
+    # beyond the LL128 direct area (~2 MiB of lines): the run splits
+    before = comms[0].launches
+    _grouped_round(comms, bufs, [(1 << 20) + 9, (1 << 20) + 11, 1000], 1 % n, "direct")
+    assert comms[0].launches - before == 2
+    for c in comms:
+        c.check()
+
+
 def test_group_rules():
     comms = comms_for(2)
     buf = [torch.zeros(64, dtype=torch.uint8, device="cuda:0") for _ in comms]

@@ -126,7 +126,7 @@ def test_ll128_direct_lines():
     credits): sizes around both thresholds and the 120-byte line payload,
     every root, misaligned views, the two formats interleaved back to back on
     the same halves (each result checked before the next call), a grouped run
-    (every message on fused 16-byte LL lines)."""
+    (fused LL128 direct lines with the small members as segments)."""
     devices = list(range(min(ngpu(), 8)))
     n = len(devices)
     comms = B.Comm.local(devices, timeout_s=10, ll128_direct_min=65536)
