@@ -109,6 +109,7 @@ void set_option(GroupOptions& o, const std::string& key, const std::string& v) {
   else if (key == "ll128_coop") o.ll128_coop = i32() != 0;
   else if (key == "ll128_ctas") o.ll128_ctas = std::clamp(i32(), 0, dev::kLL128MaxCtas);
   else if (key == "ll128_direct_min") o.ll128_direct_min = u64();
+  else if (key == "ll128_direct_ctas") o.ll128_direct_ctas = std::clamp(i32(), 0, 1024);
   else if (key == "protocol") {
     o.protocol = i32();
     if (o.protocol < 0 || o.protocol > 5) throw std::invalid_argument("protocol must be 0..5");
@@ -133,7 +134,7 @@ void set_option(GroupOptions& o, const std::string& key, const std::string& v) {
 
 constexpr const char* kOptionNames[] = {
     "poll_ns", "window_bytes", "min_slice", "max_ctas", "strict_sys", "sys_scope", "eager_post", "writer_fence",
-    "local_fused", "local_ctas", "local_item", "local_claim", "ll", "ll128", "ll128_coop", "ll128_ctas", "ll128_direct_min", "protocol", "ll_max", "ll_chain_max", "ll128_max",
+    "local_fused", "local_ctas", "local_item", "local_claim", "ll", "ll128", "ll128_coop", "ll128_ctas", "ll128_direct_min", "ll128_direct_ctas", "protocol", "ll_max", "ll_chain_max", "ll128_max",
     "host_piece", "stages", "stage_bytes", "nvls", "nvls_strict", "nvls_slot", "nvls_ctas", "nvls_ll_max"};
 
 }  // namespace
@@ -1155,7 +1156,9 @@ void Group::launch_ll_segs(const std::vector<int>& locals, const std::vector<std
   }
   if (mode == 3) {  // LL128 direct: a warp moves 4 lines per step, ~2 steps per warp; no co-residency needed
     const std::uint32_t per_cta = dev::kLLThreads / 32 * 4 * 2;
-    P.ctas = std::clamp<int>(static_cast<int>((P.lines + per_cta - 1) / per_cta), 1, dev::kLLMaxCtas);
+    int cap = opt_.ll128_direct_ctas > 0 ? opt_.ll128_direct_ctas : sms_;
+    if (P.n_local > 1) cap = std::min(cap, resident);  // (ranks sharing a GPU: one cooperative launch)
+    P.ctas = std::clamp<int>(static_cast<int>((P.lines + per_cta - 1) / per_cta), 1, cap);
   }
   P.timeout_ns = opt_.timeout_ns;
   P.coop = opt_.ll128_coop ? 1 : 0;

@@ -107,6 +107,8 @@ struct GroupOptions {
                                                             // travel as 128-byte LL128 lines (every rank on its own
                                                             // GPU; 0 = never, no landing areas for them either):
                                                             // n = 4, 8 back to back, 1 MiB: 11.4 vs 15.4 us
+  int ll128_direct_ctas = 0;                                // its CTAs per rank cap (0 = one per SM: n = 2, 1 MiB,
+                                                            // 8 back to back 7.9 vs 8.4 us with 64)
   int protocol = 0;                                         // chain: 0 auto (table), 1 pull, 2 push
   std::uint64_t ll_max_bytes = 0;                           // LL threshold (0 = 2 MiB, lowered for many ranks)
   std::int64_t ll_chain_max_bytes = -1;                     // LL pipelined chain up to this size (-1 = default)
