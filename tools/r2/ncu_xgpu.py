@@ -14,7 +14,11 @@ kernels complete. NVLS below the 64 MiB ring never waits at the root either
 copies its copy out). Without ncu both kernels run concurrently and the call
 succeeds; the receiver's buffer is verified either way.
 
-  python tools/r2/ncu_xgpu.py pull|ll128|pull_vec|nvls BYTES [--timeout S]
+`direct128` / `direct_ll`: the `direct` schedule on LL128 direct lines / on
+16-byte LL lines (ll128_direct_min=0), BYTES <= 2 MiB; the root never waits
+on a first call, so both kernels complete under ncu too.
+
+  python tools/r2/ncu_xgpu.py pull|ll128|pull_vec|nvls|direct128|direct_ll BYTES [--timeout S]
 """
 import argparse
 import os
@@ -27,12 +31,12 @@ import paper_1707_09414_b200 as B  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=["pull", "ll128", "pull_vec", "nvls"])
+    ap.add_argument("mode", choices=["pull", "ll128", "pull_vec", "nvls", "direct128", "direct_ll"])
     ap.add_argument("bytes", type=int)
     ap.add_argument("--chunk", type=int, default=65536)
     ap.add_argument("--timeout", type=float, default=3.0)
     args = ap.parse_args()
-    opts = {"stage_bytes": 0} if args.mode == "pull_vec" else {}
+    opts = {"stage_bytes": 0} if args.mode == "pull_vec" else {"ll128_direct_min": 0} if args.mode == "direct_ll" else {}
     comms = B.Comm.local([0, 1], timeout_s=args.timeout, **opts)
     for c in comms:
         c.set_protocol({"ll128": "ll128", "nvls": "nvls"}.get(args.mode, "pull"))
@@ -42,6 +46,11 @@ def main():
                                 generator=torch.Generator(device="cuda:0").manual_seed(3)))
     torch.cuda.synchronize(0)
     cfg = B.AlgorithmConfig(B.Algorithm.chain_pipelined, 0, args.chunk)
+    if args.mode.startswith("direct"):
+        for c in comms:
+            c.set_protocol("auto")
+        cfg = B.AlgorithmConfig(B.Algorithm.direct, 0, 0)
+        print("path:", comms[0].path(m, cfg))
     B.bcast_all(comms, bufs, m, "uint8", 0, cfg)
     status = []
     for r, c in enumerate(comms):
