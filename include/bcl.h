@@ -238,7 +238,7 @@ bcl_status_t bcl_comm_set_table(bcl_comm_t c, bcl_table_t t);
 bcl_status_t bcl_comm_plan(bcl_comm_t c, const bcl_config_t* config, int root, uint64_t bytes, int* slices,
                            uint64_t* slice_bytes, uint32_t* n_chunks, int* ctas);
 /* The device path a call of this shape would run (config NULL = tuned), as
- * text: "ll_kernel/direct", "ll_kernel/chain", "ll128_kernel",
+ * text: "ll_kernel/direct", "ll128_kernel/direct", "ll_kernel/chain", "ll128_kernel",
  * "local_chain_kernel", "bcast_kernel/pull[/tma]", "bcast_kernel/push[/tma]",
  * "bcast_kernel/events", "nvls_kernel" or "none"; *len = bytes needed incl. NUL. */
 bcl_status_t bcl_comm_path(bcl_comm_t c, const bcl_config_t* config, int root, uint64_t bytes, char* out,
