@@ -240,7 +240,7 @@ bcl_status_t bcl_comm_plan(bcl_comm_t c, const bcl_config_t* config, int root, u
 /* The device path a call of this shape would run (config NULL = tuned), as
  * text: "ll_kernel/direct", "ll128_kernel/direct", "ll_kernel/chain", "ll128_kernel",
  * "local_chain_kernel", "bcast_kernel/pull[/tma]", "bcast_kernel/push[/tma]",
- * "bcast_kernel/events", "nvls_kernel" or "none"; *len = bytes needed incl. NUL. */
+ * "bcast_kernel/events", "nvls_kernel", "nvls_ll_kernel" or "none"; *len = bytes needed incl. NUL. */
 bcl_status_t bcl_comm_path(bcl_comm_t c, const bcl_config_t* config, int root, uint64_t bytes, char* out,
                            size_t cap, size_t* len);
 /* Pipelined-chain transport protocol: 0 auto (line protocols where the
