@@ -260,6 +260,7 @@ def _ipc_worker(rank, world, port, q):
                                               ("chain_pipelined", (5 << 20) + 3, world - 1),
                                               ("chain_pipelined", 8 << 20, 1 % world),
                                               ("direct", 1 << 20, world - 1),
+                                              ("direct", 2 << 20, 0), ("direct", (128 << 10) + 5, 1 % world),
                                               ("chain_pipelined", (3 << 20) + 1, 0)]):
             payload = O.payload(it, m)
             if rank == root:
