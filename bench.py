@@ -397,7 +397,7 @@ def bench_single(args, torch):
 
     # e2e through the C-ABI with pinned host buffers (run_bcast_host).
     hosts = [torch.empty(m, dtype=torch.uint8, pin_memory=True) for _ in range(n)]
-    hosts[0].copy_(bufs[0].cpu())
+    hosts[0].copy_(bufs[0])  # by DMA: no CPU-cached lines for the H2D to snoop (HOST_RESET_NOTE)
     zeros = torch.zeros(m, dtype=torch.uint8, device=dev)
     check = torch.empty(m, dtype=torch.uint8, device=dev)
 
@@ -547,13 +547,12 @@ def bench_multi(args, torch, rank, world):
 
     # e2e through the C-ABI with pinned host buffers (bcl_bcast_host)
     host = torch.empty(m, dtype=torch.uint8, pin_memory=True)
-    ref_host = ref_all[:m].cpu()
     e2e = []
     zeros = torch.zeros(m, dtype=torch.uint8, device=dev)
     chk = torch.empty(m, dtype=torch.uint8, device=dev)
     for it in range(args.warmup + max(3, args.steps // 2)):
-        if rank == 0:
-            host.copy_(ref_host)
+        if rank == 0:  # the root's payload lands in its host buffer by DMA too (HOST_RESET_NOTE)
+            host.copy_(ref_all[:m])
         else:
             host_reset(host, zeros)
         dist.barrier(device_ids=[local])

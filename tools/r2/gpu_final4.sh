@@ -7,4 +7,3 @@ CUDA_VISIBLE_DEVICES=0 timeout 900 python -m pytest tests -q -m gpu > $OUT/pytes
 echo "pytest 1gpu rc=$? $(tail -1 $OUT/pytest_gpu_1gpu.log)"
 CUDA_VISIBLE_DEVICES=0 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_1gpu.log 2>&1
 echo "smoke rc=$? $(tail -1 $OUT/smoke_1gpu.log)"
-timeout 300 python tools/r2/pcie_topo_probe.py > $OUT/pcie_topo.txt 2>&1; cat $OUT/pcie_topo.txt
