@@ -209,7 +209,11 @@ class AlgorithmConfig:
     chunk_bytes: int = 0
 
     def _c(self):
-        return _Config(int(self.algorithm), self.radix_k, self.chunk_bytes)
+        c = self.__dict__.get("_cached")  # (immutable: built once, passed by reference on every call)
+        if c is None:
+            c = _Config(int(self.algorithm), self.radix_k, self.chunk_bytes)
+            object.__setattr__(self, "_cached", c)
+        return c
 
     @staticmethod
     def _from(c):

@@ -211,9 +211,12 @@ class Comm:
     # ---------------------------------------------------------- data plane
     def bcast(self, buf, count: int, dtype="uint8", root: int = 0,
               config: Optional[AlgorithmConfig] = None, stream=None) -> None:
-        """bcast(buf, count, dtype, root, comm): enqueued on `stream`."""
-        _check(lib().bcl_bcast(C.c_void_p(_ptr(buf)), count, _dtype(dtype), root, self._h, _cfg(config),
-                               C.c_void_p(_stream(stream))))
+        """bcast(buf, count, dtype, root, comm): enqueued on `stream`. (The
+        per-call path is kept lean: a training step issues one per tensor.)"""
+        status = lib().bcl_bcast(_ptr(buf), count, _dtype(dtype), root, self._h,
+                                 None if config is None else C.byref(config._c()), _stream(stream))
+        if status:
+            _check(status)
 
     def bcast_host(self, host_buf, count: int, dtype="uint8", root: int = 0,
                    config: Optional[AlgorithmConfig] = None, stream=None) -> None:

@@ -51,12 +51,18 @@ class DeviceScope {
  public:
   explicit DeviceScope(int dev) {
     cudaGetDevice(&saved_);
-    if (dev != saved_) ck(cudaSetDevice(dev), "cudaSetDevice");
+    if (dev != saved_) {
+      ck(cudaSetDevice(dev), "cudaSetDevice");
+      switched_ = true;
+    }
   }
-  ~DeviceScope() { cudaSetDevice(saved_); }
+  ~DeviceScope() {
+    if (switched_) cudaSetDevice(saved_);
+  }
 
  private:
   int saved_{0};
+  bool switched_{false};
 };
 
 std::string describe(const dev::ErrorRecord& e) {
@@ -969,12 +975,12 @@ AlgorithmConfig Group::choose(std::uint64_t bytes, const AlgorithmConfig* cfg) c
 
 // ------------------------------------------------------------------ plans
 
-CallPlan Group::plan(const AlgorithmConfig& cfg, int root, std::uint64_t bytes) {
+std::shared_ptr<const CallPlan> Group::plan_ptr(const AlgorithmConfig& cfg, int root, std::uint64_t bytes) {
   const auto key = std::make_tuple(static_cast<int>(cfg.algorithm), cfg.radix_k, cfg.chunk_bytes, root, bytes);
   {
     std::lock_guard<std::mutex> lock(plan_mu_);
     auto it = plans_.find(key);
-    if (it != plans_.end()) return *it->second;
+    if (it != plans_.end()) return it->second;
   }
   cfg.validate();
   auto p = std::make_shared<CallPlan>();
@@ -1052,7 +1058,7 @@ CallPlan Group::plan(const AlgorithmConfig& cfg, int root, std::uint64_t bytes) 
   std::lock_guard<std::mutex> lock(plan_mu_);
   if (plans_.size() > 256) plans_.clear();
   plans_[key] = p;
-  return *p;
+  return p;
 }
 
 // ---------------------------------------------------------------- launches
@@ -1193,7 +1199,8 @@ void Group::launch_ll_segs(const std::vector<int>& locals, const std::vector<std
 // launch_group, on state every rank shares).
 std::string Group::path(const AlgorithmConfig* cfg, int root, std::uint64_t bytes) {
   const AlgorithmConfig c = choose(bytes, cfg);
-  const CallPlan p = plan(c, root, bytes);
+  const auto pp = plan_ptr(c, root, bytes);
+  const CallPlan& p = *pp;
   if (n_ == 1) return "none";
   std::vector<int> locals;
   for (int i = 0; i < local_count(); ++i) locals.push_back(i);
@@ -1283,9 +1290,10 @@ void Group::bcast(int li, void* buf, std::uint64_t bytes, int root, const Algori
   // (Per-process ranks: line protocols take any device buffer; the lane
   // executor needs heap or registered buffers, checked in fill_rank_work.)
   const AlgorithmConfig c = choose(bytes, cfg);
-  const CallPlan p = plan(c, root, bytes);
+  const auto pp = plan_ptr(c, root, bytes);
+  const CallPlan& p = *pp;
   if (n_ == 1) return;  // nothing moves (reference: n = 1 leaves the buffer untouched)
-  if (defer(Deferred{false, li, {buf}, bytes, root, p, {stream}, opt_.protocol})) return;
+  if (defer(Deferred{false, li, {buf}, bytes, root, pp, {stream}, opt_.protocol})) return;
   launch_group({li}, {buf}, bytes, root, p, stream);
 }
 
@@ -1301,7 +1309,8 @@ void Group::bcast_all(const std::vector<void*>& bufs, std::uint64_t bytes, int r
     if (bytes > 0 && b == nullptr) throw std::invalid_argument("null buffer");
   }
   const AlgorithmConfig c = choose(bytes, cfg);
-  const CallPlan p = plan(c, root, bytes);
+  const auto pp = plan_ptr(c, root, bytes);
+  const CallPlan& p = *pp;
   if (n_ == 1) return;
   std::vector<cudaStream_t> per;  // per device, first rank's stream
   for (const auto& kv : by_device_) {
@@ -1309,7 +1318,7 @@ void Group::bcast_all(const std::vector<void*>& bufs, std::uint64_t bytes, int r
     per.push_back(streams.empty() ? local_[static_cast<std::size_t>(first)].stream
                                   : streams[static_cast<std::size_t>(first)]);
   }
-  if (defer(Deferred{true, -1, bufs, bytes, root, p, per, opt_.protocol})) return;
+  if (defer(Deferred{true, -1, bufs, bytes, root, pp, per, opt_.protocol})) return;
   std::size_t d = 0;
   for (const auto& kv : by_device_) {
     std::vector<void*> b;
@@ -1359,7 +1368,7 @@ bool Group::defer(Deferred d) {
 // them to launch_ll_segs modes),
 // or 0 when it cannot be fused -- the decisions of launch_group.
 int Group::fuse_kind(const Deferred& d) {
-  const CallPlan& p = d.plan;
+  const CallPlan& p = *d.plan;
   std::vector<int> locals;
   if (d.all) {
     for (int i = 0; i < local_count(); ++i) locals.push_back(i);
@@ -1432,10 +1441,10 @@ void Group::flush_deferred() {
         for (const auto& kv : by_device_) {
           std::vector<void*> b;
           for (int li : kv.second) b.push_back(d.bufs[static_cast<std::size_t>(li)]);
-          launch_group(kv.second, b, d.bytes, d.root, d.plan, d.streams[k++]);
+          launch_group(kv.second, b, d.bytes, d.root, *d.plan, d.streams[k++]);
         }
       } else {
-        launch_group({d.li}, d.bufs, d.bytes, d.root, d.plan, d.streams.front());
+        launch_group({d.li}, d.bufs, d.bytes, d.root, *d.plan, d.streams.front());
       }
     } else {
       std::vector<std::uint64_t> seg_bytes;

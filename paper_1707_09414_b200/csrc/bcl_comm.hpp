@@ -224,7 +224,10 @@ class Group {
   void clear_table();
   const TuningTable& table() const;
   AlgorithmConfig choose(std::uint64_t bytes, const AlgorithmConfig* cfg) const;
-  CallPlan plan(const AlgorithmConfig& cfg, int root, std::uint64_t bytes);
+  CallPlan plan(const AlgorithmConfig& cfg, int root, std::uint64_t bytes) { return *plan_ptr(cfg, root, bytes); }
+  // The cached plan itself (shared: a call neither copies its event lists nor
+  // outlives it if connect() clears the cache).
+  std::shared_ptr<const CallPlan> plan_ptr(const AlgorithmConfig& cfg, int root, std::uint64_t bytes);
   // Name of the device path (kernel/protocol) a call of this shape runs.
   std::string path(const AlgorithmConfig* cfg, int root, std::uint64_t bytes);
 
@@ -263,7 +266,7 @@ class Group {
     std::vector<void*> bufs;            // bcast_all: one per local rank
     std::uint64_t bytes;
     int root;
-    CallPlan plan;
+    std::shared_ptr<const CallPlan> plan;
     std::vector<cudaStream_t> streams;  // bcast_all: one per device (by_device_ order)
     int protocol;                       // set_protocol in effect at the call
   };
