@@ -1317,8 +1317,8 @@ __global__ void __launch_bounds__(kLLThreads, NL == 1 ? 3 : 2) ll128_kernel(cons
 // and receivers poll their own copy line by line: half the root's egress of
 // 16-byte LL lines. The halves, the credits and the reuse rule are the LL
 // direct ones (a half is reused once its receivers credited the last call of
-// either format that wrote it). One call's lines fit the area: no ring, no
-// co-residency needed.
+// either format that wrote it). One launch's lines -- one call, or a group's
+// run of messages as segments -- fit the area: no ring, no co-residency needed.
 template <int NL, int NS>
 __global__ void __launch_bounds__(kLLThreads) ll128_direct_kernel(const __grid_constant__ LLParamsT<NL, NS> P) {
   pdl_wait();
