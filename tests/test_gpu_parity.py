@@ -403,6 +403,13 @@ def test_options_are_validated():
         B.Comm.local([0, 0], stage_bytes=8192, stages=4)
     with pytest.raises(ValueError, match="nvls_slot"):
         B.Comm.local([0, 0], nvls_slot=3000)
+    # LL128 direct: threshold and grid knobs; 0 turns the lines off, a threshold above the LL cap too
+    d = cfg_of("direct")
+    assert B.Comm.local([0, 0], ll128=1, ll128_direct_min=0)[0].path(1 << 20, d) == "ll_kernel/direct"
+    assert B.Comm.local([0, 0], ll128=1, ll128_direct_min=64 << 20)[0].path(2 << 20, d) == "ll_kernel/direct"
+    assert B.Comm.local([0, 0], ll128=1, ll128_direct_min=4096, ll128_direct_ctas=8)[0].path(4096, d) == \
+        "ll128_kernel/direct"
+    assert B.Comm.local([0, 0])[0].path(1 << 20, d) == "ll_kernel/direct"  # shared GPU without ll128=1
     comms = comms_for(2)  # ranks sharing a GPU: LL128 only with the ll128=1 option
     bufs = [torch.zeros(16, dtype=torch.uint8, device="cuda:0") for _ in comms]
     for c in comms:
