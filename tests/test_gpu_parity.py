@@ -407,8 +407,12 @@ def test_options_are_validated():
     d = cfg_of("direct")
     assert B.Comm.local([0, 0], ll128=1, ll128_direct_min=0)[0].path(1 << 20, d) == "ll_kernel/direct"
     assert B.Comm.local([0, 0], ll128=1, ll128_direct_min=64 << 20)[0].path(2 << 20, d) == "ll_kernel/direct"
-    assert B.Comm.local([0, 0], ll128=1, ll128_direct_min=4096, ll128_direct_ctas=8)[0].path(4096, d) == \
-        "ll128_kernel/direct"
+    small = B.Comm.local([0, 0], ll128=1, ll128_direct_min=4096, ll128_direct_ctas=8)
+    assert small[0].path(4096, d) == "ll128_kernel/direct"
+    bufs = [torch.full((100003,), 7 if r == 1 else 0, dtype=torch.uint8, device="cuda:0") for r in range(2)]
+    B.bcast_all(small, bufs, 100003, "uint8", 1, d)  # ~834 lines on 8 CTAs: every warp loops
+    torch.cuda.synchronize()
+    assert all(int(b.min()) == 7 == int(b.max()) for b in bufs)
     assert B.Comm.local([0, 0])[0].path(1 << 20, d) == "ll_kernel/direct"  # shared GPU without ll128=1
     comms = comms_for(2)  # ranks sharing a GPU: LL128 only with the ll128=1 option
     bufs = [torch.zeros(16, dtype=torch.uint8, device="cuda:0") for _ in comms]
