@@ -267,3 +267,19 @@ def test_group_calls_without_a_gpu():
         _lib._check(lib.bcl_group_end())
     with B.group():
         pass
+
+
+def test_config_struct_is_cached_and_value_semantics_hold():
+    """AlgorithmConfig builds its C struct once (the per-call binding passes
+    it by reference); equality, hashing, pickling and the struct's fields
+    still follow the three dataclass fields."""
+    import pickle
+    a = B.AlgorithmConfig(B.Algorithm.chain_pipelined, 0, 65536)
+    s1 = a._c()
+    assert a._c() is s1 and (s1.algorithm, s1.radix_k, s1.chunk_bytes) == (4, 0, 65536)
+    b = B.AlgorithmConfig.of("chain_pipelined", chunk_bytes=65536)
+    assert a == b and hash(a) == hash(b) and {a: 1}[b] == 1
+    c = pickle.loads(pickle.dumps(a))
+    assert c == a and c._c().chunk_bytes == 65536
+    assert B.AlgorithmConfig(B.Algorithm.knomial, 2, 0) != a
+    assert repr(a) == "AlgorithmConfig(algorithm=<Algorithm.chain_pipelined: 4>, radix_k=0, chunk_bytes=65536)"
