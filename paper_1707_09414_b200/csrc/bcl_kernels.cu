@@ -1116,6 +1116,22 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const __grid_constant__ 
   }
 }
 
+// Payload bytes thread `part` (0-7) of an LL128 line carries: line `line`
+// of a message of `bytes` bytes holds [line * 120, line * 120 + 120); the
+// thread moves [off, off + len0) as word 0 and [off + 8, off + 8 + len1) as
+// word 1 (part 7's word 1 is the flag).
+__device__ __forceinline__ void ll128_piece(int part, std::uint32_t line, std::uint64_t bytes, std::uint64_t* off,
+                                            std::uint32_t* len0, std::uint32_t* len1) {
+  *off = static_cast<std::uint64_t>(line) * kLL128Payload + static_cast<std::uint64_t>(part) * 16;
+  const std::uint64_t end = static_cast<std::uint64_t>(line) * kLL128Payload + kLL128Payload;
+  const std::uint64_t lim = end < bytes ? end : bytes;
+  auto clip = [&](std::uint64_t a) -> std::uint32_t {
+    return a >= lim ? 0u : static_cast<std::uint32_t>(lim - a < 8 ? lim - a : 8);
+  };
+  *len0 = clip(*off);
+  *len1 = part == 7 ? 0u : clip(*off + 8);
+}
+
 // LL128 pipelined chain. A 128-byte line carries 120 payload bytes and a flag
 // in its last 8 bytes; eight threads own one line (16 bytes each) and a warp
 // moves four lines (a "group") per instruction. Like NCCL's LL128 this relies
@@ -1189,15 +1205,7 @@ __global__ void __launch_bounds__(kLLThreads, NL == 1 ? 3 : 2) ll128_kernel(cons
   // rank's last CTA just advances the epoch at the end.)
   // `line` counts from its segment's first line; `bytes` = the segment's.
   auto piece = [&](std::uint32_t line, std::uint64_t bytes, std::uint64_t* off, std::uint32_t* len0,
-                   std::uint32_t* len1) {
-    // payload bytes of this thread: [off, off + len0) -> word 0, [off + 8, ... + len1) -> word 1
-    *off = static_cast<std::uint64_t>(line) * kLL128Payload + static_cast<std::uint64_t>(part) * 16;
-    const std::uint64_t end = static_cast<std::uint64_t>(line) * kLL128Payload + kLL128Payload;
-    const std::uint64_t lim = end < bytes ? end : bytes;
-    auto clip = [&](std::uint64_t a) -> std::uint32_t { return a >= lim ? 0u : static_cast<std::uint32_t>(lim - a < 8 ? lim - a : 8); };
-    *len0 = clip(*off);
-    *len1 = part == 7 ? 0u : clip(*off + 8);
-  };
+                   std::uint32_t* len1) { ll128_piece(part, line, bytes, off, len0, len1); };
   const ulonglong2* ring_self = reinterpret_cast<const ulonglong2*>(R.ll + P.chain128_area);
   ulonglong2* ring_next = writer ? reinterpret_cast<ulonglong2*>(R.peers->ll[next] + P.chain128_area) : nullptr;
   const std::uint64_t* my_credit = R.wcredit + warp;  // our successor's consumption of our groups
@@ -1341,14 +1349,7 @@ __global__ void __launch_bounds__(kLLThreads) ll128_direct_kernel(const __grid_c
   // (a group's messages are segments: a line belongs to one, its payload
   // offset counts from the segment's first line)
   auto piece = [&](std::uint32_t line, std::uint64_t bytes, std::uint64_t* off, std::uint32_t* len0,
-                   std::uint32_t* len1) {
-    *off = static_cast<std::uint64_t>(line) * kLL128Payload + static_cast<std::uint64_t>(part) * 16;
-    const std::uint64_t end = static_cast<std::uint64_t>(line) * kLL128Payload + kLL128Payload;
-    const std::uint64_t lim = end < bytes ? end : bytes;
-    auto clip = [&](std::uint64_t a) -> std::uint32_t { return a >= lim ? 0u : static_cast<std::uint32_t>(lim - a < 8 ? lim - a : 8); };
-    *len0 = clip(*off);
-    *len1 = part == 7 ? 0u : clip(*off + 8);
-  };
+                   std::uint32_t* len1) { ll128_piece(part, line, bytes, off, len0, len1); };
   if (root) {
     // The half was last written (LL or LL128 direct) in epoch need: its
     // receivers must have read it.
